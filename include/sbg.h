@@ -1,0 +1,162 @@
+/*
+ * sbg.h — C ABI of the B200-native SBCI sigma / update hot path (libsbg.so).
+ *
+ * This is the drop-in boundary for the reference's operator plugin API
+ * (/root/reference/proj/include/sbci/operator.hpp:19-48, fci/fci_operator.hpp:60-120) and its
+ * solver entry points (sbci1.hpp:526-579, sbci2.hpp:527-623). Plain pointers and sizes only:
+ * no C++ or torch types cross this line. Every call returns an error code; the message of the
+ * last failure on the calling thread is available from sbg_last_error().
+ *
+ *   SBG_OK            0
+ *   SBG_EINVAL        1   maps to std::invalid_argument in the reference (operator.hpp:26, sigma.hpp:92, ...)
+ *   SBG_ENONCONV      2   maps to sbci::NonConvergenceError (config.hpp:92-100); CLI exit code 2
+ *   SBG_EDEVICE       3   CUDA / NCCL failure (no reference equivalent; never silently downgraded)
+ *   SBG_ERUNTIME      4   maps to std::runtime_error (e.g. the determinant guard, fci_operator.hpp:107-109)
+ *
+ * Vectors crossing the ABI are dense, alpha-major (det = ia * n_beta_strings + ib,
+ * determinants.hpp:73), fp64, length sbg_dim(). Inside the library they live in HBM as padded
+ * row blocks; the padding never crosses the ABI.
+ */
+#ifndef SBG_H
+#define SBG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define SBG_OK 0
+#define SBG_EINVAL 1
+#define SBG_ENONCONV 2
+#define SBG_EDEVICE 3
+#define SBG_ERUNTIME 4
+
+typedef struct sbg_ctx sbg_ctx;
+
+/* One single-excitation table entry: a+_p a_q |source> = sign |target>.
+ * Mirrors sbci::fci::Excitation (fci/sigma.hpp:19-23) byte for byte (16 bytes). */
+typedef struct sbg_excitation {
+    uint16_t p, q;
+    uint32_t target;
+    double sign;
+} sbg_excitation;
+
+/* Mirrors sbci::SolverConfig (config.hpp:10-60); sbg_config_default() gives the reference defaults. */
+typedef struct sbg_config {
+    double eps0, r0, b_th, eps1, x_th1, x_th2, r1;
+    int32_t max_cycle;          /* 0 = method default (20 sbci1, 10 sbci2) */
+    int32_t hx_refresh_restarts;
+    int64_t t_max;
+    double lindep, clamp_delta;
+} sbg_config;
+
+/* Per-state and per-run results (ConvergedEigenpair sbci1.hpp:27-34, RunSummary trace.hpp:212-221). */
+#define SBG_MAX_ROOTS 64
+typedef struct sbg_stats {
+    int32_t nroots;
+    int32_t iterations[SBG_MAX_ROOTS];
+    int32_t restarts[SBG_MAX_ROOTS];
+    double final_residual[SBG_MAX_ROOTS];
+    uint64_t matvecs;
+    int64_t total_iterations;
+    int32_t total_restarts;
+    int32_t hx_refreshes;
+    int32_t peak_vectors;
+    double wall_time_s;
+    /* filled on SBG_ENONCONV (NonConvergenceError{state, best_energy, best_residual}) */
+    int32_t failed_state;
+    double best_energy, best_residual;
+    /* device-side accounting for the bench */
+    double sigma_seconds;       /* summed sigma time (CUDA events) */
+    uint64_t kernel_launches;   /* kernels launched by the library during the call */
+} sbg_stats;
+
+/* Per-iteration trace record (TraceRecord trace.hpp:22-44, sbci1 fields). */
+typedef struct sbg_trace_record {
+    int32_t state, t;
+    double energy, dE, res_norm, x_norm, kinetic;
+    uint64_t matvecs;
+    int32_t restart_reason; /* -1 none, else RestartReason (0 stall_small_b, 1 norm_out_of_range, 2 residual_blowup, 3 max_cycle) */
+    double b, c;
+} sbg_trace_record;
+typedef void (*sbg_trace_fn)(const sbg_trace_record* rec, void* user);
+
+/* ---- host-only helpers (no GPU needed) ---- */
+const char* sbg_last_error(void);
+const char* sbg_version(void);
+uint64_t sbg_binomial(int n, int k);                                  /* determinants.hpp:17-31 */
+int sbg_determinant_count(int norb, int n_alpha, int n_beta, uint64_t* out); /* determinants.hpp:33-37 */
+sbg_config sbg_config_default(void);                                  /* config.hpp:11-22 */
+int sbg_config_validate(const sbg_config* cfg);                       /* config.hpp:26-43 */
+/* BASELINE.json synthetic integrals (pinned generator). h1[norb^2], eri[norb^4]. */
+int sbg_synthetic_integrals(int norb, uint64_t seed, double offdiag_scale, double* h1, double* eri);
+/* alpha-string block owned by `rank` of `world` (SURVEY §8e partition). */
+int sbg_shard_range(int64_t n_alpha_strings, int rank, int world, int64_t* lo, int64_t* hi);
+int sbg_device_count(void);
+
+/* ---- operator (replaces as_operator + FciOperator, fci_operator.hpp:60-120) ----
+ * nelec/ms2 define the sector as in FciProblem (n_alpha = (nelec+ms2)/2). eri must hold all eight
+ * permutations (fcidump.hpp:53-65). max_det is the determinant guard (kDefaultDeterminantGuard =
+ * 5,000,000 in the reference); the guard message matches the reference's. */
+int sbg_create(int norb, int nelec, int ms2, double e_core, const double* h1, const double* eri,
+               int device, uint64_t max_det, sbg_ctx** out);
+/* Distributed variant: one rank per GPU, CI vector sharded by alpha-string blocks.
+ * nccl_unique_id points at the 128-byte ncclUniqueId created on rank 0 (world > 1). */
+int sbg_create_dist(int norb, int nelec, int ms2, double e_core, const double* h1, const double* eri,
+                    int device, uint64_t max_det, int rank, int world, const void* nccl_unique_id,
+                    sbg_ctx** out);
+int sbg_nccl_unique_id(void* out128);
+void sbg_destroy(sbg_ctx* ctx);
+
+int64_t sbg_dim(const sbg_ctx* ctx);                                 /* SymmetricOperator::dim */
+int sbg_sector(const sbg_ctx* ctx, int* norb, int* n_alpha, int* n_beta, int64_t* n_alpha_strings,
+               int64_t* n_beta_strings);
+int sbg_local_rows(const sbg_ctx* ctx, int64_t* lo, int64_t* hi);    /* alpha rows owned by this rank */
+/* Exact diagonal <D|H|D> (fci_operator.hpp:16-57), bit-identical to the reference. Host buffer, n_det. */
+int sbg_diagonal(sbg_ctx* ctx, double* out);
+/* Strings (u64[n_strings]) and link table (sbg_excitation[n_strings * L], row-major, reference order)
+ * of one spin channel (0 = alpha, 1 = beta). Either pointer may be NULL. */
+int sbg_table_sizes(const sbg_ctx* ctx, int spin, int64_t* n_strings, int64_t* row_len);
+int sbg_string_tables(sbg_ctx* ctx, int spin, uint64_t* strings, sbg_excitation* links);
+
+/* sigma = H x for nvec vectors (host buffers, each n_det). Counts nvec applications
+ * (SymmetricOperator::apply, operator.hpp:25-31). x and y may not alias. */
+int sbg_sigma(sbg_ctx* ctx, const double* x, double* y, int nvec);
+/* Same on dense device buffers (n_det each) on the given cudaStream_t (NULL = library stream).
+ * Inputs already resident in HBM; used by the bench's device-resident leg. */
+int sbg_sigma_device(sbg_ctx* ctx, const double* d_x, double* d_y, void* stream);
+/* Padded-layout device entry points (no pack/unpack), for the throughput bench:
+ * buffers of sbg_padded_len() doubles in the library's internal layout (local rows only). */
+int64_t sbg_padded_len(const sbg_ctx* ctx);
+int sbg_pack(sbg_ctx* ctx, const double* d_dense_full, double* d_padded_local, void* stream);
+int sbg_unpack(sbg_ctx* ctx, const double* d_padded_local, double* d_dense_local, void* stream);
+int sbg_sigma_padded(sbg_ctx* ctx, const double* d_x_padded_local, double* d_y_padded_local, void* stream);
+uint64_t sbg_apply_count(const sbg_ctx* ctx);
+void sbg_reset_apply_count(sbg_ctx* ctx);
+uint64_t sbg_kernel_launches(const sbg_ctx* ctx);
+/* Flop count of one sigma (algorithm actually executed), split by kernel. */
+int sbg_sigma_flops(const sbg_ctx* ctx, double* alpha_beta, double* same_spin, double* total);
+
+/* ---- solvers (drivers of sbci1.hpp:526-579 / sbci2.hpp:527-623 on device-resident vectors) ----
+ * method: 1 = SBCI1. energies[nroots] ascending; vectors (nullable) nroots x n_det host buffer,
+ * unit norm. trace may be NULL. */
+int sbg_solve(sbg_ctx* ctx, int method, int nroots, const sbg_config* cfg, double* energies,
+              double* vectors, sbg_stats* stats, sbg_trace_fn trace, void* trace_user);
+
+/* self test of the DMMA fragment layouts used by the sigma kernels (GPU) */
+int sbg_selftest(void);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SBG_H */

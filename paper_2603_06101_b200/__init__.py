@@ -1,0 +1,12 @@
+"""B200-native SBCI sigma/update hot path (arXiv 2603.06101) — drop-in for the reference's FCI
+operator and SBCI1 driver. Product path: libsbg.so (sm_100a CUDA kernels + C++ host driver),
+reached through the C ABI in include/sbg.h. No CPU fallback."""
+from .fci import (K_DEFAULT_DETERMINANT_GUARD, FciOperator, FciProblem, FcidumpError, as_operator, binomial,
+                  determinant_count, parse_fcidump, parse_fcidump_file, sigma_apply, synthetic_problem)
+from .solver import (ConvergedEigenpair, MultiStateResult, NonConvergenceError, RunSummary, SolverConfig,
+                     StateSummary, TraceRecord, solve_n_states_sbci1)
+
+__all__ = ["K_DEFAULT_DETERMINANT_GUARD", "FciOperator", "FciProblem", "FcidumpError", "as_operator", "binomial",
+           "determinant_count", "parse_fcidump", "parse_fcidump_file", "sigma_apply", "synthetic_problem",
+           "ConvergedEigenpair", "MultiStateResult", "NonConvergenceError", "RunSummary", "SolverConfig",
+           "StateSummary", "TraceRecord", "solve_n_states_sbci1"]

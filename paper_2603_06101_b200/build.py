@@ -1,0 +1,67 @@
+"""Builds the product library paper_2603_06101_b200/libsbg.so (sm_100a only) with nvcc.
+
+    python -m paper_2603_06101_b200.build [--verbose-ptxas]
+
+Objects go to build/ (git-ignored); the .so lands in-tree next to this file so it travels to the
+GPU box with the repo snapshot. tables.cu is compiled with --fmad=false (bit-exact diagonal).
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+OBJ = os.path.join(ROOT, "build", "sbg")
+LIB = os.path.join(PKG, "libsbg.so")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
+         "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
+SOURCES = ["tables.cu", "sigma_ab.cu", "sigma_ss.cu", "vec.cu", "selftest.cu", "context.cu", "solver.cu", "api.cu"]
+PER_FILE = {"tables.cu": ["--fmad=false"]}
+
+
+def nvcc():
+    for c in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
+        if c and os.path.exists(c):
+            return c
+    raise RuntimeError("nvcc not found")
+
+
+def _compile(src, ptxas_verbose):
+    out = os.path.join(OBJ, src.replace(".cu", ".o"))
+    cmd = [nvcc(), *ARCH, *FLAGS, *PER_FILE.get(src, []), "-dc" if False else "-c", os.path.join(CSRC, src), "-o", out]
+    if ptxas_verbose:
+        cmd += ["-Xptxas", "-v"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
+    return out, r.stderr
+
+
+def build(ptxas_verbose=False, force=False):
+    os.makedirs(OBJ, exist_ok=True)
+    newest_src = max(os.path.getmtime(os.path.join(CSRC, f)) for f in os.listdir(CSRC))
+    newest_src = max(newest_src, os.path.getmtime(os.path.join(ROOT, "include", "sbg.h")))
+    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) > newest_src and not ptxas_verbose:
+        return LIB
+    with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
+        results = list(ex.map(lambda s: _compile(s, ptxas_verbose), SOURCES))
+    if ptxas_verbose:
+        for _, err in results:
+            sys.stderr.write(err)
+    objs = [o for o, _ in results]
+    cmd = [nvcc(), *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-lnccl", "-Xlinker", "-rpath,/usr/lib/x86_64-linux-gnu"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("link failed:\n" + r.stderr)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(ptxas_verbose="--verbose-ptxas" in sys.argv, force="--force" in sys.argv))

@@ -1,0 +1,395 @@
+// api.cu — the extern "C" boundary (include/sbg.h). Translates C++ exceptions into the
+// reference's error classes' codes and keeps a thread-local message (sbg_last_error).
+#include <nccl.h>
+
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <random>
+#include <string>
+
+#include "../../include/sbg.h"
+#include "context.hpp"
+#include "solver.hpp"
+
+struct sbg_ctx {
+    std::unique_ptr<sbg::Context> c;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return SBG_OK;
+    } catch (const sbg::NonConvergenceError& e) {
+        g_err = e.what();
+        return SBG_ENONCONV;
+    } catch (const sbg::DeviceError& e) {
+        g_err = e.what();
+        return SBG_EDEVICE;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return SBG_EINVAL;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return SBG_ERUNTIME;
+    }
+}
+
+uint64_t binomial_u64(int n, int k) {  // determinants.hpp:17-31
+    if (k < 0 || k > n) return 0;
+    k = std::min(k, n - k);
+    uint64_t r = 1;
+    for (int i = 1; i <= k; ++i) {
+        const uint64_t num = (uint64_t)(n - k + i);
+        const uint64_t g = std::gcd(r, (uint64_t)i);
+        r = (r / g) * num / ((uint64_t)i / g);
+    }
+    return r;
+}
+
+sbg::SolverConfig to_cfg(const sbg_config* c) {
+    sbg::SolverConfig s;
+    if (!c) return s;
+    s.eps0 = c->eps0;
+    s.r0 = c->r0;
+    s.b_th = c->b_th;
+    s.eps1 = c->eps1;
+    s.x_th1 = c->x_th1;
+    s.x_th2 = c->x_th2;
+    s.r1 = c->r1;
+    s.max_cycle = c->max_cycle;
+    s.t_max = (long)c->t_max;
+    s.lindep = c->lindep;
+    s.clamp_delta = c->clamp_delta;
+    s.hx_refresh_restarts = c->hx_refresh_restarts;
+    return s;
+}
+
+void require_ctx(const sbg_ctx* ctx) {
+    if (!ctx || !ctx->c) throw std::invalid_argument("null sbg_ctx");
+}
+}  // namespace
+
+namespace sbg {
+void shard_range(int64_t n, int rank, int world, int64_t* lo, int64_t* hi);
+}
+
+extern "C" {
+
+const char* sbg_last_error(void) { return g_err.c_str(); }
+const char* sbg_version(void) { return "sbg 0.1 (sm_100a)"; }
+uint64_t sbg_binomial(int n, int k) { return binomial_u64(n, k); }
+
+int sbg_determinant_count(int norb, int n_alpha, int n_beta, uint64_t* out) {
+    return guarded([&] {
+        if (norb < 0 || norb > 64) throw std::invalid_argument("determinant_count: norb out of range");
+        if (n_alpha < 0 || n_beta < 0 || n_alpha > norb || n_beta > norb)
+            throw std::invalid_argument("determinant_count: electron count out of range");
+        *out = binomial_u64(norb, n_alpha) * binomial_u64(norb, n_beta);
+    });
+}
+
+sbg_config sbg_config_default(void) {
+    sbg::SolverConfig s;
+    sbg_config c{};
+    c.eps0 = s.eps0;
+    c.r0 = s.r0;
+    c.b_th = s.b_th;
+    c.eps1 = s.eps1;
+    c.x_th1 = s.x_th1;
+    c.x_th2 = s.x_th2;
+    c.r1 = s.r1;
+    c.max_cycle = s.max_cycle;
+    c.hx_refresh_restarts = s.hx_refresh_restarts;
+    c.t_max = s.t_max;
+    c.lindep = s.lindep;
+    c.clamp_delta = s.clamp_delta;
+    return c;
+}
+
+int sbg_config_validate(const sbg_config* cfg) {
+    return guarded([&] { to_cfg(cfg).validate(); });
+}
+
+// Pinned BASELINE.json generator; bit-identical to oracle/sbci_oracle.cpp:or_synthetic.
+int sbg_synthetic_integrals(int norb, uint64_t seed, double offdiag_scale, double* h1, double* eri) {
+    return guarded([&] {
+        if (norb < 1 || norb > 32) throw std::invalid_argument("synthetic: norb out of range");
+        std::mt19937_64 eng(seed);
+        auto uni = [&]() { return (double)(eng() >> 11) * 0x1.0p-53; };
+        auto normal = [&]() {
+            const double u1 = uni(), u2 = uni();
+            return std::sqrt(-2.0 * std::log(1.0 - u1)) * std::cos(6.283185307179586476925286766559 * u2);
+        };
+        for (int p = 0; p < norb; ++p)
+            for (int q = p; q < norb; ++q) {
+                const double base = (p == q) ? (-1.0 + 2.0 * p / norb) : 0.0;
+                const double v = base + 0.05 * normal();
+                h1[p * norb + q] = v;
+                h1[q * norb + p] = v;
+            }
+        const size_t no2 = (size_t)norb * norb;
+        std::vector<double> L((size_t)norb * no2);
+        for (int k = 0; k < norb; ++k)
+            for (int p = 0; p < norb; ++p)
+                for (int q = p; q < norb; ++q) {
+                    const double v = (p == q) ? 0.5 + 0.1 * normal() : offdiag_scale * normal();
+                    L[k * no2 + p * norb + q] = v;
+                    L[k * no2 + q * norb + p] = v;
+                }
+        for (size_t pq = 0; pq < no2; ++pq)
+            for (size_t rs = 0; rs < no2; ++rs) {
+                double s = 0.0;
+                for (int k = 0; k < norb; ++k) s += L[k * no2 + pq] * L[k * no2 + rs];
+                eri[pq * no2 + rs] = s;
+            }
+    });
+}
+
+int sbg_shard_range(int64_t n, int rank, int world, int64_t* lo, int64_t* hi) {
+    return guarded([&] {
+        if (world < 1 || rank < 0 || rank >= world || n < 0) throw std::invalid_argument("shard_range: bad arguments");
+        sbg::shard_range(n, rank, world, lo, hi);
+    });
+}
+
+int sbg_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int sbg_create(int norb, int nelec, int ms2, double e_core, const double* h1, const double* eri, int device,
+               uint64_t max_det, sbg_ctx** out) {
+    return sbg_create_dist(norb, nelec, ms2, e_core, h1, eri, device, max_det, 0, 1, nullptr, out);
+}
+
+int sbg_create_dist(int norb, int nelec, int ms2, double e_core, const double* h1, const double* eri, int device,
+                    uint64_t max_det, int rank, int world, const void* nccl_unique_id, sbg_ctx** out) {
+    return guarded([&] {
+        if (!out || !h1 || !eri) throw std::invalid_argument("sbg_create: null argument");
+        if (world > 1 && !nccl_unique_id) throw std::invalid_argument("sbg_create_dist: missing NCCL unique id");
+        auto* c = new sbg_ctx;
+        try {
+            c->c = std::make_unique<sbg::Context>(norb, nelec, ms2, e_core, h1, eri, device, max_det, rank, world,
+                                                  nccl_unique_id);
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
+    });
+}
+
+int sbg_nccl_unique_id(void* out128) {
+    return guarded([&] {
+        ncclUniqueId id;
+        if (ncclGetUniqueId(&id) != ncclSuccess) throw sbg::DeviceError("ncclGetUniqueId failed");
+        std::memcpy(out128, &id, sizeof(id));
+    });
+}
+
+void sbg_destroy(sbg_ctx* ctx) { delete ctx; }
+
+int64_t sbg_dim(const sbg_ctx* ctx) { return ctx && ctx->c ? ctx->c->ndet : -1; }
+
+int sbg_sector(const sbg_ctx* ctx, int* norb, int* n_alpha, int* n_beta, int64_t* nas, int64_t* nbs) {
+    return guarded([&] {
+        require_ctx(ctx);
+        const auto& c = *ctx->c;
+        if (norb) *norb = c.norb;
+        if (n_alpha) *n_alpha = c.na_el;
+        if (n_beta) *n_beta = c.nb_el;
+        if (nas) *nas = c.NA;
+        if (nbs) *nbs = c.NB;
+    });
+}
+
+int sbg_local_rows(const sbg_ctx* ctx, int64_t* lo, int64_t* hi) {
+    return guarded([&] {
+        require_ctx(ctx);
+        *lo = ctx->c->row_lo;
+        *hi = ctx->c->row_hi;
+    });
+}
+
+int sbg_diagonal(sbg_ctx* ctx, double* out) {
+    return guarded([&] {
+        require_ctx(ctx);
+        auto& c = *ctx->c;
+        c.download_local(c.diagonal().p, out + c.row_lo * c.NB, c.st);
+        SBG_CUDA(cudaStreamSynchronize(c.st));
+    });
+}
+
+int sbg_table_sizes(const sbg_ctx* ctx, int spin, int64_t* n_strings, int64_t* row_len) {
+    return guarded([&] {
+        require_ctx(ctx);
+        if (spin != 0 && spin != 1) throw std::invalid_argument("spin must be 0 or 1");
+        if (n_strings) *n_strings = spin == 0 ? ctx->c->NA : ctx->c->NB;
+        if (row_len) *row_len = ctx->c->row_len(spin);
+    });
+}
+
+int sbg_string_tables(sbg_ctx* ctx, int spin, uint64_t* strings, sbg_excitation* links) {
+    return guarded([&] {
+        require_ctx(ctx);
+        if (spin != 0 && spin != 1) throw std::invalid_argument("spin must be 0 or 1");
+        ctx->c->string_tables(spin, strings, reinterpret_cast<sbg::Excitation*>(links));
+    });
+}
+
+int sbg_sigma(sbg_ctx* ctx, const double* x, double* y, int nvec) {
+    return guarded([&] {
+        require_ctx(ctx);
+        if (nvec < 0 || (!x && nvec) || (!y && nvec)) throw std::invalid_argument("sbg_sigma: bad arguments");
+        auto& c = *ctx->c;
+        sbg::DBuf dx = c.alloc_vec(), dy = c.alloc_vec();
+        for (int v = 0; v < nvec; ++v) {
+            c.upload_local(x + (size_t)v * c.ndet, dx.p, c.st);
+            c.sigma(dx, dy);
+            c.download_local(dy.p, y + (size_t)v * c.ndet + c.row_lo * c.NB, c.st);
+        }
+        SBG_CUDA(cudaStreamSynchronize(c.st));
+    });
+}
+
+int64_t sbg_padded_len(const sbg_ctx* ctx) { return ctx && ctx->c ? ctx->c->padded_len() : -1; }
+
+int sbg_pack(sbg_ctx* ctx, const double* d_dense_full, double* d_padded_local, void* stream) {
+    return guarded([&] {
+        require_ctx(ctx);
+        auto& c = *ctx->c;
+        cudaStream_t s = stream ? (cudaStream_t)stream : c.st;
+        SBG_CUDA(cudaMemsetAsync(d_padded_local, 0, c.padded_len() * 8, s));
+        c.pack_device(d_dense_full, d_padded_local, s);
+    });
+}
+
+int sbg_unpack(sbg_ctx* ctx, const double* d_padded_local, double* d_dense_local, void* stream) {
+    return guarded([&] {
+        require_ctx(ctx);
+        auto& c = *ctx->c;
+        c.unpack_device(d_padded_local, d_dense_local, stream ? (cudaStream_t)stream : c.st);
+    });
+}
+
+int sbg_sigma_padded(sbg_ctx* ctx, const double* dx, double* dy, void* stream) {
+    return guarded([&] {
+        require_ctx(ctx);
+        auto& c = *ctx->c;
+        c.sigma(dx, dy, stream ? (cudaStream_t)stream : c.st);
+    });
+}
+
+int sbg_sigma_device(sbg_ctx* ctx, const double* d_x, double* d_y, void* stream) {
+    return guarded([&] {
+        require_ctx(ctx);
+        auto& c = *ctx->c;
+        cudaStream_t s = stream ? (cudaStream_t)stream : c.st;
+        sbg::DBuf px = c.alloc_vec(), py = c.alloc_vec();
+        c.pack_device(d_x, px.p, s);
+        c.sigma(px.p, py.p, s);
+        c.unpack_device(py.p, d_y + c.row_lo * c.NB, s);
+        SBG_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+uint64_t sbg_apply_count(const sbg_ctx* ctx) { return ctx && ctx->c ? ctx->c->applies().load() : 0; }
+void sbg_reset_apply_count(sbg_ctx* ctx) {
+    if (ctx && ctx->c) ctx->c->applies().store(0);
+}
+uint64_t sbg_kernel_launches(const sbg_ctx* ctx) { return ctx && ctx->c ? ctx->c->launches : 0; }
+
+int sbg_sigma_flops(const sbg_ctx* ctx, double* ab, double* ss, double* total) {
+    return guarded([&] {
+        require_ctx(ctx);
+        if (ab) *ab = ctx->c->flops_ab;
+        if (ss) *ss = ctx->c->flops_ss;
+        if (total) *total = ctx->c->flops_ab + ctx->c->flops_ss;
+    });
+}
+
+int sbg_solve(sbg_ctx* ctx, int method, int nroots, const sbg_config* cfg, double* energies, double* vectors,
+              sbg_stats* stats, sbg_trace_fn trace, void* trace_user) {
+    return guarded([&] {
+        require_ctx(ctx);
+        if (method != 1) throw std::invalid_argument("sbg_solve: method must be 1 (sbci1)");
+        if (nroots < 1 || nroots > SBG_MAX_ROOTS) throw std::invalid_argument("sbg_solve: nroots out of range");
+        auto& c = *ctx->c;
+        std::function<void(const sbg::TraceRec&)> tf;
+        if (trace)
+            tf = [&](const sbg::TraceRec& r) {
+                sbg_trace_record rec{};
+                rec.state = r.state;
+                rec.t = r.t;
+                rec.energy = r.energy;
+                rec.dE = r.dE;
+                rec.res_norm = r.res_norm;
+                rec.x_norm = r.x_norm;
+                rec.kinetic = r.kinetic;
+                rec.matvecs = r.matvecs;
+                rec.restart_reason = r.restart_reason;
+                rec.b = r.b;
+                rec.c = r.c;
+                trace(&rec, trace_user);
+            };
+        const uint64_t launches0 = c.launches;
+        try {
+            sbg::MultiStateResult r = sbg::solve_n_states_sbci1(c, nroots, to_cfg(cfg), tf);
+            for (int k = 0; k < nroots; ++k) {
+                energies[k] = r.pairs[k].energy;
+                if (vectors) c.download_local(r.pairs[k].vector.p, vectors + (size_t)k * c.ndet + c.row_lo * c.NB, c.st);
+            }
+            SBG_CUDA(cudaStreamSynchronize(c.st));
+            if (stats) {
+                std::memset(stats, 0, sizeof(*stats));
+                stats->nroots = nroots;
+                for (int k = 0; k < nroots; ++k) {
+                    stats->iterations[k] = r.pairs[k].iterations;
+                    stats->restarts[k] = r.pairs[k].restarts;
+                    stats->final_residual[k] = r.pairs[k].final_residual;
+                }
+                stats->matvecs = r.matvecs;
+                stats->total_iterations = r.total_iterations;
+                stats->total_restarts = r.total_restarts;
+                stats->hx_refreshes = r.hx_refreshes;
+                stats->peak_vectors = r.peak_vectors;
+                stats->wall_time_s = r.wall_time_s;
+                stats->failed_state = -1;
+                stats->kernel_launches = c.launches - launches0;
+            }
+        } catch (const sbg::NonConvergenceError& e) {
+            if (stats) {
+                std::memset(stats, 0, sizeof(*stats));
+                stats->failed_state = e.state;
+                stats->best_energy = e.best_energy;
+                stats->best_residual = e.best_residual;
+            }
+            throw;
+        }
+    });
+}
+
+int sbg_selftest(void) {
+    int bad = -1;
+    const int rc = guarded([&] {
+        SBG_CUDA(cudaSetDevice(0));
+        bad = sbg::run_mma_selftest();
+    });
+    if (rc != SBG_OK) return rc;
+    if (bad != 0) {
+        g_err = "DMMA fragment layout mismatch in " + std::to_string(bad) + " entries";
+        return SBG_EDEVICE;
+    }
+    return SBG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,386 @@
+// context.cu — construction of the device-resident FCI operator and the sigma orchestration.
+#include "context.hpp"
+
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+namespace sbg {
+
+// ------------------------------------------------------------------ buffers
+DBuf::DBuf(int64_t count) : n(count) {
+    if (count > 0) {
+        SBG_CUDA(cudaMalloc(&p, (size_t)count * sizeof(double)));
+        SBG_CUDA(cudaMemset(p, 0, (size_t)count * sizeof(double)));
+    }
+}
+DBuf::~DBuf() {
+    if (p) cudaFree(p);
+}
+DBuf& DBuf::operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+        if (p) cudaFree(p);
+        p = o.p;
+        n = o.n;
+        o.p = nullptr;
+        o.n = 0;
+    }
+    return *this;
+}
+
+// ------------------------------------------------------------------ NCCL plumbing
+struct Comm {
+    ncclComm_t comm = nullptr;
+    ~Comm() {
+        if (comm) ncclCommDestroy(comm);
+    }
+};
+#define SBG_NCCL(x)                                                                                     \
+    do {                                                                                                \
+        ncclResult_t r_ = (x);                                                                          \
+        if (r_ != ncclSuccess) throw DeviceError(std::string("NCCL error ") + ncclGetErrorString(r_) + \
+                                                 " in " #x);                                            \
+    } while (0)
+
+namespace {
+
+template <class T>
+T* dmalloc(size_t n) {
+    T* p = nullptr;
+    SBG_CUDA(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+    return p;
+}
+
+__global__ void k_add_block(double* dst, int64_t ldd, const double* src, int64_t rows, int64_t cols) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= rows * cols) return;
+    const int64_t r = i / cols, c = i % cols;
+    dst[r * ldd + c] += src[i];
+}
+
+}  // namespace
+
+// rows [lo,hi) of a block partition with equal block sizes ceil(n/world); the last
+// ranks may own fewer (or zero) rows.
+void shard_range(int64_t n, int rank, int world, int64_t* lo, int64_t* hi) {
+    const int64_t per = (n + world - 1) / world;
+    *lo = std::min<int64_t>(n, (int64_t)rank * per);
+    *hi = std::min<int64_t>(n, *lo + per);
+}
+
+// ------------------------------------------------------------------ context
+Context::Context(int norb_, int nelec_, int ms2_, double e_core_, const double* h1, const double* eri, int device_,
+                 uint64_t max_det, int rank_, int world_, const void* nccl_id)
+    : norb(norb_), nelec(nelec_), ms2(ms2_), e_core(e_core_), rank(rank_), world(world_), device(device_) {
+    if (norb < 1 || norb > kMaxOrb) throw InvalidArgument("FciProblem: norb must be in [1, 32]");
+    if (nelec < 0 || nelec > 2 * norb) throw InvalidArgument("as_operator: NELEC out of range");
+    if ((nelec + ms2) % 2 != 0) throw InvalidArgument("as_operator: MS2 parity mismatch");
+    na_el = (nelec + ms2) / 2;
+    nb_el = (nelec - ms2) / 2;
+    if (na_el < 0 || nb_el < 0 || na_el > norb || nb_el > norb)
+        throw InvalidArgument("determinant_count: electron count out of range");
+    if (na_el + nb_el == 0) throw InvalidArgument("FciOperator: empty electron sector");
+    NA = (int64_t)binom_host_calc(norb, na_el);
+    NB = (int64_t)binom_host_calc(norb, nb_el);
+    ndet = NA * NB;
+    if ((uint64_t)ndet > max_det)
+        throw std::runtime_error("as_operator: sector holds " + std::to_string(ndet) +
+                                 " determinants, above the guard of " + std::to_string(max_det) +
+                                 " (pass a larger bound to override)");
+    if (world < 1 || rank < 0 || rank >= world) throw InvalidArgument("sbg_create_dist: bad rank/world");
+    ld = round_up(NB, 32);
+    ldT = round_up(NA, 32);
+    shard_range(NA, rank, world, &row_lo, &row_hi);
+    nrows = row_hi - row_lo;
+
+    SBG_CUDA(cudaSetDevice(device));
+    SBG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+    SBG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    SBG_CUDA(cudaEventCreate(&ev0_));
+    SBG_CUDA(cudaEventCreate(&ev1_));
+
+    if (world > 1) {
+        comm_ = std::make_unique<Comm>();
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id, sizeof(id));
+        SBG_NCCL(ncclCommInitRank(&comm_->comm, world, id, rank));
+    }
+
+    rws.grid = 2 * nsm;
+    rws.partial = dmalloc<double>((size_t)rws.grid * kMaxDot);
+    rws.result = dmalloc<double>(kMaxDot);
+    SBG_CUDA(cudaMallocHost(&rws.host, kMaxDot * sizeof(double)));
+
+    build_tables(h1, eri);
+}
+
+Context::~Context() {
+    if (st) cudaStreamSynchronize(st);
+    for (void* p : {(void*)d_sa_, (void*)d_sb_, (void*)d_la_, (void*)d_lb_, (void*)d_h1_, (void*)d_eri_, (void*)d_Vp_,
+                    (void*)d_Va_, (void*)d_codes_, (void*)rws.partial, (void*)rws.result})
+        if (p) cudaFree(p);
+    if (rws.host) cudaFreeHost(rws.host);
+    comm_.reset();
+    if (ev0_) cudaEventDestroy(ev0_);
+    if (ev1_) cudaEventDestroy(ev1_);
+    if (st) cudaStreamDestroy(st);
+}
+
+DBuf Context::alloc_vec() const { return DBuf(padded_len()); }
+
+void Context::build_tables(const double* h1, const double* eri) {
+    const size_t n2 = (size_t)norb * norb, n4 = n2 * n2;
+    d_h1_ = dmalloc<double>(n2);
+    d_eri_ = dmalloc<double>(n4);
+    SBG_CUDA(cudaMemcpyAsync(d_h1_, h1, n2 * 8, cudaMemcpyHostToDevice, st));
+    SBG_CUDA(cudaMemcpyAsync(d_eri_, eri, n4 * 8, cudaMemcpyHostToDevice, st));
+    d_sa_ = dmalloc<uint64_t>(NA);
+    d_sb_ = dmalloc<uint64_t>(NB);
+    launch_strings(d_sa_, NA, na_el, norb, st);
+    launch_strings(d_sb_, NB, nb_el, norb, st);
+    launches += 2;
+
+    // exact diagonal (fci_operator.hpp:16-57)
+    {
+        double* ea = dmalloc<double>(NA);
+        double* eb = dmalloc<double>(NB);
+        launch_string_energy(d_sa_, NA, norb, d_h1_, d_eri_, ea, st);
+        launch_string_energy(d_sb_, NB, norb, d_h1_, d_eri_, eb, st);
+        diag_ = alloc_vec();
+        launch_diag(d_sa_, d_sb_, ea, eb, row_lo, nrows, NB, ld, norb, d_eri_, e_core, diag_.p, st);
+        launches += 3;
+        SBG_CUDA(cudaStreamSynchronize(st));
+        cudaFree(ea);
+        cudaFree(eb);
+    }
+
+    auto g = [&](int p, int q, int r, int s) { return eri[((size_t)(p * norb + q) * norb + r) * norb + s]; };
+    // alpha-beta integrals with both one-body terms folded (sigma_ab.cu header)
+    have_ab_ = na_el > 0 && nb_el > 0;
+    if (have_ab_) {
+        const int np = norb * (norb + 1) / 2;
+        std::vector<double> Vp((size_t)np * np);
+        for (int p = 0; p < norb; ++p)
+            for (int q = 0; q <= p; ++q)
+                for (int r = 0; r < norb; ++r)
+                    for (int s = 0; s <= r; ++s) {
+                        double v = g(p, q, r, s);
+                        if (r == s) v += h1[p * norb + q] / nb_el;
+                        if (p == q) v += h1[r * norb + s] / na_el;
+                        Vp[(size_t)pair_sym(p, q) * np + pair_sym(r, s)] = v;
+                    }
+        d_Vp_ = dmalloc<double>(Vp.size());
+        SBG_CUDA(cudaMemcpyAsync(d_Vp_, Vp.data(), Vp.size() * 8, cudaMemcpyHostToDevice, st));
+        ab_ = plan_sigma_ab(norb, na_el, nb_el, NA, NB, ld, nsm);
+        d_codes_ = dmalloc<uint16_t>((size_t)ld * ab_.npad);
+        launch_scatter_codes(d_sb_, NB, ld, norb, ab_.npair, ab_.npad, d_codes_, st);
+        launches += 1;
+        SBG_CUDA(cudaStreamSynchronize(st));  // Vp host buffer
+    }
+    // same-spin antisymmetrized pair integrals W(pr,qs) = (pq|rs) - (ps|rq), p<r, q<s
+    if (norb >= 2) {
+        const int npa = norb * (norb - 1) / 2;
+        std::vector<double> Va((size_t)npa * npa);
+        for (int r = 1; r < norb; ++r)
+            for (int p = 0; p < r; ++p)
+                for (int s = 1; s < norb; ++s)
+                    for (int q = 0; q < s; ++q)
+                        Va[(size_t)pair_strict(p, r) * npa + pair_strict(q, s)] = g(p, q, r, s) - g(p, s, r, q);
+        d_Va_ = dmalloc<double>(Va.size());
+        SBG_CUDA(cudaMemcpyAsync(d_Va_, Va.data(), Va.size() * 8, cudaMemcpyHostToDevice, st));
+        SBG_CUDA(cudaStreamSynchronize(st));
+    }
+    ssa_ = plan_sigma_ss(norb, na_el);
+    ssb_ = plan_sigma_ss(norb, nb_el);
+    if (!have_ab_) ensure_links();
+
+    // flop accounting: useful (unpadded) multiply-adds x 2
+    flops_ab = have_ab_ ? 2.0 * ab_.npair * ab_.K * (double)ndet : 0.0;
+    flops_ss = 2.0 * ssa_.P * ssa_.P * (double)ssa_.NK * NB + 2.0 * ssb_.P * ssb_.P * (double)ssb_.NK * NA;
+
+    // workspaces
+    if (world > 1) {
+        const int64_t per = (NA + world - 1) / world;
+        xfull_ = DBuf(per * world * ld);
+        saa_ = DBuf(NA * ld);
+        a2a_send_ = DBuf(NA * ld);
+        a2a_recv_ = DBuf(nrows * ld);
+    }
+    if (ssb_.P > 0) {
+        xT_ = DBuf(NB * ldT);
+        sT_ = DBuf(NB * ldT);
+    }
+    SBG_CUDA(cudaStreamSynchronize(st));
+}
+
+void Context::ensure_links() {
+    if (d_la_) return;
+    d_la_ = dmalloc<Excitation>((size_t)NA * row_len(0));
+    d_lb_ = dmalloc<Excitation>((size_t)NB * row_len(1));
+    launch_links(d_sa_, NA, norb, (int)row_len(0), d_la_, st);
+    launch_links(d_sb_, NB, norb, (int)row_len(1), d_lb_, st);
+    launches += 2;
+    SBG_CUDA(cudaStreamSynchronize(st));
+}
+
+int64_t Context::row_len(int spin) const {
+    const int k = spin == 0 ? na_el : nb_el;
+    return (int64_t)k * (norb - k + 1);
+}
+
+void Context::string_tables(int spin, uint64_t* strings, Excitation* links) {
+    const int64_t n = spin == 0 ? NA : NB;
+    if (strings)
+        SBG_CUDA(cudaMemcpyAsync(strings, spin == 0 ? d_sa_ : d_sb_, n * 8, cudaMemcpyDeviceToHost, st));
+    if (links) {
+        ensure_links();
+        SBG_CUDA(cudaMemcpyAsync(links, spin == 0 ? d_la_ : d_lb_, (size_t)n * row_len(spin) * sizeof(Excitation),
+                                 cudaMemcpyDeviceToHost, st));
+    }
+    SBG_CUDA(cudaStreamSynchronize(st));
+}
+
+void Context::upload_local(const double* host_dense_full, double* d_padded, cudaStream_t s) const {
+    if (nrows == 0) return;
+    SBG_CUDA(cudaMemcpy2DAsync(d_padded, ld * 8, host_dense_full + row_lo * NB, NB * 8, NB * 8, nrows,
+                               cudaMemcpyHostToDevice, s));
+}
+void Context::download_local(const double* d_padded, double* host_dense_local, cudaStream_t s) const {
+    if (nrows == 0) return;
+    SBG_CUDA(cudaMemcpy2DAsync(host_dense_local, NB * 8, d_padded, ld * 8, NB * 8, nrows, cudaMemcpyDeviceToHost, s));
+}
+void Context::pack_device(const double* d_dense_full, double* d_padded, cudaStream_t s) const {
+    if (nrows == 0) return;
+    SBG_CUDA(cudaMemcpy2DAsync(d_padded, ld * 8, d_dense_full + row_lo * NB, NB * 8, NB * 8, nrows,
+                               cudaMemcpyDeviceToDevice, s));
+}
+void Context::unpack_device(const double* d_padded, double* d_dense_local, cudaStream_t s) const {
+    if (nrows == 0) return;
+    SBG_CUDA(cudaMemcpy2DAsync(d_dense_local, NB * 8, d_padded, ld * 8, NB * 8, nrows, cudaMemcpyDeviceToDevice, s));
+}
+
+void Context::gather_full(const double* x_local, cudaStream_t s) {
+    const int64_t per = (NA + world - 1) / world;
+    // every rank contributes `per` rows (zero rows past NA on the last ranks)
+    SBG_CUDA(cudaMemsetAsync(xfull_.p + (int64_t)rank * per * ld, 0, per * ld * 8, s));
+    if (nrows > 0)
+        SBG_CUDA(cudaMemcpyAsync(xfull_.p + (int64_t)rank * per * ld, x_local, nrows * ld * 8,
+                                 cudaMemcpyDeviceToDevice, s));
+    SBG_NCCL(ncclAllGather(xfull_.p + (int64_t)rank * per * ld, xfull_.p, (size_t)(per * ld), ncclDouble,
+                           comm_->comm, s));
+}
+
+void Context::allreduce_inplace_device(double* d, int count) {
+    if (world > 1 && count > 0) SBG_NCCL(ncclAllReduce(d, d, count, ncclDouble, ncclSum, comm_->comm, st));
+}
+
+const double* Context::finish_dots(int ndot) {
+    allreduce_inplace_device(rws.result, ndot);
+    SBG_CUDA(cudaMemcpyAsync(rws.host, rws.result, ndot * 8, cudaMemcpyDeviceToHost, st));
+    SBG_CUDA(cudaStreamSynchronize(st));
+    return rws.host;
+}
+
+// y = H x (SymmetricOperator::apply, operator.hpp:25-31). Kernel sequence:
+//   1. [world>1] all-gather x over NVLink (the only data-path collective of a sigma build)
+//   2. beta-beta: transpose x -> x^T, same-spin kernel on x^T, transpose back into y (local rows)
+//   3. alpha-alpha: same-spin kernel on x, fp64 reductions into y (world>1: column window +
+//      all-to-all of the blocks)
+//   4. alpha-beta + one-body + e_core: sigma_ab, accumulating into y
+void Context::sigma(const double* x_local, double* y_local, cudaStream_t s) {
+    SBG_CUDA(cudaEventRecord(ev0_, s));
+    const double* xf = x_local;
+    if (world > 1) {
+        gather_full(x_local, s);
+        xf = xfull_.p;
+    }
+    bool y_written = false;
+    // ---- beta-beta via the transpose
+    if (ssb_.P > 0) {
+        launch_transpose(xf, NA, NB, ld, xT_.p, ldT, NB, 0, s);
+        SBG_CUDA(cudaMemsetAsync(sT_.p, 0, (size_t)NB * ldT * 8, s));
+        launch_sigma_ss(ssb_, xT_.p, sT_.p, d_Va_, ldT, row_lo, row_hi, s);
+        // y[r][c] = sT[c][row_lo + r]
+        launch_transpose(sT_.p + row_lo, NB, nrows, ldT, y_local, ld, nrows, 0, s);
+        launches += 3;
+        y_written = true;
+    }
+    if (!y_written) SBG_CUDA(cudaMemsetAsync(y_local, 0, (size_t)nrows * ld * 8, s));
+    // ---- alpha-alpha
+    if (ssa_.P > 0) {
+        if (world == 1) {
+            launch_sigma_ss(ssa_, xf, y_local, d_Va_, ld, 0, NB, s);
+            launches += 1;
+        } else {
+            int64_t clo, chi;
+            shard_range(NB, rank, world, &clo, &chi);
+            SBG_CUDA(cudaMemsetAsync(saa_.p, 0, (size_t)NA * ld * 8, s));
+            launch_sigma_ss(ssa_, xf, saa_.p, d_Va_, ld, clo, chi, s);
+            launches += 1;
+            // all-to-all: send rows of rank r' restricted to my column window; receive my rows of
+            // every rank's window.
+            const int64_t wl = chi - clo;
+            std::vector<int64_t> rlo(world), rhi(world), cwl(world), cwh(world);
+            for (int r = 0; r < world; ++r) {
+                shard_range(NA, r, world, &rlo[r], &rhi[r]);
+                shard_range(NB, r, world, &cwl[r], &cwh[r]);
+            }
+            int64_t off = 0;
+            for (int r = 0; r < world; ++r) {
+                const int64_t nr = rhi[r] - rlo[r];
+                if (nr > 0 && wl > 0)
+                    SBG_CUDA(cudaMemcpy2DAsync(a2a_send_.p + off, wl * 8, saa_.p + rlo[r] * ld + clo, ld * 8, wl * 8,
+                                               nr, cudaMemcpyDeviceToDevice, s));
+                off += nr * wl;
+            }
+            SBG_NCCL(ncclGroupStart());
+            off = 0;
+            int64_t roff = 0;
+            for (int r = 0; r < world; ++r) {
+                const int64_t nr = rhi[r] - rlo[r];
+                const int64_t rw = cwh[r] - cwl[r];
+                if (r != rank) {
+                    if (nr * wl > 0) SBG_NCCL(ncclSend(a2a_send_.p + off, (size_t)(nr * wl), ncclDouble, r, comm_->comm, s));
+                    if (nrows * rw > 0)
+                        SBG_NCCL(ncclRecv(a2a_recv_.p + roff, (size_t)(nrows * rw), ncclDouble, r, comm_->comm, s));
+                } else if (nrows * rw > 0) {
+                    SBG_CUDA(cudaMemcpyAsync(a2a_recv_.p + roff, a2a_send_.p + off, nrows * rw * 8,
+                                             cudaMemcpyDeviceToDevice, s));
+                }
+                off += nr * wl;
+                roff += nrows * rw;
+            }
+            SBG_NCCL(ncclGroupEnd());
+            roff = 0;
+            for (int r = 0; r < world; ++r) {
+                const int64_t rw = cwh[r] - cwl[r];
+                if (nrows * rw > 0) {
+                    const int64_t n = nrows * rw;
+                    k_add_block<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(y_local + cwl[r], ld, a2a_recv_.p + roff,
+                                                                            nrows, rw);
+                    SBG_LAUNCH_CHECK();
+                    launches += 1;
+                }
+                roff += nrows * rw;
+            }
+        }
+    }
+    // ---- alpha-beta (+ one-body folded, + e_core)
+    if (have_ab_) {
+        launch_sigma_ab(ab_, xf, y_local, d_Vp_, d_codes_, row_lo, row_hi, e_core, 1, nsm, s);
+        launches += 1;
+    } else {
+        ensure_links();
+        // rows of this rank: the one-body kernel works on full-height buffers; single GPU only
+        if (world > 1) throw InvalidArgument("single-spin sectors are not supported across ranks");
+        launch_onebody(xf, y_local, d_la_, (int)row_len(0), d_lb_, (int)row_len(1), d_h1_, norb, NA, NB, ld, e_core,
+                       1, s);
+        launches += 1;
+    }
+    SBG_CUDA(cudaEventRecord(ev1_, s));
+    applies_.fetch_add(1, std::memory_order_relaxed);
+}
+
+}  // namespace sbg

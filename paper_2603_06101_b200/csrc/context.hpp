@@ -1,0 +1,102 @@
+// context.hpp — device-resident FCI operator: the B200 replacement of sbci::fci::FciOperator
+// (fci_operator.hpp:60-86). Owns the string tables, folded integrals, scatter codes, the exact
+// diagonal and the sigma workspaces in HBM; sigma() is SymmetricOperator::apply (operator.hpp:25-31)
+// on device vectors.
+//
+// HBM layout of every length-n_det vector: row-major [rows][ld] with rows = the
+// alpha strings owned by this rank (contiguous block) and ld = n_beta_strings rounded
+// up to 32 (256-byte rows, so 16-byte cp.async / TMA-sized gathers never straddle a row); the
+// padding columns are kept at exactly zero by every kernel.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <atomic>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace sbg {
+
+struct DBuf {
+    double* p = nullptr;
+    int64_t n = 0;
+    DBuf() = default;
+    explicit DBuf(int64_t count);
+    ~DBuf();
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DBuf& operator=(DBuf&& o) noexcept;
+    bool empty() const { return p == nullptr; }
+};
+
+struct Comm;  // NCCL plumbing (dist.cu); null for a single GPU
+
+class Context {
+public:
+    Context(int norb, int nelec, int ms2, double e_core, const double* h1, const double* eri, int device,
+            uint64_t max_det, int rank, int world, const void* nccl_id);
+    ~Context();
+
+    // sector
+    int norb, nelec, ms2, na_el, nb_el;
+    double e_core;
+    int64_t NA, NB, ndet, ld, ldT;
+    int64_t row_lo, row_hi, nrows;  // alpha rows owned by this rank
+    int rank, world, device, nsm;
+    cudaStream_t st = nullptr;
+
+    int64_t padded_len() const { return nrows * ld; }
+    DBuf alloc_vec() const;  // zero-initialised padded local vector
+
+    // y = H x on padded local vectors (counts one application)
+    void sigma(const double* x_local, double* y_local, cudaStream_t s);
+    void sigma(const DBuf& x, DBuf& y) { sigma(x.p, y.p, st); }
+
+    // host <-> padded device conversions (dense local rows = rows [row_lo,row_hi) of the n_det vector)
+    void upload_local(const double* host_dense_full, double* d_padded, cudaStream_t s) const;
+    void download_local(const double* d_padded, double* host_dense_local, cudaStream_t s) const;
+    void pack_device(const double* d_dense_full, double* d_padded, cudaStream_t s) const;
+    void unpack_device(const double* d_padded, double* d_dense_local, cudaStream_t s) const;
+
+    // tables
+    const DBuf& diagonal() const { return diag_; }
+    void string_tables(int spin, uint64_t* strings, Excitation* links);
+    int64_t row_len(int spin) const;
+
+    // reductions: dot buffer all-reduced over ranks and copied to host
+    ReduceWs rws;
+    const double* finish_dots(int ndot);  // sync; returns host pointer
+    void allreduce_inplace_device(double* d, int count);
+
+    std::atomic<uint64_t>& applies() { return applies_; }
+    uint64_t launches = 0;
+    double sigma_ms = 0.0;  // accumulated device time of sigma calls (events)
+    double flops_ab = 0, flops_ss = 0;
+
+private:
+    void build_tables(const double* h1, const double* eri);
+    void ensure_links();
+    void gather_full(const double* x_local, cudaStream_t s);
+
+    std::atomic<uint64_t> applies_{0};
+    std::unique_ptr<Comm> comm_;
+    // device tables
+    uint64_t *d_sa_ = nullptr, *d_sb_ = nullptr;
+    Excitation *d_la_ = nullptr, *d_lb_ = nullptr;
+    double *d_h1_ = nullptr, *d_eri_ = nullptr, *d_Vp_ = nullptr, *d_Va_ = nullptr, *d_Vb_ = nullptr;
+    uint16_t* d_codes_ = nullptr;
+    DBuf diag_;
+    // sigma workspaces
+    DBuf xfull_, xT_, sT_, saa_, a2a_send_, a2a_recv_;
+    AbPlan ab_{};
+    SsPlan ssa_{}, ssb_{};
+    bool have_ab_ = false;
+    cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+};
+
+}  // namespace sbg

@@ -1,0 +1,111 @@
+// kernels.cuh — launch interfaces of the sm_100a kernels (host-callable).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace sbg {
+
+// byte-compatible with sbg_excitation / sbci::fci::Excitation (fci/sigma.hpp:19-23)
+struct Excitation {
+    uint16_t p, q;
+    uint32_t target;
+    double sign;
+};
+static_assert(sizeof(Excitation) == 16, "Excitation layout");
+
+// ---- tables.cu ----
+void launch_strings(uint64_t* out, int64_t n, int nel, int norb, cudaStream_t st);
+void launch_links(const uint64_t* strings, int64_t n, int norb, int row_len, Excitation* out, cudaStream_t st);
+void launch_string_energy(const uint64_t* strings, int64_t n, int norb, const double* h1, const double* eri,
+                          double* out, cudaStream_t st);
+void launch_diag(const uint64_t* sa, const uint64_t* sb, const double* ea, const double* eb, int64_t row_lo,
+                 int64_t nrows, int64_t nb, int64_t ld, int norb, const double* eri, double e_core, double* out,
+                 cudaStream_t st);
+void launch_scatter_codes(const uint64_t* sb, int64_t nb, int64_t ld, int norb, int npair, int npad, uint16_t* out,
+                          cudaStream_t st);
+
+// ---- sigma_ab.cu: opposite-spin term (+ folded one-body, + e_core), K6 ----
+struct AbPlan {
+    int norb, na_el, nb_el, npair, npad, mb16, extra, K, KS, threads;
+    int64_t NA, NB, ld;
+    size_t smem;
+};
+AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int64_t ld, int nsm);
+void launch_sigma_ab(const AbPlan& pl, const double* x_full, double* y_local, const double* Vp, const uint16_t* codes,
+                     int64_t row_lo, int64_t row_hi, double e_core, int accumulate, int grid, cudaStream_t st);
+
+// ---- sigma_ss.cu: same-spin term via the (n-2)-electron intermediate, K4/K5 ----
+struct SsPlan {
+    int norb, nel, P, KSS, warps, npa;
+    int64_t NK;
+    size_t smem;
+};
+SsPlan plan_sigma_ss(int norb, int nel);
+void launch_sigma_ss(const SsPlan& pl, const double* x, double* y, const double* Va, int64_t ldx, int64_t col_lo,
+                     int64_t col_hi, cudaStream_t st);
+// dst[c][r] = src[r][c] (+ dst if accumulate), for r < R, c < C; dst padding columns (r >= R) zeroed.
+void launch_transpose(const double* src, int64_t R, int64_t C, int64_t lds, double* dst, int64_t ldd, int64_t dst_rows,
+                      int accumulate, cudaStream_t st);
+// one-body + e_core sigma for sectors without an opposite-spin term (n_alpha == 0 or n_beta == 0)
+void launch_onebody(const double* x, double* y, const Excitation* la, int La, const Excitation* lb, int Lb,
+                    const double* h1, int norb, int64_t NA, int64_t NB, int64_t ld, double e_core, int accumulate,
+                    cudaStream_t st);
+
+// ---- vec.cu: fused HBM passes of the SBCI update (K7-K9) ----
+constexpr int kMaxIn = 10, kMaxOut = 5, kMaxDot = 16;
+struct LinArgs {
+    int64_t n;  // doubles per vector (padded local length, even)
+    int nin, nout, ndot;
+    const double* in[kMaxIn];
+    double* out[kMaxOut];
+    // out[j] = sum_s coef[j][s] * slot[s], slots 0..9 = inputs, 10..14 = outputs already computed (j' < j);
+    // out[j] may be null (value only used by later outputs / dots)
+    double coef[kMaxOut][kMaxIn + kMaxOut];
+    unsigned char da[kMaxDot], db[kMaxDot];  // dot slots
+};
+struct ReduceWs {
+    double* partial;  // [grid][kMaxDot]
+    double* result;   // [kMaxDot] device
+    double* host;     // pinned [kMaxDot]
+    int grid;
+};
+// returns nothing; results land in ws.result (device). Caller copies to host after collectives.
+void launch_lincomb(const LinArgs& a, const ReduceWs& ws, cudaStream_t st);
+// z = zres / den(D - shift) - sum_c o_c xc_c ; with dots per LinArgs-like slot spec on (zres=0, D=1, x=2, y=3, z_out=8)
+struct PrecArgs {
+    int64_t n;
+    const double* zres;
+    const double* D;
+    double shift, clamp;
+    int nxc;
+    const double* xc[8];
+    double o[8];     // overlaps to subtract (used when mode == 1)
+    int mode;        // 0: only compute overlaps xc_c . (zres/den) ; 1: write z and compute dots
+    double* z;
+    const double* x;
+    const double* y;  // may be null
+};
+void launch_precond(const PrecArgs& a, const ReduceWs& ws, cudaStream_t st);
+// subspace matrix of the materialized basis (sbci1.hpp:193-219): returns V00,V01,V11 (two) or
+// V00,V01,V02,V11,V12,V22 (three)
+struct SubArgs {
+    int64_t n;
+    const double *x, *y, *z, *hx, *hy, *hz;
+    double Ax, Bx, By, Cx, Cy, Cz;
+    int three;
+};
+void launch_subspace(const SubArgs& a, const ReduceWs& ws, cudaStream_t st);
+// generic deterministic dot/norm reductions finish: partials -> result
+void launch_reduce_finish(const ReduceWs& ws, int ndot, cudaStream_t st);
+// argmin with index tie-break over a padded matrix (valid cols < ncols), excluding (value,index) <= prev
+void launch_argmin_after(const double* D, int64_t nrows, int64_t ncols, int64_t ld, int64_t row_lo, double prev_v,
+                         int64_t prev_i, double* out_v, int64_t* out_i, double* part_v, int64_t* part_i, int grid,
+                         cudaStream_t st);
+void launch_kinetic(const double* y, const double* D, double shift, int64_t n, const ReduceWs& ws, cudaStream_t st);
+void launch_fill(double* p, int64_t n, double v, cudaStream_t st);
+void launch_set_element(double* p, int64_t idx, double v, cudaStream_t st);
+
+// ---- selftest.cu ----
+int run_mma_selftest();
+
+}  // namespace sbg

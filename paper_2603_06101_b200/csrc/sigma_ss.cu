@@ -1,0 +1,252 @@
+// sigma_ss.cu — K4/K5: same-spin two-body sigma terms through the (n-2)-electron intermediate,
+// plus the tiled transposes that turn the beta-beta term into an alpha-alpha one, and the
+// one-body kernel used only for sectors without an opposite-spin term.
+//
+// Normal-ordered same-spin two-body operator (the reference carries it inside its spin-summed
+// h2e, fci/sigma.hpp:56-81 / 86-137):
+//   1/2 sum (pq|rs) a+_p a+_r a_s a_q = sum_{p<r, q<s} W(pr,qs) a+_p a+_r a_s a_q,
+//   W(pr,qs) = (pq|rs) - (ps|rq).
+// Resolving through K = (n-2)-electron strings:
+//   sigma(I,:) += sum_K phi(K;pr) W(pr,qs) phi(K;qs) c(J,:),  I = K+{p,r}, J = K+{q,s},
+//   phi(K;q,s) = <K|a_s a_q|K+{q,s}> = (-1)^(pop_below(J,q) + pop_below(J-q,s)).
+// Per K that is a dense (P x P) x (P x ncols) DGEMM with P = C(norb-n+2, 2) gathered rows and P
+// scattered rows; the batch dimension (the other spin) is contiguous, so gathers are coalesced
+// row reads and the scatter is a coalesced fp64 reduction (red.global.add.f64) into L2.
+#include <algorithm>
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace sbg {
+
+namespace {
+
+constexpr int NTS = 64;         // batch columns per tile
+constexpr int XSTRIDE = NTS + 4;
+constexpr int TILES_PER_CTA = 4;
+
+struct SsParams {
+    const double* x;
+    double* y;
+    const double* Va;
+    int norb, nel, P, npa;
+    int64_t ldx, col_lo, col_hi;
+};
+
+template <int KSS>
+__global__ void __launch_bounds__(128) k_sigma_ss(const SsParams p) {
+    constexpr int KPP = KSS * 4;
+    extern __shared__ __align__(16) double smem[];
+    double* Xs = smem;                        // [KPP][XSTRIDE]
+    const int ysrows = max(KPP, 16 * (int)(blockDim.x >> 5));
+    double* Ys = Xs + KPP * XSTRIDE;          // [ysrows][NTS]
+    int* sJ = reinterpret_cast<int*>(Ys + ysrows * NTS);
+    int* sPi = sJ + KPP;
+    double* sPhi = reinterpret_cast<double*>(sPi + KPP);
+
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int w = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    const int P = p.P, norb = p.norb;
+    const uint64_t K = string_unrank(blockIdx.x, p.nel - 2, norb);
+    const uint64_t full = ((uint64_t)1 << norb) - 1;
+
+    for (int i = tid; i < KPP; i += nthr) {
+        int J = -1, pi = 0;
+        double phi = 0.0;
+        if (i < P) {
+            // i-th pair (q<s) of the empty orbitals of K, lexicographic in (s, q)
+            const uint64_t vac = ~K & full;
+            int cnt = 0, q = -1, s = -1;
+            for (uint64_t ms = vac; ms && q < 0; ms &= ms - 1) {
+                const int ss = __ffsll((long long)ms) - 1;
+                for (uint64_t mq = vac & (((uint64_t)1 << ss) - 1); mq; mq &= mq - 1) {
+                    if (cnt == i) {
+                        q = __ffsll((long long)mq) - 1;
+                        s = ss;
+                        break;
+                    }
+                    ++cnt;
+                }
+            }
+            const uint64_t Jm = K | ((uint64_t)1 << q) | ((uint64_t)1 << s);
+            J = (int)string_rank(Jm);
+            phi = ((pop_below(Jm, q) + pop_below(Jm ^ ((uint64_t)1 << q), s)) & 1) ? -1.0 : 1.0;
+            pi = pair_strict(q, s);
+        }
+        sJ[i] = J;
+        sPi[i] = pi;
+        sPhi[i] = phi;
+    }
+    __syncthreads();
+    if (sJ[0] < 0) return;  // no pairs (cannot happen for P >= 1)
+    for (int i = tid; i < KPP; i += nthr)
+        if (i >= P) sJ[i] = sJ[0];  // padding rows read a valid row; their A entries are zero
+
+    double a0[KSS], a1[KSS];
+    const int i0 = 16 * w + g;
+#pragma unroll
+    for (int j = 0; j < KSS; ++j) {
+        const int jj = 4 * j + t;
+        a0[j] = (i0 < P && jj < P) ? sPhi[i0] * sPhi[jj] * p.Va[(size_t)sPi[i0] * p.npa + sPi[jj]] : 0.0;
+        a1[j] = (i0 + 8 < P && jj < P) ? sPhi[i0 + 8] * sPhi[jj] * p.Va[(size_t)sPi[i0 + 8] * p.npa + sPi[jj]] : 0.0;
+    }
+    __syncthreads();
+
+    const int64_t c_begin = p.col_lo + (int64_t)blockIdx.y * TILES_PER_CTA * NTS;
+    for (int tt = 0; tt < TILES_PER_CTA; ++tt) {
+        const int64_t c0 = c_begin + (int64_t)tt * NTS;
+        if (c0 >= p.col_hi) break;
+        for (int c = tid; c < KPP * (NTS / 2); c += nthr) {
+            const int k = c / (NTS / 2), part = c % (NTS / 2);
+            cp_async16(Xs + k * XSTRIDE + part * 2, p.x + (int64_t)sJ[k] * p.ldx + c0 + part * 2);
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncthreads();
+        double acc[NTS / 8][4];
+#pragma unroll
+        for (int nb = 0; nb < NTS / 8; ++nb)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[nb][e] = 0.0;
+#pragma unroll
+        for (int j = 0; j < KSS; ++j) {
+            const double* Xk = Xs + (4 * j + t) * XSTRIDE + g;
+#pragma unroll
+            for (int nb = 0; nb < NTS / 8; ++nb) dmma_16x8x4(acc[nb], a0[j], a1[j], Xk[nb * 8]);
+        }
+#pragma unroll
+        for (int nb = 0; nb < NTS / 8; ++nb) {
+            const int col = nb * 8 + 2 * t;
+            Ys[i0 * NTS + col] = acc[nb][0];
+            Ys[i0 * NTS + col + 1] = acc[nb][1];
+            Ys[(i0 + 8) * NTS + col] = acc[nb][2];
+            Ys[(i0 + 8) * NTS + col + 1] = acc[nb][3];
+        }
+        __syncthreads();
+        const int64_t ncol = std::min<int64_t>(NTS, p.col_hi - c0);
+        for (int idx = tid; idx < P * NTS; idx += nthr) {
+            const int i = idx / NTS, c = idx % NTS;
+            if (c < ncol) red_add_f64(p.y + (int64_t)sJ[i] * p.ldx + c0 + c, Ys[idx]);
+        }
+        __syncthreads();
+    }
+}
+
+template <int KSS>
+void launch_kss(const SsPlan& pl, const SsParams& prm, dim3 grid, cudaStream_t st) {
+    auto kern = k_sigma_ss<KSS>;
+    static thread_local int configured = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (configured != dev) {
+        SBG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+        configured = dev;
+    }
+    kern<<<grid, pl.warps * 32, pl.smem, st>>>(prm);
+    SBG_LAUNCH_CHECK();
+}
+
+// 32x32 tiled transpose of fp64 with a padded shared tile
+__global__ void k_transpose(const double* __restrict__ src, int64_t R, int64_t C, int64_t lds, double* __restrict__ dst,
+                            int64_t ldd, int64_t dst_rows, int accumulate) {
+    __shared__ double tile[32][33];
+    const int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;  // src rows / cols
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int64_t r = r0 + i, c = c0 + threadIdx.x;
+        tile[i][threadIdx.x] = (r < R && c < C) ? src[r * lds + c] : 0.0;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int64_t c = c0 + i, r = r0 + threadIdx.x;  // dst row c, dst col r
+        if (c < dst_rows && r < ldd) {
+            double v = tile[threadIdx.x][i];
+            if (accumulate) v += dst[c * ldd + r];
+            dst[c * ldd + r] = v;
+        }
+    }
+}
+
+// sigma += h-part for sectors where one spin is empty (no alpha-beta kernel to fold it into):
+// y(Ia,Ib) = [y] + e_core x + sum_{l in links_a(Ia)} s h_{p q} x(J,Ib) + sum_{m in links_b(Ib)} s h x(Ia,J)
+__global__ void k_onebody(const double* x, double* y, const Excitation* la, int La, const Excitation* lb, int Lb,
+                          const double* h1, int norb, int64_t NA, int64_t NB, int64_t ld, double e_core,
+                          int accumulate) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= NA * ld) return;
+    const int64_t ia = idx / ld, ib = idx % ld;
+    double v = 0.0;
+    if (ib < NB) {
+        v = e_core * x[idx];
+        for (int l = 0; l < La; ++l) {
+            const Excitation e = la[ia * La + l];
+            v += e.sign * h1[e.p * norb + e.q] * x[(int64_t)e.target * ld + ib];
+        }
+        for (int l = 0; l < Lb; ++l) {
+            const Excitation e = lb[ib * Lb + l];
+            v += e.sign * h1[e.p * norb + e.q] * x[ia * ld + e.target];
+        }
+        if (accumulate) v += y[idx];
+    }
+    y[idx] = v;
+}
+
+}  // namespace
+
+SsPlan plan_sigma_ss(int norb, int nel) {
+    SsPlan pl{};
+    pl.norb = norb;
+    pl.nel = nel;
+    pl.npa = norb * (norb - 1) / 2;
+    if (nel < 2) {
+        pl.P = 0;
+        pl.NK = 0;
+        return pl;
+    }
+    const int nv = norb - nel + 2;
+    pl.P = nv * (nv - 1) / 2;
+    pl.NK = (int64_t)binom_host_calc(norb, nel - 2);
+    pl.KSS = (pl.P + 3) / 4;
+    pl.warps = (pl.P + 15) / 16;
+    const int KPP = pl.KSS * 4;
+    const int rows = std::max(KPP, 16 * pl.warps);
+    pl.smem = (size_t)KPP * XSTRIDE * 8 + (size_t)rows * NTS * 8 + (size_t)KPP * 8 + (size_t)KPP * 8 + 16;
+    if (pl.KSS > 16 || pl.warps > 4) throw InvalidArgument("sigma_ss: orbital space too large for this build");
+    return pl;
+}
+
+void launch_sigma_ss(const SsPlan& pl, const double* x, double* y, const double* Va, int64_t ldx, int64_t col_lo,
+                     int64_t col_hi, cudaStream_t st) {
+    ensure_binomials();
+    if (pl.P == 0 || pl.NK == 0 || col_hi <= col_lo) return;
+    SsParams prm{x, y, Va, pl.norb, pl.nel, pl.P, pl.npa, ldx, col_lo, col_hi};
+    const int64_t ncols = col_hi - col_lo;
+    const int64_t gy = (ncols + TILES_PER_CTA * NTS - 1) / (TILES_PER_CTA * NTS);
+    dim3 grid((unsigned)pl.NK, (unsigned)gy);
+    switch (pl.KSS) {
+#define SBG_KSS(n) \
+    case n: launch_kss<n>(pl, prm, grid, st); break;
+        SBG_KSS(1) SBG_KSS(2) SBG_KSS(3) SBG_KSS(4) SBG_KSS(5) SBG_KSS(6) SBG_KSS(7) SBG_KSS(8) SBG_KSS(9)
+        SBG_KSS(10) SBG_KSS(11) SBG_KSS(12) SBG_KSS(13) SBG_KSS(14) SBG_KSS(15) SBG_KSS(16)
+#undef SBG_KSS
+        default: throw InvalidArgument("sigma_ss: unsupported pair count");
+    }
+}
+
+void launch_transpose(const double* src, int64_t R, int64_t C, int64_t lds, double* dst, int64_t ldd, int64_t dst_rows,
+                      int accumulate, cudaStream_t st) {
+    // grid over src tiles covering rows [0, max(R, ldd)) so that dst padding columns are written
+    const int64_t rr = std::max(R, ldd), cc = std::max(C, dst_rows);
+    dim3 grid((unsigned)((rr + 31) / 32), (unsigned)((cc + 31) / 32));
+    k_transpose<<<grid, dim3(32, 8), 0, st>>>(src, R, C, lds, dst, ldd, dst_rows, accumulate);
+    SBG_LAUNCH_CHECK();
+}
+
+void launch_onebody(const double* x, double* y, const Excitation* la, int La, const Excitation* lb, int Lb,
+                    const double* h1, int norb, int64_t NA, int64_t NB, int64_t ld, double e_core, int accumulate,
+                    cudaStream_t st) {
+    const int64_t n = NA * ld;
+    k_onebody<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, y, la, La, lb, Lb, h1, norb, NA, NB, ld, e_core,
+                                                            accumulate);
+    SBG_LAUNCH_CHECK();
+}
+
+}  // namespace sbg

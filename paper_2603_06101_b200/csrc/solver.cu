@@ -1,0 +1,705 @@
+// solver.cu — the SBCI1 driver on device-resident vectors (reference: sbci1.hpp:45-579,
+// precond.hpp:19-111). Structure and scalar logic follow the reference line by line; the vector
+// work is issued as fused passes (vec.cu) whose dot products are the only data that crosses to
+// the host each step.
+#include "solver.hpp"
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <optional>
+
+namespace sbg {
+
+namespace {
+
+constexpr int kSbci1DefaultMaxCycle = 20;
+
+// ------------------------------------------------------------------ fused pass builder
+struct Lin {
+    LinArgs a{};
+    Lin() { std::memset(&a, 0, sizeof(a)); }
+    int in(const double* p) {
+        a.in[a.nin] = p;
+        return a.nin++;
+    }
+    // out = sum coef*slot, returns slot id of the output
+    int out(double* p, std::initializer_list<std::pair<int, double>> terms) {
+        const int j = a.nout++;
+        a.out[j] = p;
+        for (auto& t : terms) a.coef[j][t.first] = t.second;
+        return kMaxIn + j;
+    }
+    int dot(int s1, int s2) {
+        a.da[a.ndot] = (unsigned char)s1;
+        a.db[a.ndot] = (unsigned char)s2;
+        return a.ndot++;
+    }
+    std::vector<double> run(Context& c) {
+        a.n = c.padded_len();
+        launch_lincomb(a, c.rws, c.st);
+        c.launches += 1 + (a.ndot > 0);
+        std::vector<double> r(a.ndot);
+        if (a.ndot > 0) {
+            const double* h = c.finish_dots(a.ndot);
+            std::copy(h, h + a.ndot, r.begin());
+        }
+        return r;
+    }
+};
+
+struct Seed {
+    DBuf x, hx;
+    double energy = 0.0;
+};
+
+class Ops {
+public:
+    explicit Ops(Context& c) : c_(c) {}
+    Context& c_;
+
+    double dot(const DBuf& u, const DBuf& v) {
+        Lin L;
+        const int a = L.in(u.p), b = L.in(v.p);
+        L.dot(a, b);
+        return L.run(c_)[0];
+    }
+    double norm(const DBuf& u) { return std::sqrt(dot(u, u)); }
+    void scale(DBuf& u, double s) {  // u *= s (vector_ops.hpp:42-44)
+        Lin L;
+        const int a = L.in(u.p);
+        L.out(u.p, {{a, s}});
+        L.run(c_);
+    }
+    void scale2(DBuf& u, DBuf& v, double s) {
+        Lin L;
+        const int a = L.in(u.p), b = L.in(v.p);
+        L.out(u.p, {{a, s}});
+        L.out(v.p, {{b, s}});
+        L.run(c_);
+    }
+    void copy(DBuf& dst, const DBuf& src) {
+        SBG_CUDA(cudaMemcpyAsync(dst.p, src.p, c_.padded_len() * 8, cudaMemcpyDeviceToDevice, c_.st));
+    }
+    DBuf clone(const DBuf& src) {
+        DBuf d(c_.padded_len());
+        copy(d, src);
+        return d;
+    }
+    void zero(DBuf& u) { SBG_CUDA(cudaMemsetAsync(u.p, 0, c_.padded_len() * 8, c_.st)); }
+    // r = a*u + b*v (combine, vector_ops.hpp:53-58)
+    void combine(DBuf& r, double a, const DBuf& u, double b, const DBuf& v) {
+        Lin L;
+        const int su = L.in(u.p), sv = L.in(v.p);
+        L.out(r.p, {{su, a}, {sv, b}});
+        L.run(c_);
+    }
+    void apply(const DBuf& x, DBuf& y) { c_.sigma(x, y); }
+
+    // global element read / unit vector (rank-aware)
+    double read(const DBuf& v, int64_t gidx) {
+        const int64_t row = gidx / c_.NB, col = gidx % c_.NB;
+        double* r = c_.rws.result;
+        if (row >= c_.row_lo && row < c_.row_hi)
+            SBG_CUDA(cudaMemcpyAsync(r, v.p + (row - c_.row_lo) * c_.ld + col, 8, cudaMemcpyDeviceToDevice, c_.st));
+        else
+            SBG_CUDA(cudaMemsetAsync(r, 0, 8, c_.st));
+        return c_.finish_dots(1)[0];
+    }
+    void set_unit(DBuf& v, int64_t gidx) {
+        zero(v);
+        const int64_t row = gidx / c_.NB, col = gidx % c_.NB;
+        if (row >= c_.row_lo && row < c_.row_hi) {
+            launch_set_element(v.p, (row - c_.row_lo) * c_.ld + col, 1.0, c_.st);
+            c_.launches++;
+        }
+    }
+    // n smallest diagonal entries, ties by index (the stable_sort of sbci1.hpp:50-53)
+    std::vector<int64_t> lowest_diagonal(int n) {
+        const int grid = c_.rws.grid;
+        double* pv;
+        int64_t* pi;
+        SBG_CUDA(cudaMalloc(&pv, grid * 8));
+        SBG_CUDA(cudaMalloc(&pi, grid * 8));
+        std::vector<double> hv(grid);
+        std::vector<int64_t> hi(grid);
+        std::vector<int64_t> out;
+        double prev_v = -std::numeric_limits<double>::infinity();
+        int64_t prev_i = -1;
+        for (int k = 0; k < n; ++k) {
+            launch_argmin_after(c_.diagonal().p, c_.nrows, c_.NB, c_.ld, c_.row_lo, prev_v, prev_i, nullptr, nullptr,
+                                pv, pi, grid, c_.st);
+            c_.launches++;
+            SBG_CUDA(cudaMemcpyAsync(hv.data(), pv, grid * 8, cudaMemcpyDeviceToHost, c_.st));
+            SBG_CUDA(cudaMemcpyAsync(hi.data(), pi, grid * 8, cudaMemcpyDeviceToHost, c_.st));
+            SBG_CUDA(cudaStreamSynchronize(c_.st));
+            double bv = std::numeric_limits<double>::max();
+            int64_t bi = std::numeric_limits<int64_t>::max();
+            for (int b = 0; b < grid; ++b)
+                if (hv[b] < bv || (hv[b] == bv && hi[b] < bi)) {
+                    bv = hv[b];
+                    bi = hi[b];
+                }
+            if (c_.world > 1) {
+                // all ranks' candidates: gather (value, index) through the dot buffer
+                std::vector<double> all(2 * c_.world, 0.0);
+                all[2 * c_.rank] = bv;
+                all[2 * c_.rank + 1] = (double)bi;
+                // sum-allreduce of a one-hot layout == allgather
+                SBG_CUDA(cudaMemcpyAsync(c_.rws.result, all.data(), all.size() * 8, cudaMemcpyHostToDevice, c_.st));
+                const double* h = c_.finish_dots((int)all.size());
+                for (int r = 0; r < c_.world; ++r) {
+                    const double v = h[2 * r];
+                    const int64_t i = (int64_t)h[2 * r + 1];
+                    if (v < bv || (v == bv && i < bi)) {
+                        bv = v;
+                        bi = i;
+                    }
+                }
+            }
+            out.push_back(bi);
+            prev_v = bv;
+            prev_i = bi;
+        }
+        cudaFree(pv);
+        cudaFree(pi);
+        return out;
+    }
+};
+
+// ------------------------------------------------------------------ preconditioner & deflation
+struct Precond {  // GroundShiftPreconditioner (precond.hpp:19-47)
+    const DBuf* D;
+    double shift, clamp;
+    void update_shift(double e) {
+        if (!std::isfinite(e)) throw std::invalid_argument("update_shift: E must be finite");
+        shift = e;
+    }
+};
+
+struct Deflation {  // DeflationSet (precond.hpp:54-102) with cached images
+    struct Member {
+        DBuf x, hx;
+        double e;
+    };
+    std::vector<Member> m;
+    bool empty() const { return m.empty(); }
+    size_t size() const { return m.size(); }
+
+    void add_with_image(Ops& o, DBuf x, DBuf hx, double e) {
+        const double n = o.norm(x);
+        if (std::abs(n - 1.0) > 1e-12) throw std::invalid_argument("DeflationSet::add: vector must be unit norm");
+        for (auto& mm : m)
+            if (std::abs(o.dot(mm.x, x)) > 1e-10)
+                throw std::invalid_argument("DeflationSet::add: vector not orthogonal to stored set");
+        m.push_back({std::move(x), std::move(hx), e});
+    }
+    // v -= x_i (x_i . v), sequentially over members (precond.hpp:78-80)
+    void project_out(Ops& o, DBuf& v) {
+        for (auto& mm : m) {
+            const double ov = o.dot(mm.x, v);
+            Lin L;
+            const int sv = L.in(v.p), sx = L.in(mm.x.p);
+            L.out(v.p, {{sv, 1.0}, {sx, -ov}});
+            L.run(o.c_);
+        }
+    }
+    // precond.hpp:84-93
+    void project_out_pair(Ops& o, DBuf& v, DBuf& hv) {
+        for (auto& mm : m) {
+            const double ov = o.dot(mm.x, v);
+            Lin L;
+            const int sv = L.in(v.p), sx = L.in(mm.x.p), sh = L.in(hv.p), shx = L.in(mm.hx.p);
+            L.out(v.p, {{sv, 1.0}, {sx, -ov}});
+            L.out(hv.p, {{sh, 1.0}, {shx, -ov}});
+            L.run(o.c_);
+        }
+    }
+};
+
+// ------------------------------------------------------------------ state
+struct State {  // Sbci1State (sbci1.hpp:95-105)
+    int alpha = 0, t = 0;
+    DBuf x, hx, y, hy, zres;
+    double energy = 0.0;
+    double b_prev = 1.0, c_prev = 0.0, k_prev = 1.0;
+    int restart_count = 0;
+    long total_iterations = 0;
+};
+
+struct StepData {
+    StepOutcome outcome;
+    double dE = 0.0, dz = 0.0;
+    bool have_ritz = false;
+    double sx = 0, sy = 0, sz = 0, b = 0, c = 0, ritz_e = 0;
+    bool three = false;
+    bool committed = false;
+    double x_norm = 0.0;  // |x| after the step (valid when committed)
+};
+
+std::optional<RestartReason> check_restart(int alpha, double b, double dE, double x_norm, double dz, int t,
+                                           const SolverConfig& cfg, int max_cycle) {  // sbci1.hpp:109-117
+    if (alpha > 0 && std::abs(b) < cfg.b_th && dE < cfg.eps1) return RestartReason::StallSmallB;
+    if (x_norm < cfg.x_th1 || x_norm > cfg.x_th2) return RestartReason::NormOutOfRange;
+    if (dz > cfg.r1 && t > 0) return RestartReason::ResidualBlowup;
+    if (t + 1 >= max_cycle) return RestartReason::MaxCycle;
+    return std::nullopt;
+}
+
+class Driver {
+public:
+    Driver(Context& c, const SolverConfig& cfg, const std::function<void(const TraceRec&)>& trace)
+        : c_(c), o_(c), cfg_(cfg), trace_(trace), z_(c.padded_len()), hz_(c.padded_len()) {}
+
+    // z = (1 - sum x_c x_c^T)(D - E0)^-1 zres with the Gram-Schmidt dots (precond.hpp:106-111)
+    std::vector<double> make_z(const State& st, const Precond& pre, const Deflation& defl, bool with_y) {
+        PrecArgs pa{};
+        pa.n = c_.padded_len();
+        pa.zres = st.zres.p;
+        pa.D = pre.D->p;
+        pa.shift = pre.shift;
+        pa.clamp = pre.clamp;
+        pa.nxc = (int)defl.size();
+        for (size_t i = 0; i < defl.size(); ++i) pa.xc[i] = defl.m[i].x.p;
+        if (pa.nxc > 0) {
+            pa.mode = 0;
+            launch_precond(pa, c_.rws, c_.st);
+            c_.launches += 2;
+            const double* h = c_.finish_dots(pa.nxc);
+            for (int i = 0; i < pa.nxc; ++i) pa.o[i] = h[i];
+        }
+        pa.mode = 1;
+        pa.z = z_.p;
+        pa.x = st.x.p;
+        pa.y = with_y ? st.y.p : nullptr;
+        launch_precond(pa, c_.rws, c_.st);
+        c_.launches += 2;
+        const int nd = with_y ? 6 : 3;
+        const double* h = c_.finish_dots(nd);
+        return std::vector<double>(h, h + nd);  // xx, xz, zz [, xy, yy, yz]
+    }
+
+    // sbci1_step_impl (sbci1.hpp:147-323)
+    StepData step(State& st, const Precond& pre, Deflation& defl, int max_cycle) {
+        StepData out;
+        bool use_three = st.t >= 1;
+        const auto d = make_z(st, pre, defl, use_three);
+        const double nxx = d[0], nxz = d[1], nzz = d[2];
+        if (std::sqrt(nzz) < cfg_.lindep * std::sqrt(nxx)) {
+            const double xhx = o_.dot(st.x, st.hx);
+            if (nxx == 0.0) throw std::invalid_argument("rayleigh_quotient: zero vector");
+            st.energy = xhx / nxx;
+            out.outcome = StepOutcome::converged();
+            out.dE = 0.0;
+            out.dz = o_.norm(st.zres);
+            out.x_norm = std::sqrt(nxx);
+            return out;
+        }
+        GramSchmidtCoeffs gs;
+        if (use_three) {
+            gs = gram_schmidt_from_dots(nxx, d[3], d[4], nxz, d[5], nzz, true, cfg_.lindep);
+            if (gs.y_degenerate) use_three = false;
+            else if (gs.z_degenerate) {
+                out.outcome = StepOutcome::restart(RestartReason::StallSmallB);
+                return out;
+            }
+        }
+        if (!use_three) {
+            gs = gram_schmidt_from_dots(nxx, 0.0, 0.0, nxz, 0.0, nzz, false, cfg_.lindep);
+            if (gs.z_degenerate) {
+                out.outcome = StepOutcome::restart(RestartReason::StallSmallB);
+                return out;
+            }
+        }
+        o_.apply(z_, hz_);
+
+        SubArgs sa{};
+        sa.n = c_.padded_len();
+        sa.x = st.x.p;
+        sa.y = st.y.p;
+        sa.z = z_.p;
+        sa.hx = st.hx.p;
+        sa.hy = st.hy.p;
+        sa.hz = hz_.p;
+        sa.Ax = gs.A_x;
+        sa.Bx = gs.B_x;
+        sa.By = gs.B_y;
+        sa.Cx = gs.C_x;
+        sa.Cy = gs.C_y;
+        sa.Cz = gs.C_z;
+        sa.three = use_three;
+        launch_subspace(sa, c_.rws, c_.st);
+        c_.launches += 2;
+        const int m = use_three ? 3 : 2;
+        const double* h = c_.finish_dots(m * m);
+        SmallMatrix v(m);
+        for (int i = 0; i < m; ++i)
+            for (int j = i; j < m; ++j) v(i, j) = v(j, i) = 0.5 * (h[i * m + j] + h[j * m + i]);
+        const SmallEigResult eig = jacobi_symmetric_eig(v);
+
+        const double vx = eig.eigenvectors(0, 0), vy = use_three ? eig.eigenvectors(1, 0) : 0.0,
+                     vz = eig.eigenvectors(m - 1, 0);
+        const double wx = eig.eigenvectors(0, 1), wy = use_three ? eig.eigenvectors(1, 1) : 0.0,
+                     wz = eig.eigenvectors(m - 1, 1);
+        const double e_new = eig.eigenvalues[0];
+        const double k_den = vx * gs.A_x + vy * gs.B_x + vz * gs.C_x;
+        if (std::abs(k_den) < 1e-14) {
+            out.outcome = StepOutcome::restart(RestartReason::StallSmallB);
+            return out;
+        }
+        const double k = 1.0 / k_den;
+        double b, c;
+        if (use_three) {
+            const double b_den = vy * gs.B_y + vz * gs.C_y;
+            if (std::abs(b_den) < 1e-14) {
+                out.outcome = StepOutcome::restart(RestartReason::StallSmallB);
+                return out;
+            }
+            b = k * b_den;
+            c = -vz * gs.C_z / b_den;
+        } else {
+            b = 1.0;
+            c = -k * vz * gs.C_z;
+        }
+        // cancellation guard (sbci1.hpp:259-262): norms of y' and x' before committing
+        {
+            Lin L;
+            const int sx = L.in(st.x.p), sy = L.in(st.y.p), sz = L.in(z_.p);
+            const int yn = use_three ? L.out(nullptr, {{sy, 1.0}, {sz, -c}}) : L.out(nullptr, {{sz, -c}});
+            const int xn = L.out(nullptr, {{sx, 1.0}, {yn, b}});
+            L.dot(yn, yn);
+            L.dot(xn, xn);
+            const auto r = L.run(c_);
+            if (std::sqrt(nxx) + std::abs(b) * std::sqrt(r[0]) > 1e6 * std::max(std::sqrt(r[1]), 1e-300)) {
+                out.outcome = StepOutcome::restart(RestartReason::StallSmallB);
+                return out;
+            }
+        }
+        // commit (sbci1.hpp:263-267): y' = y - c z, Hy' = Hy - c Hz, x' = x + b y', Hx' = Hx + b Hy',
+        // z' = (1/k) Hx' - (E'/k) x'; reductions |z'|^2, |x'|^2 and the deflation overlaps x_c . z'
+        double zz2, xx2;
+        std::vector<double> ovl;
+        {
+            Lin L;
+            const int sx = L.in(st.x.p), sy = L.in(st.y.p), sz = L.in(z_.p), shx = L.in(st.hx.p),
+                      shy = L.in(st.hy.p), shz = L.in(hz_.p);
+            std::vector<int> sxc;
+            for (auto& mm : defl.m) sxc.push_back(L.in(mm.x.p));
+            const int yn = use_three ? L.out(st.y.p, {{sy, 1.0}, {sz, -c}}) : L.out(st.y.p, {{sz, -c}});
+            const int hyn = use_three ? L.out(st.hy.p, {{shy, 1.0}, {shz, -c}}) : L.out(st.hy.p, {{shz, -c}});
+            const int xn = L.out(st.x.p, {{sx, 1.0}, {yn, b}});
+            const int hxn = L.out(st.hx.p, {{shx, 1.0}, {hyn, b}});
+            const int zn = L.out(st.zres.p, {{hxn, 1.0 / k}, {xn, -e_new / k}});
+            L.dot(zn, zn);
+            L.dot(xn, xn);
+            for (int s : sxc) L.dot(s, zn);
+            const auto r = L.run(c_);
+            zz2 = r[0];
+            xx2 = r[1];
+            ovl.assign(r.begin() + 2, r.end());
+        }
+        out.committed = true;
+        out.dE = std::abs(e_new - st.energy);
+        out.dz = std::sqrt(zz2);
+        out.x_norm = std::sqrt(xx2);
+        double dz_defl = out.dz;
+        if (!defl.empty()) {  // |(1 - sum x_c x_c^T) z'| (sbci1.hpp:274-279)
+            Lin L;
+            const int sz = L.in(st.zres.p);
+            std::vector<std::pair<int, double>> terms{{sz, 1.0}};
+            std::vector<int> sxc;
+            for (size_t i = 0; i < defl.size(); ++i) sxc.push_back(L.in(defl.m[i].x.p));
+            LinArgs& A = L.a;
+            const int j = A.nout++;
+            A.out[j] = nullptr;
+            A.coef[j][sz] = 1.0;
+            for (size_t i = 0; i < sxc.size(); ++i) A.coef[j][sxc[i]] = -ovl[i];
+            L.dot(kMaxIn + j, kMaxIn + j);
+            dz_defl = std::sqrt(L.run(c_)[0]);
+        }
+        st.energy = e_new;
+        st.b_prev = b;
+        st.c_prev = c;
+        st.k_prev = k;
+        // second-lowest Ritz vector coefficients (sbci1.hpp:287-311); materialized only on convergence
+        out.have_ritz = true;
+        out.sx = wx * gs.A_x + wy * gs.B_x + wz * gs.C_x;
+        out.sy = wy * gs.B_y + wz * gs.C_y;
+        out.sz = wz * gs.C_z;
+        out.b = b;
+        out.c = c;
+        out.three = use_three;
+        out.ritz_e = eig.eigenvalues[1];
+
+        if (out.dE < cfg_.eps0 && std::min(out.dz, dz_defl) < cfg_.r0) {
+            out.outcome = StepOutcome::converged();
+            return out;
+        }
+        if (auto reason = check_restart(st.alpha, b, out.dE, out.x_norm, out.dz, st.t, cfg_, max_cycle)) {
+            out.outcome = StepOutcome::restart(*reason);
+            return out;
+        }
+        out.outcome = StepOutcome::cont();
+        return out;
+    }
+
+    // the converged step's second Ritz vector (sbci1.hpp:287-311), rebuilt from x_{t+1}, y_{t+1},
+    // z, Hz: x_t = x - b y, y_t = y + c z, s = sx x_t + sy y_t + sz z (same summation order)
+    Seed second_ritz(const State& st, const StepData& s) {
+        Seed r;
+        r.x = DBuf(c_.padded_len());
+        r.hx = DBuf(c_.padded_len());
+        for (int pass = 0; pass < 2; ++pass) {
+            Lin L;
+            const int sx = L.in(pass ? st.hx.p : st.x.p), sy = L.in(pass ? st.hy.p : st.y.p),
+                      sz = L.in(pass ? hz_.p : z_.p);
+            const int xt = L.out(nullptr, {{sx, 1.0}, {sy, -s.b}});
+            const int yt = L.out(nullptr, {{sy, 1.0}, {sz, s.c}});
+            const int zc = L.out(nullptr, {{sz, 1.0}});
+            if (s.three) L.out(pass ? r.hx.p : r.x.p, {{xt, s.sx}, {yt, s.sy}, {zc, s.sz}});
+            else L.out(pass ? r.hx.p : r.x.p, {{xt, s.sx}, {zc, s.sz}});
+            L.run(c_);
+        }
+        r.energy = s.ritz_e;
+        return r;
+    }
+
+    StepData last_;
+    Context& c_;
+    Ops o_;
+    SolverConfig cfg_;
+    const std::function<void(const TraceRec&)>& trace_;
+    DBuf z_, hz_;
+};
+
+struct Sbci1Result {
+    StateResult pair;
+    DBuf converged_image;
+    std::optional<Seed> next_seed;
+    int hx_refreshes = 0;
+};
+
+// solve_state_sbci1 (sbci1.hpp:357-473)
+Sbci1Result solve_state(Driver& dr, Precond& pre, Deflation& defl, Seed seed, int alpha, bool track) {
+    Context& c = dr.c_;
+    Ops& o = dr.o_;
+    const SolverConfig& cfg = dr.cfg_;
+    cfg.validate();
+    const int max_cycle = cfg.effective_max_cycle(kSbci1DefaultMaxCycle);
+    defl.project_out_pair(o, seed.x, seed.hx);
+    const double seed_norm = o.norm(seed.x);
+    if (seed_norm < cfg.lindep) throw std::invalid_argument("solve_state_sbci1: seed collapsed under deflation");
+    o.scale2(seed.x, seed.hx, 1.0 / seed_norm);
+
+    State st;
+    st.alpha = alpha;
+    st.x = std::move(seed.x);
+    st.hx = std::move(seed.hx);
+    st.y = DBuf(c.padded_len());
+    st.hy = DBuf(c.padded_len());
+    st.zres = DBuf(c.padded_len());
+    st.energy = o.dot(st.x, st.hx);
+    o.combine(st.zres, 1.0, st.hx, -st.energy, st.x);
+
+    Sbci1Result result;
+    if (track) pre.update_shift(st.energy);
+    {
+        const auto d = dr.make_z(st, pre, defl, false);
+        if (std::sqrt(d[2]) < cfg.lindep) {
+            result.pair.state = alpha;
+            result.pair.energy = st.energy;
+            result.pair.final_residual = o.norm(st.zres);
+            result.pair.vector = std::move(st.x);
+            result.converged_image = std::move(st.hx);
+            return result;
+        }
+    }
+    while (st.total_iterations < cfg.t_max) {
+        StepData step = dr.step(st, pre, defl, max_cycle);
+        ++st.total_iterations;
+        if (dr.trace_) {
+            TraceRec rec;
+            rec.state = alpha;
+            rec.t = st.t;
+            rec.energy = st.energy;
+            rec.dE = step.dE;
+            rec.res_norm = step.dz;
+            rec.x_norm = step.committed ? step.x_norm : o.norm(st.x);
+            launch_kinetic(st.y.p, pre.D->p, pre.shift, c.padded_len(), c.rws, c.st);
+            c.launches += 2;
+            rec.kinetic = c.finish_dots(1)[0];
+            rec.matvecs = c.applies().load();
+            rec.b = st.b_prev;
+            rec.c = st.c_prev;
+            rec.restart_reason = step.outcome.kind == StepOutcome::Kind::Restart ? (int)step.outcome.reason : -1;
+            dr.trace_(rec);
+        }
+        if (track) pre.update_shift(st.energy);
+        switch (step.outcome.kind) {
+            case StepOutcome::Kind::Converged: {
+                StateResult pair;
+                pair.state = alpha;
+                const double xx = o.dot(st.x, st.x);
+                if (xx == 0.0) throw std::invalid_argument("rayleigh_quotient: zero vector");
+                pair.energy = o.dot(st.x, st.hx) / xx;
+                const double nm = std::sqrt(xx);
+                if (step.have_ritz) result.next_seed = dr.second_ritz(st, step);
+                pair.vector = std::move(st.x);
+                if (nm > 0.0) o.scale(pair.vector, 1.0 / nm);
+                for (auto& mm : defl.m)
+                    if (std::abs(o.dot(mm.x, pair.vector)) > 1e-9)
+                        throw NonConvergenceError(alpha, pair.energy, step.dz);
+                pair.iterations = (int)st.total_iterations;
+                pair.restarts = st.restart_count;
+                pair.final_residual = step.dz;
+                result.pair = std::move(pair);
+                o.scale(st.hx, nm > 0.0 ? 1.0 / nm : 1.0);
+                result.converged_image = std::move(st.hx);
+                return result;
+            }
+            case StepOutcome::Kind::Restart: {
+                double nm = o.norm(st.x);
+                if (nm < cfg.lindep) throw NonConvergenceError(alpha, st.energy, step.dz);
+                o.scale2(st.x, st.hx, 1.0 / nm);
+                if (!defl.empty()) {
+                    defl.project_out_pair(o, st.x, st.hx);
+                    nm = o.norm(st.x);
+                    if (nm < cfg.lindep) throw NonConvergenceError(alpha, st.energy, step.dz);
+                    o.scale2(st.x, st.hx, 1.0 / nm);
+                    st.energy = o.dot(st.x, st.hx);
+                }
+                o.zero(st.y);
+                o.zero(st.hy);
+                ++st.restart_count;
+                if (cfg.hx_refresh_restarts > 0 && st.restart_count % cfg.hx_refresh_restarts == 0) {
+                    o.apply(st.x, st.hx);
+                    ++result.hx_refreshes;
+                }
+                o.combine(st.zres, 1.0, st.hx, -st.energy, st.x);
+                st.t = 0;
+                break;
+            }
+            case StepOutcome::Kind::Continue:
+                ++st.t;
+                break;
+        }
+    }
+    throw NonConvergenceError(alpha, st.energy, o.norm(st.zres));
+}
+
+// init_guess_from_diagonal (sbci1.hpp:45-92)
+std::vector<Seed> init_guess(Context& c, Ops& o, int n) {
+    if (n < 1 || (int64_t)n > c.ndet) throw std::invalid_argument("init_guess_from_diagonal: need 1 <= n <= dim");
+    const auto idx = o.lowest_diagonal(n);
+    std::vector<DBuf> images;
+    {
+        DBuf e(c.padded_len());
+        for (int k = 0; k < n; ++k) {
+            o.set_unit(e, idx[k]);
+            images.emplace_back(c.padded_len());
+            o.apply(e, images.back());
+        }
+    }
+    const int m = n;
+    SmallMatrix proj(m);
+    for (int i = 0; i < m; ++i)
+        for (int j = 0; j < m; ++j) proj(i, j) = o.read(images[j], idx[i]);
+    for (int i = 0; i < m; ++i)
+        for (int j = i + 1; j < m; ++j) {
+            const double s = 0.5 * (proj(i, j) + proj(j, i));
+            proj(i, j) = proj(j, i) = s;
+        }
+    const SmallEigResult eig = jacobi_symmetric_eig(proj);
+    std::vector<Seed> seeds(m);
+    for (int a = 0; a < m; ++a) {
+        Seed& s = seeds[a];
+        s.x = DBuf(c.padded_len());
+        s.hx = DBuf(c.padded_len());
+        for (int i = 0; i < m; ++i) {
+            const int64_t gi = idx[i];
+            const int64_t row = gi / c.NB, col = gi % c.NB;
+            if (row >= c.row_lo && row < c.row_hi) {
+                launch_set_element(s.x.p, (row - c.row_lo) * c.ld + col, eig.eigenvectors(i, a), c.st);
+                c.launches++;
+            }
+        }
+        // hx = sum_i v_ia images_i, accumulated in order (axpy chain)
+        for (int i0 = 0; i0 < m; i0 += kMaxIn - 1) {
+            Lin L;
+            LinArgs& A = L.a;
+            const int j = A.nout++;
+            A.out[j] = s.hx.p;
+            if (i0 > 0) A.coef[j][L.in(s.hx.p)] = 1.0;
+            for (int i = i0; i < std::min(m, i0 + kMaxIn - 1); ++i) A.coef[j][L.in(images[i].p)] = eig.eigenvectors(i, a);
+            L.run(c);
+        }
+        s.energy = eig.eigenvalues[a];
+    }
+    return seeds;
+}
+
+// select_seed (sbci1.hpp:501-519): lowest Rayleigh quotient after deflation
+Seed select_seed(Context& c, Ops& o, std::vector<const Seed*> cands, Deflation& defl, double lindep) {
+    std::optional<Seed> best;
+    for (const Seed* cand : cands) {
+        Seed s;
+        s.x = o.clone(cand->x);
+        s.hx = o.clone(cand->hx);
+        defl.project_out_pair(o, s.x, s.hx);
+        const double nm = o.norm(s.x);
+        if (nm < std::max(lindep, 1e-8)) continue;
+        o.scale2(s.x, s.hx, 1.0 / nm);
+        s.energy = o.dot(s.x, s.hx);
+        if (!best || s.energy < best->energy) best = std::move(s);
+    }
+    (void)c;
+    if (!best) throw std::runtime_error("all seed candidates collapsed under deflation");
+    return std::move(*best);
+}
+
+}  // namespace
+
+// solve_n_states_sbci1 (sbci1.hpp:526-579)
+MultiStateResult solve_n_states_sbci1(Context& c, int n, const SolverConfig& cfg,
+                                      const std::function<void(const TraceRec&)>& trace) {
+    cfg.validate();
+    if (n < 1) throw std::invalid_argument("solve_n_states_sbci1: n must be >= 1");
+    const auto t0 = std::chrono::steady_clock::now();
+    const uint64_t applies_before = c.applies().load();
+    Ops o(c);
+    Driver dr(c, cfg, trace);
+    std::vector<Seed> guesses = init_guess(c, o, n);
+    Precond pre{&c.diagonal(), guesses.front().energy, cfg.clamp_delta};
+    if (!(pre.clamp > 0.0)) throw std::invalid_argument("clamp_delta must be positive");
+    Deflation defl;
+    MultiStateResult out;
+    std::optional<Seed> carried;
+    for (int alpha = 0; alpha < n; ++alpha) {
+        std::vector<const Seed*> cands;
+        if (carried) cands.push_back(&*carried);
+        for (int b = alpha; b < (int)guesses.size(); ++b) cands.push_back(&guesses[b]);
+        for (int b = 0; b < alpha && b < (int)guesses.size(); ++b) cands.push_back(&guesses[b]);
+        Seed seed = select_seed(c, o, cands, defl, cfg.lindep);
+        carried.reset();
+        Sbci1Result res = solve_state(dr, pre, defl, std::move(seed), alpha, alpha == 0);
+        if (alpha == 0) pre.update_shift(res.pair.energy);
+        out.total_iterations += res.pair.iterations;
+        out.total_restarts += res.pair.restarts;
+        out.hx_refreshes += res.hx_refreshes;
+        // the deflation set keeps its own copy of the converged vector
+        DBuf keep = o.clone(res.pair.vector);
+        defl.add_with_image(o, std::move(keep), std::move(res.converged_image), res.pair.energy);
+        out.pairs.push_back(std::move(res.pair));
+        carried = std::move(res.next_seed);
+    }
+    std::stable_sort(out.pairs.begin(), out.pairs.end(),
+                     [](const StateResult& a, const StateResult& b) { return a.energy < b.energy; });
+    out.matvecs = c.applies().load() - applies_before;
+    out.peak_vectors = 7 + (int)defl.size();
+    SBG_CUDA(cudaStreamSynchronize(c.st));
+    out.wall_time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return out;
+}
+
+}  // namespace sbg

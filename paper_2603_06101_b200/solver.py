@@ -1,0 +1,150 @@
+"""Python mirror of the reference's solver surface (config.hpp, sbci1.hpp:27-34/489-579,
+trace.hpp:22-221); the solve itself runs in libsbg (C++ host driver + sm_100a kernels)."""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field, fields
+
+import numpy as np
+
+from ._lib import TRACE_FN, Config, Stats, check, lib
+
+RESTART_REASONS = ("stall_small_b", "norm_out_of_range", "residual_blowup", "max_cycle")
+
+
+class NonConvergenceError(RuntimeError):
+    """sbci::NonConvergenceError (config.hpp:92-100); CLI exit code 2."""
+
+    def __init__(self, msg, state=-1, best_energy=float("nan"), best_residual=float("nan")):
+        super().__init__(msg)
+        self.state, self.best_energy, self.best_residual = state, best_energy, best_residual
+
+
+@dataclass
+class SolverConfig:
+    """Thresholds, defaults = the paper's values (config.hpp:10-22)."""
+    eps0: float = 1e-10
+    r0: float = 1e-5
+    b_th: float = 1e-2
+    eps1: float = 1e-7
+    x_th1: float = 0.1
+    x_th2: float = 1.2
+    r1: float = 1.0
+    max_cycle: int = 0
+    t_max: int = 10000
+    lindep: float = 1e-14
+    clamp_delta: float = 1e-10
+    hx_refresh_restarts: int = 5
+
+    def effective_max_cycle(self, method_default: int) -> int:
+        return self.max_cycle if self.max_cycle > 0 else method_default
+
+    def to_c(self) -> Config:
+        c = Config()
+        for f in fields(self):
+            setattr(c, f.name, getattr(self, f.name))
+        return c
+
+    def validate(self):
+        c = self.to_c()
+        check(lib().sbg_config_validate(C.byref(c)))
+
+    @staticmethod
+    def preset(name: str) -> "SolverConfig":
+        if name == "tight":
+            return SolverConfig(eps0=1e-10, r0=1e-5)
+        if name == "loose":
+            return SolverConfig(eps0=1e-8, r0=1e-4)
+        raise ValueError(f"unknown preset '{name}' (expected tight or loose)")
+
+
+@dataclass
+class ConvergedEigenpair:
+    state: int
+    energy: float
+    vector: np.ndarray
+    iterations: int
+    restarts: int
+    final_residual: float
+
+
+@dataclass
+class StateSummary:
+    state: int
+    energy: float
+    iterations: int
+    restarts: int
+    final_residual: float
+    s_squared: float = float("nan")
+
+
+@dataclass
+class RunSummary:
+    method: str = "sbci1"
+    states: list = field(default_factory=list)
+    total_iterations: int = 0
+    total_restarts: int = 0
+    matvecs: int = 0
+    hx_refreshes: int = 0
+    peak_vectors: int = 0
+    wall_time_s: float = 0.0
+    kernel_launches: int = 0
+
+    def energies(self):
+        return [s.energy for s in self.states]
+
+
+@dataclass
+class TraceRecord:
+    method: str
+    state: int
+    t: int
+    energy: float
+    dE: float
+    res_norm: float
+    x_norm: float
+    kinetic: float
+    matvecs: int
+    restart_reason: str
+    b: float
+    c: float
+
+
+@dataclass
+class MultiStateResult:
+    pairs: list
+    summary: RunSummary
+
+
+def solve_n_states_sbci1(op, n: int, cfg: SolverConfig | None = None, sink=None, want_vectors: bool = True):
+    """Sequential lowest-n SBCI1 driver (sbci1.hpp:526-579) on the GPU operator.
+    `sink` is a callable receiving TraceRecord per iteration (TraceSink::record)."""
+    cfg = cfg or SolverConfig()
+    cfg.validate()
+    if n < 1:
+        raise ValueError("solve_n_states_sbci1: n must be >= 1")
+    dim = op.dim()
+    e = np.zeros(n)
+    vec = np.zeros((n, dim)) if want_vectors else None
+    st = Stats()
+    cc = cfg.to_c()
+    cb = TRACE_FN(0)
+    if sink is not None:
+        def _cb(rec_p, _user):
+            r = rec_p.contents
+            sink(TraceRecord("sbci1", r.state, r.t, r.energy, r.dE, r.res_norm, r.x_norm, r.kinetic, r.matvecs,
+                             RESTART_REASONS[r.restart_reason] if r.restart_reason >= 0 else "", r.b, r.c))
+        cb = TRACE_FN(_cb)
+    rc = lib().sbg_solve(op.handle, 1, n, C.byref(cc), e.ctypes.data_as(C.POINTER(C.c_double)),
+                         vec.ctypes.data_as(C.POINTER(C.c_double)) if vec is not None else None, C.byref(st), cb, None)
+    if rc == 2:
+        raise NonConvergenceError(lib().sbg_last_error().decode(), st.failed_state, st.best_energy, st.best_residual)
+    check(rc)
+    pairs, states = [], []
+    for k in range(n):
+        pairs.append(ConvergedEigenpair(k, float(e[k]), vec[k] if vec is not None else None, st.iterations[k],
+                                        st.restarts[k], st.final_residual[k]))
+        states.append(StateSummary(k, float(e[k]), st.iterations[k], st.restarts[k], st.final_residual[k]))
+    summ = RunSummary("sbci1", states, st.total_iterations, st.total_restarts, st.matvecs, st.hx_refreshes,
+                      st.peak_vectors, st.wall_time_s, st.kernel_launches)
+    return MultiStateResult(pairs, summ)
