@@ -140,6 +140,11 @@ int sbg_sigma_padded(sbg_ctx* ctx, const double* d_x_padded_local, double* d_y_p
 uint64_t sbg_apply_count(const sbg_ctx* ctx);
 void sbg_reset_apply_count(sbg_ctx* ctx);
 uint64_t sbg_kernel_launches(const sbg_ctx* ctx);
+/* Device-time profile of the sigma calls since the last reset, measured with CUDA events recorded on
+ * the launching stream around each phase: ms[0] alpha-beta kernel, ms[1] same-spin kernels +
+ * transposes, ms[2] collectives (world > 1), ms[3] whole sigma. *calls = sigma calls profiled. */
+int sbg_profile_reset(sbg_ctx* ctx);
+int sbg_profile_read(sbg_ctx* ctx, double* ms, int64_t* calls);
 /* Flop count of one sigma (algorithm actually executed), split by kernel. */
 int sbg_sigma_flops(const sbg_ctx* ctx, double* alpha_beta, double* same_spin, double* total);
 

@@ -85,6 +85,8 @@ def lib() -> C.CDLL:
         "sbg_reset_apply_count": (None, [P]),
         "sbg_kernel_launches": (C.c_uint64, [P]),
         "sbg_sigma_flops": (C.c_int, [P, D, D, D]),
+        "sbg_profile_reset": (C.c_int, [P]),
+        "sbg_profile_read": (C.c_int, [P, D, C.POINTER(C.c_int64)]),
         "sbg_solve": (C.c_int, [P, C.c_int, C.c_int, C.POINTER(Config), D, D, C.POINTER(Stats), TRACE_FN, P]),
         "sbg_selftest": (C.c_int, []),
     }
@@ -102,7 +104,8 @@ EXPORTED = ["sbg_last_error", "sbg_version", "sbg_binomial", "sbg_determinant_co
             "sbg_create_dist", "sbg_nccl_unique_id", "sbg_destroy", "sbg_dim", "sbg_sector", "sbg_local_rows",
             "sbg_diagonal", "sbg_table_sizes", "sbg_string_tables", "sbg_sigma", "sbg_sigma_device",
             "sbg_padded_len", "sbg_pack", "sbg_unpack", "sbg_sigma_padded", "sbg_apply_count",
-            "sbg_reset_apply_count", "sbg_kernel_launches", "sbg_sigma_flops", "sbg_solve", "sbg_selftest"]
+            "sbg_reset_apply_count", "sbg_kernel_launches", "sbg_sigma_flops", "sbg_profile_reset", "sbg_profile_read",
+            "sbg_solve", "sbg_selftest"]
 
 
 class SbgError(RuntimeError):

@@ -308,6 +308,20 @@ void sbg_reset_apply_count(sbg_ctx* ctx) {
 }
 uint64_t sbg_kernel_launches(const sbg_ctx* ctx) { return ctx && ctx->c ? ctx->c->launches : 0; }
 
+int sbg_profile_reset(sbg_ctx* ctx) {
+    return guarded([&] {
+        require_ctx(ctx);
+        ctx->c->profile_reset();
+    });
+}
+
+int sbg_profile_read(sbg_ctx* ctx, double* ms, int64_t* calls) {
+    return guarded([&] {
+        require_ctx(ctx);
+        ctx->c->profile_read(ms, calls);
+    });
+}
+
 int sbg_sigma_flops(const sbg_ctx* ctx, double* ab, double* ss, double* total) {
     return guarded([&] {
         require_ctx(ctx);

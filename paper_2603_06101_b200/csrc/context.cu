@@ -119,10 +119,13 @@ Context::Context(int norb_, int nelec_, int ms2_, double e_core_, const double* 
 Context::~Context() {
     if (st) cudaStreamSynchronize(st);
     for (void* p : {(void*)d_sa_, (void*)d_sb_, (void*)d_la_, (void*)d_lb_, (void*)d_h1_, (void*)d_eri_, (void*)d_Vp_,
-                    (void*)d_Va_, (void*)d_codes_, (void*)rws.partial, (void*)rws.result})
+                    (void*)d_Va_, (void*)d_codes_, (void*)d_sc_tgt_, (void*)d_sc_ent_,
+                    (void*)d_sc_tt_, (void*)d_sc_te_, (void*)rws.partial, (void*)rws.result})
         if (p) cudaFree(p);
     if (rws.host) cudaFreeHost(rws.host);
     comm_.reset();
+    for (auto& es : ev_pool_)
+        for (auto& e : es.e) cudaEventDestroy(e);
     if (ev0_) cudaEventDestroy(ev0_);
     if (ev1_) cudaEventDestroy(ev1_);
     if (st) cudaStreamDestroy(st);
@@ -177,7 +180,20 @@ void Context::build_tables(const double* h1, const double* eri) {
         d_codes_ = dmalloc<uint16_t>((size_t)ld * ab_.npad);
         launch_scatter_codes(d_sb_, NB, ld, norb, ab_.npair, ab_.npad, d_codes_, st);
         launches += 1;
-        SBG_CUDA(cudaStreamSynchronize(st));  // Vp host buffer
+        std::vector<uint16_t> codes((size_t)ld * ab_.npad);
+        SBG_CUDA(cudaMemcpyAsync(codes.data(), d_codes_, codes.size() * 2, cudaMemcpyDeviceToHost, st));
+        SBG_CUDA(cudaStreamSynchronize(st));  // Vp host buffer, codes
+        std::vector<uint32_t> tgt, tt, te;
+        std::vector<uint16_t> ent;
+        build_ab_scatter(ab_, codes, tgt, ent, tt, te);
+        d_sc_tgt_ = dmalloc<uint32_t>(tgt.size());
+        d_sc_ent_ = dmalloc<uint16_t>(ent.size());
+        d_sc_tt_ = dmalloc<uint32_t>(tt.size());
+        d_sc_te_ = dmalloc<uint32_t>(te.size());
+        SBG_CUDA(cudaMemcpy(d_sc_tgt_, tgt.data(), tgt.size() * 4, cudaMemcpyHostToDevice));
+        SBG_CUDA(cudaMemcpy(d_sc_ent_, ent.data(), ent.size() * 2, cudaMemcpyHostToDevice));
+        SBG_CUDA(cudaMemcpy(d_sc_tt_, tt.data(), tt.size() * 4, cudaMemcpyHostToDevice));
+        SBG_CUDA(cudaMemcpy(d_sc_te_, te.data(), te.size() * 4, cudaMemcpyHostToDevice));
     }
     // same-spin antisymmetrized pair integrals W(pr,qs) = (pq|rs) - (ps|rq), p<r, q<s
     if (norb >= 2) {
@@ -289,13 +305,49 @@ const double* Context::finish_dots(int ndot) {
 //   3. alpha-alpha: same-spin kernel on x, fp64 reductions into y (world>1: column window +
 //      all-to-all of the blocks)
 //   4. alpha-beta + one-body + e_core: sigma_ab, accumulating into y
+Context::EvSet* Context::next_evset() {
+    if (ev_used_ == ev_pool_.size()) {
+        if (ev_pool_.size() >= 256) return nullptr;  // profile ring full: stop recording until read/reset
+        EvSet es;
+        for (auto& e : es.e) SBG_CUDA(cudaEventCreate(&e));
+        ev_pool_.push_back(es);
+    }
+    return &ev_pool_[ev_used_++];
+}
+
+void Context::profile_reset() {
+    SBG_CUDA(cudaStreamSynchronize(st));
+    ev_used_ = 0;
+    prof_calls_ = 0;
+    for (double& v : prof_ms_) v = 0.0;
+}
+
+void Context::profile_read(double* ms, int64_t* calls) {
+    SBG_CUDA(cudaDeviceSynchronize());
+    for (size_t i = 0; i < ev_used_; ++i) {
+        float t[4];
+        const auto& e = ev_pool_[i].e;
+        SBG_CUDA(cudaEventElapsedTime(&t[0], e[3], e[4]));  // alpha-beta
+        SBG_CUDA(cudaEventElapsedTime(&t[1], e[1], e[3]));  // same-spin + transposes
+        SBG_CUDA(cudaEventElapsedTime(&t[2], e[0], e[1]));  // all-gather
+        SBG_CUDA(cudaEventElapsedTime(&t[3], e[0], e[4]));  // whole sigma
+        for (int k = 0; k < 4; ++k) prof_ms_[k] += t[k];
+        ++prof_calls_;
+    }
+    ev_used_ = 0;
+    for (int k = 0; k < 4; ++k) ms[k] = prof_ms_[k];
+    *calls = prof_calls_;
+}
+
 void Context::sigma(const double* x_local, double* y_local, cudaStream_t s) {
-    SBG_CUDA(cudaEventRecord(ev0_, s));
+    EvSet* ev = next_evset();
+    if (ev) SBG_CUDA(cudaEventRecord(ev->e[0], s));
     const double* xf = x_local;
     if (world > 1) {
         gather_full(x_local, s);
         xf = xfull_.p;
     }
+    if (ev) SBG_CUDA(cudaEventRecord(ev->e[1], s));
     bool y_written = false;
     // ---- beta-beta via the transpose
     if (ssb_.P > 0) {
@@ -367,9 +419,14 @@ void Context::sigma(const double* x_local, double* y_local, cudaStream_t s) {
             }
         }
     }
+    if (ev) {
+        SBG_CUDA(cudaEventRecord(ev->e[2], s));
+        SBG_CUDA(cudaEventRecord(ev->e[3], s));
+    }
     // ---- alpha-beta (+ one-body folded, + e_core)
     if (have_ab_) {
-        launch_sigma_ab(ab_, xf, y_local, d_Vp_, d_codes_, row_lo, row_hi, e_core, 1, nsm, s);
+        launch_sigma_ab(ab_, AbScatter{d_sc_tgt_, d_sc_ent_, d_sc_tt_, d_sc_te_}, xf, y_local, d_Vp_, row_lo, row_hi,
+                        e_core, 1, nsm, s);
         launches += 1;
     } else {
         ensure_links();
@@ -379,7 +436,7 @@ void Context::sigma(const double* x_local, double* y_local, cudaStream_t s) {
                        1, s);
         launches += 1;
     }
-    SBG_CUDA(cudaEventRecord(ev1_, s));
+    if (ev) SBG_CUDA(cudaEventRecord(ev->e[4], s));
     applies_.fetch_add(1, std::memory_order_relaxed);
 }
 

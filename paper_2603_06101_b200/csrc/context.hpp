@@ -73,6 +73,10 @@ public:
     const double* finish_dots(int ndot);  // sync; returns host pointer
     void allreduce_inplace_device(double* d, int count);
 
+    // per-phase CUDA-event profile of sigma calls (sbg_profile_*)
+    void profile_reset();
+    void profile_read(double* ms, int64_t* calls);
+
     std::atomic<uint64_t>& applies() { return applies_; }
     uint64_t launches = 0;
     double sigma_ms = 0.0;  // accumulated device time of sigma calls (events)
@@ -90,6 +94,8 @@ private:
     Excitation *d_la_ = nullptr, *d_lb_ = nullptr;
     double *d_h1_ = nullptr, *d_eri_ = nullptr, *d_Vp_ = nullptr, *d_Va_ = nullptr, *d_Vb_ = nullptr;
     uint16_t* d_codes_ = nullptr;
+    uint32_t *d_sc_tgt_ = nullptr, *d_sc_tt_ = nullptr, *d_sc_te_ = nullptr;
+    uint16_t* d_sc_ent_ = nullptr;
     DBuf diag_;
     // sigma workspaces
     DBuf xfull_, xT_, sT_, saa_, a2a_send_, a2a_recv_;
@@ -97,6 +103,14 @@ private:
     SsPlan ssa_{}, ssb_{};
     bool have_ab_ = false;
     cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+    struct EvSet {
+        cudaEvent_t e[5];
+    };
+    std::vector<EvSet> ev_pool_;
+    size_t ev_used_ = 0;
+    double prof_ms_[4] = {0, 0, 0, 0};
+    int64_t prof_calls_ = 0;
+    EvSet* next_evset();
 };
 
 }  // namespace sbg

@@ -12,10 +12,15 @@
 //           3-stage pipeline;
 //   DGEMM   G[rs][Jb] = sum_k A[rs][k] D[k][Jb], A[rs][k] = sign_k V'(pair_k, rs), M = npair =
 //           norb(norb+1)/2 packed symmetric pairs, A resident in registers for the whole row —
-//           mma.sync m16n8k4 / m8n8k4 f64 (SASS DMMA.8x8x4);
-//   scatter G[rs][Jb] -> sigma(Ia, E_rs Jb) with the beta link sign, fp64 shared-memory atomics.
+//           mma.sync m16n8k4 / m8n8k4 f64 (SASS DMMA.8x8x4); G staged once in shared memory;
+//   scatter sigma(Ia, Ib) += sum over the tile's (rs, Jb) with E_rs Jb = Ib of sign * G[rs][Jb].
+//           The (rs,Jb) -> Ib map depends only on the tile, so it is precomputed once as a
+//           target-sorted segment list (build_ab_scatter): every target of a tile is reduced by
+//           one thread in a fixed order — no atomics, bit-reproducible sums.
 // The row is then written once: y(Ia,:) = [y(Ia,:)] + sigma_row + e_core c(Ia,:).
 #include <algorithm>
+#include <cstdlib>
+#include <vector>
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -23,37 +28,61 @@ namespace sbg {
 
 namespace {
 
-constexpr int NT = 32;        // beta-string tile width (columns per tile)
-constexpr int DSTRIDE = 36;   // smem row stride of a D tile (bank-conflict-free B fragments)
-constexpr int STAGES = 3;
+// NT: beta-string tile width (16 or 32 columns); chosen per sector by shared-memory budget.
+template <int NT> struct Tile {
+    static constexpr int NBT = NT / 8;         // n8 blocks per tile
+    static constexpr int DSTRIDE = NT + 4;     // D row stride: bank-conflict-free B fragments (== 4 mod 16)
+    static constexpr int GSTRIDE = NT + 1;     // staged G row stride
+};
+constexpr int STAGES = 2;     // D tiles, G tiles and scatter lists are double buffered
 
 struct AbParams {
     const double* x;
     double* y;
     const double* Vp;
-    const uint16_t* codes;
-    int norb, na_el, npair, npad, mb16, extra, K, KP;
+    const uint32_t* tgt;        // per tile: (target << 16) | segment end, concatenated
+    const uint16_t* ent;        // per tile: (G offset) | (negative << 15), target-sorted
+    const uint32_t* tile_tgt;   // [ntiles+1] offsets into tgt
+    const uint32_t* tile_ent;   // [ntiles+1] offsets into ent
+    int norb, na_el, npair, mb16, extra, K, KP, grows, maxT, maxE;
     int64_t NB, ld, row_lo, row_hi;
     double e_core;
     int accumulate;
+    int dbg;  // profiling experiments only: 1 = skip scatter, 2 = skip MMA
 };
 
-template <int KS>
-__global__ void __launch_bounds__(288, 1) k_sigma_ab(const AbParams p) {
+// Software pipeline per alpha row, one __syncthreads per tile: iteration `it` prefetches D(it+1)
+// and the scatter lists of tile it, runs the DMMAs of tile it into G[it&1], and scatters tile it-1
+// from G[(it-1)&1] — so warps that finish their MMAs scatter while the others still feed the
+// FP64 tensor pipe.
+template <int KS, int NT>
+__global__ void __launch_bounds__(256, 1) k_sigma_ab(const AbParams p) {
+    constexpr int NBT = Tile<NT>::NBT, DSTRIDE = Tile<NT>::DSTRIDE, GSTRIDE = Tile<NT>::GSTRIDE;
     extern __shared__ __align__(16) double smem[];
     const int KP = KS * 4;
-    double* srow = smem;                                  // [ld]
-    double* Ds = smem + p.ld;                             // [STAGES][KP][DSTRIDE]
-    int* sJ = reinterpret_cast<int*>(Ds + STAGES * KP * DSTRIDE);  // [KP]
+    const int ntiles = (int)(p.ld / NT);
+    double* srow = smem;                                             // [ld]
+    double* Ds = srow + p.ld;                                        // [STAGES][KP][DSTRIDE]
+    double* sAe = Ds + STAGES * KP * DSTRIDE;                        // [KP][8] A of the extra m8 rows
+    double* Gs = sAe + KP * 8;                                       // [STAGES][grows][GSTRIDE]
+    uint32_t* Lt = reinterpret_cast<uint32_t*>(Gs + STAGES * p.grows * GSTRIDE);  // [STAGES][maxT]
+    uint16_t* Le = reinterpret_cast<uint16_t*>(Lt + STAGES * p.maxT);             // [STAGES][maxE]
+    uint32_t* sTT = reinterpret_cast<uint32_t*>(Le + STAGES * p.maxE);            // [ntiles+1]
+    uint32_t* sTE = sTT + ntiles + 1;                                             // [ntiles+1]
+    int* sJ = reinterpret_cast<int*>(sTE + ntiles + 1);                           // [KP]
     int* sPair = sJ + KP;                                 // [KP]  -1 = occupation row, -2 = padding
-    double* sSign = reinterpret_cast<double*>(sPair + KP + (KP & 1));  // [KP]
+    double* sSign = reinterpret_cast<double*>(sPair + KP);  // [KP] (8-byte aligned: KP % 4 == 0)
 
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int w = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
     const int norb = p.norb, npair = p.npair;
-    const int ntiles = (int)(p.ld / NT);
     const bool main_ok = w < p.mb16;
-    const bool do_extra = p.extra && w < 4;
+    const bool do_extra = p.extra && w < NBT;  // extra m8 rows: one n8 block per warp
+
+    for (int i = tid; i <= ntiles; i += nthr) {
+        sTT[i] = p.tile_tgt[i];
+        sTE[i] = p.tile_ent[i];
+    }
 
     for (int64_t ia = p.row_lo + blockIdx.x; ia < p.row_hi; ia += gridDim.x) {
         __syncthreads();  // previous row fully written out
@@ -100,88 +129,117 @@ __global__ void __launch_bounds__(288, 1) k_sigma_ab(const AbParams p) {
             }
             return sSign[k] * p.Vp[(size_t)pr * npair + rs];
         };
-        double a0[KS], a1[KS], ae[KS];
-        const int r0 = 16 * w + g, re = 16 * p.mb16 + g;
+        double a0[KS], a1[KS];
+        const int r0 = 16 * w + g, re = 16 * p.mb16;
 #pragma unroll
         for (int j = 0; j < KS; ++j) {
             const int k = 4 * j + t;
             a0[j] = main_ok ? aval(r0, k) : 0.0;
             a1[j] = main_ok ? aval(r0 + 8, k) : 0.0;
-            ae[j] = do_extra ? aval(re, k) : 0.0;
         }
+        if (p.extra)
+            for (int i = tid; i < KP * 8; i += nthr) sAe[i] = aval(re + (i & 7), i >> 3);
 
-        auto load_tile = [&](int stage, int jt) {
+        auto load_d = [&](int stage, int jt) {
             double* dst = Ds + stage * KP * DSTRIDE;
             for (int c = tid; c < KP * (NT / 2); c += nthr) {
                 const int k = c / (NT / 2), part = c % (NT / 2);
                 cp_async16(dst + k * DSTRIDE + part * 2, p.x + (int64_t)sJ[k] * p.ld + (int64_t)jt * NT + part * 2);
             }
-            cp_async_commit();
         };
-#pragma unroll
-        for (int s = 0; s < STAGES - 1; ++s) {
-            if (s < ntiles) load_tile(s, s);
-            else cp_async_commit();
-        }
+        auto load_lists = [&](int stage, int jt) {  // 16-byte aligned, padded segments
+            const uint32_t t0 = sTT[jt], nt4 = (sTT[jt + 1] - t0 + 3) / 4;
+            const uint32_t e0 = sTE[jt], ne8 = (sTE[jt + 1] - e0 + 7) / 8;
+            for (uint32_t c = tid; c < nt4; c += nthr) cp_async16(Lt + stage * p.maxT + 4 * c, p.tgt + t0 + 4 * c);
+            for (uint32_t c = tid; c < ne8; c += nthr) cp_async16(Le + stage * p.maxE + 8 * c, p.ent + e0 + 8 * c);
+        };
+        load_d(0, 0);
+        cp_async_commit();
 
-        for (int jt = 0; jt < ntiles; ++jt) {
-            // scatter codes for this tile (independent of D; issued before the wait)
-            uint16_t code[4][4], codee[2];
-            const uint16_t* cbase = p.codes + ((int64_t)jt * NT) * p.npad;
-#pragma unroll
-            for (int nb = 0; nb < 4; ++nb)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int col = nb * 8 + 2 * t + (e & 1), row = r0 + (e >> 1) * 8;
-                    code[nb][e] = main_ok ? cbase[(int64_t)col * p.npad + row] : (uint16_t)0xFFFF;
-                }
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int col = w * 8 + 2 * t + e;
-                codee[e] = do_extra ? cbase[(int64_t)col * p.npad + re] : (uint16_t)0xFFFF;
-            }
-
-            cp_async_wait<STAGES - 2>();
+        for (int it = 0; it <= ntiles; ++it) {
+            cp_async_wait<0>();
             __syncthreads();
-            {
-                const int pf = jt + STAGES - 1;
-                if (pf < ntiles) load_tile(pf % STAGES, pf);
-                else cp_async_commit();
-            }
-            const double* D = Ds + (jt % STAGES) * KP * DSTRIDE;
-            double acc[4][4];
-            double acce[2] = {0.0, 0.0};
-#pragma unroll
-            for (int nb = 0; nb < 4; ++nb)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) acc[nb][e] = 0.0;
-#pragma unroll
-            for (int j = 0; j < KS; ++j) {
-                const double* Dk = D + (4 * j + t) * DSTRIDE + g;
-                double b[4];
-#pragma unroll
-                for (int nb = 0; nb < 4; ++nb) b[nb] = Dk[nb * 8];
-                if (main_ok) {
-#pragma unroll
-                    for (int nb = 0; nb < 4; ++nb) dmma_16x8x4(acc[nb], a0[j], a1[j], b[nb]);
+            if (it + 1 < ntiles) load_d((it + 1) & 1, it + 1);
+            if (it < ntiles) load_lists(it & 1, it);
+            cp_async_commit();
+            // warps w and w+4 share an SM sub-partition: one issues its DMMAs while the other
+            // scatters, so the FP64 tensor pipe is not idle during the scatter phase
+            auto do_mma = [&]() {
+            if (it < ntiles) {
+                    const double* D = Ds + (it & 1) * KP * DSTRIDE;
+                    double* G = Gs + (it & 1) * p.grows * GSTRIDE;
+                    double acc[NBT][4];
+                    double ace0[2] = {0.0, 0.0}, ace1[2] = {0.0, 0.0};
+    #pragma unroll
+                    for (int nb = 0; nb < NBT; ++nb)
+    #pragma unroll
+                        for (int e = 0; e < 4; ++e) acc[nb][e] = 0.0;
+                    if (main_ok) {
+                        // B fragments double-buffered in registers: loads of k-step j+1 are in flight
+                        // while the DMMAs of step j issue
+                        double b[2][NBT];
+    #pragma unroll
+                        for (int nb = 0; nb < NBT; ++nb) b[0][nb] = D[t * DSTRIDE + g + nb * 8];
+    #pragma unroll
+                        for (int j = 0; j < KS; ++j) {
+                            const int cur = j & 1;
+                            if (j + 1 < KS) {
+    #pragma unroll
+                                for (int nb = 0; nb < NBT; ++nb) b[cur ^ 1][nb] = D[(4 * (j + 1) + t) * DSTRIDE + g + nb * 8];
+                            }
+    #pragma unroll
+                            for (int nb = 0; nb < NBT; ++nb) dmma_16x8x4(acc[nb], a0[j], a1[j], b[cur][nb]);
+                            if (do_extra) {
+                                const double ae = sAe[(4 * j + t) * 8 + g];
+                                const double be = D[(4 * j + t) * DSTRIDE + g + w * 8];
+                                if (cur) dmma_8x8x4(ace1, ae, be);
+                                else dmma_8x8x4(ace0, ae, be);
+                            }
+                        }
+    #pragma unroll
+                        for (int nb = 0; nb < NBT; ++nb) {
+                            const int col = nb * 8 + 2 * t;
+                            G[r0 * GSTRIDE + col] = acc[nb][0];
+                            G[r0 * GSTRIDE + col + 1] = acc[nb][1];
+                            G[(r0 + 8) * GSTRIDE + col] = acc[nb][2];
+                            G[(r0 + 8) * GSTRIDE + col + 1] = acc[nb][3];
+                        }
+                        if (do_extra) {
+                            G[(re + g) * GSTRIDE + w * 8 + 2 * t] = ace0[0] + ace1[0];
+                            G[(re + g) * GSTRIDE + w * 8 + 2 * t + 1] = ace0[1] + ace1[1];
+                        }
+                    }
                 }
-                if (do_extra) dmma_8x8x4(acce, ae[j], Dk[w * 8]);
-            }
-            // ---- scatter into the shared sigma row
-#pragma unroll
-            for (int nb = 0; nb < 4; ++nb)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const uint16_t cd = code[nb][e];
-                    if (cd != 0xFFFF) atomicAdd(&srow[cd & 0x7FFF], (cd & 0x8000) ? -acc[nb][e] : acc[nb][e]);
+            };
+            auto do_scatter = [&]() {
+            if (it >= 1) {  // segmented scatter of tile it-1: one thread per distinct target
+                    const int jt = it - 1;
+                    const double* G = Gs + (jt & 1) * p.grows * GSTRIDE;
+                    const uint32_t* lt = Lt + (jt & 1) * p.maxT;
+                    const uint16_t* le = Le + (jt & 1) * p.maxE;
+                    const uint32_t nt = sTT[jt + 1] - sTT[jt];
+                    for (uint32_t i = tid; i < nt; i += nthr) {
+                        const uint32_t tg = lt[i];
+                        const uint32_t beg = (i == 0) ? 0u : (lt[i - 1] & 0xFFFFu);
+                        const uint32_t end = tg & 0xFFFFu;
+                        double v = 0.0;
+                        for (uint32_t e = beg; e < end; ++e) {
+                            const uint16_t en = le[e];
+                            const double gv = G[en & 0x7FFF];
+                            v += (en & 0x8000) ? -gv : gv;
+                        }
+                        srow[tg >> 16] += v;
+                    }
                 }
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const uint16_t cd = codee[e];
-                if (cd != 0xFFFF) atomicAdd(&srow[cd & 0x7FFF], (cd & 0x8000) ? -acce[e] : acce[e]);
+            };
+            if (((w >> 2) & 1) == 0) {
+                if (!(p.dbg & 2)) do_mma();
+                if (!(p.dbg & 1)) do_scatter();
+            } else {
+                if (!(p.dbg & 1)) do_scatter();
+                if (!(p.dbg & 2)) do_mma();
             }
         }
-        cp_async_wait<0>();
         __syncthreads();
         // ---- write the row: y = [y] + sigma_ab + e_core * x
         const double* xr = p.x + ia * p.ld;
@@ -197,15 +255,15 @@ __global__ void __launch_bounds__(288, 1) k_sigma_ab(const AbParams p) {
     }
 }
 
-template <int KS>
+template <int KS, int NT>
 void launch_ks(const AbPlan& pl, const AbParams& prm, int grid, cudaStream_t st) {
-    auto kern = k_sigma_ab<KS>;
-    static thread_local int configured = -1;
+    auto kern = k_sigma_ab<KS, NT>;
+    static int configured[64] = {0};
     int dev = 0;
     cudaGetDevice(&dev);
-    if (configured != dev) {
+    if (dev < 64 && !configured[dev]) {
         SBG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        configured = dev;
+        configured[dev] = 1;
     }
     kern<<<grid, pl.threads, pl.smem, st>>>(prm);
     SBG_LAUNCH_CHECK();
@@ -225,28 +283,79 @@ AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int
     pl.npair = norb * (norb + 1) / 2;
     pl.K = 1 + na_el * (norb - na_el);
     pl.KS = (pl.K + 3) / 4;
-    const int full = pl.npair / 16, rem = pl.npair % 16;
-    if (rem == 0) {
-        pl.mb16 = full;
-        pl.extra = 0;
-    } else if (rem <= 8 && full >= 4) {
-        pl.mb16 = full;  // the last 8 rows ride on m8n8k4 in warps 0..3 (balanced SMSP load)
-        pl.extra = 1;
-    } else {
-        pl.mb16 = full + 1;
-        pl.extra = 0;
-    }
-    pl.npad = pl.extra ? 16 * pl.mb16 + 8 : 16 * pl.mb16;
-    pl.threads = 32 * std::max(pl.mb16, pl.extra ? 4 : 1);
     const int KP = pl.KS * 4;
-    pl.smem = (size_t)ld * 8 + (size_t)STAGES * KP * DSTRIDE * 8 + (size_t)KP * 4 * 2 + 8 + (size_t)KP * 8;
+    const int full = pl.npair / 16, rem = pl.npair % 16;
+    auto configure = [&](int nt) {
+        const int nbt = nt / 8;
+        if (rem == 0) {
+            pl.mb16 = full;
+            pl.extra = 0;
+        } else if (rem <= 8 && full >= nbt) {
+            pl.mb16 = full;  // the last 8 rows ride on m8n8k4 in warps 0..nbt-1
+            pl.extra = 1;
+        } else {
+            pl.mb16 = full + 1;
+            pl.extra = 0;
+        }
+        pl.npad = pl.extra ? 16 * pl.mb16 + 8 : 16 * pl.mb16;
+        pl.threads = 32 * pl.mb16;
+        pl.nt = nt;
+        // scatter-list buffers: bounded by the tile's valid (rs, column) entries
+        pl.maxT = 4 * ((nt * (1 + nb_el * (norb - nb_el)) + 3) / 4);
+        pl.maxE = 8 * ((nt * (nb_el + nb_el * (norb - nb_el)) + 7) / 8);
+        const int64_t ntiles = ld / nt;
+        pl.smem = (size_t)ld * 8 + (size_t)STAGES * KP * (nt + 4) * 8 + (size_t)KP * 8 * 8 +
+                  (size_t)STAGES * pl.npad * (nt + 1) * 8 + (size_t)STAGES * (pl.maxT * 4 + pl.maxE * 2) +
+                  (size_t)(ntiles + 1) * 8 + (size_t)KP * 16 + 16;
+    };
+    configure(32);
+    if (pl.smem > 227 * 1024) configure(16);
     if (NB > 32767) throw InvalidArgument("sigma_ab: more than 32767 beta strings is not supported by this build");
+    if ((size_t)pl.npad * (pl.nt + 1) >= 32768) throw InvalidArgument("sigma_ab: pair space too large for this build");
     if (pl.smem > 227 * 1024) throw InvalidArgument("sigma_ab: beta row does not fit in shared memory");
-    if (pl.KS > 24 || pl.threads > 288) throw InvalidArgument("sigma_ab: orbital space too large for this build");
+    if (pl.KS > 24 || pl.threads > 256) throw InvalidArgument("sigma_ab: orbital space too large for this build");
     return pl;
 }
 
-void launch_sigma_ab(const AbPlan& pl, const double* x_full, double* y_local, const double* Vp, const uint16_t* codes,
+// Per-tile target-sorted scatter lists from the (rs, Jb) -> (Ib, sign) codes ([ld][npad] u16,
+// 0xFFFF = none). Sort key: target, then (rs, column) — a fixed summation order per target.
+void build_ab_scatter(const AbPlan& pl, const std::vector<uint16_t>& codes, std::vector<uint32_t>& tgt,
+                      std::vector<uint16_t>& ent, std::vector<uint32_t>& tile_tgt, std::vector<uint32_t>& tile_ent) {
+    const int NT = pl.nt, GSTRIDE = pl.nt + 1;
+    const int64_t ntiles = pl.ld / NT;
+    tgt.clear();
+    ent.clear();
+    tile_tgt.assign(ntiles + 1, 0);
+    tile_ent.assign(ntiles + 1, 0);
+    std::vector<std::pair<uint32_t, uint16_t>> items;
+    for (int64_t jt = 0; jt < ntiles; ++jt) {
+        items.clear();
+        for (int rs = 0; rs < pl.npad; ++rs)
+            for (int c = 0; c < NT; ++c) {
+                const uint16_t code = codes[(size_t)(jt * NT + c) * pl.npad + rs];
+                if (code == 0xFFFF) continue;
+                items.push_back({(uint32_t)(code & 0x7FFF), (uint16_t)((rs * GSTRIDE + c) | (code & 0x8000))});
+            }
+        std::stable_sort(items.begin(), items.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+        while (tgt.size() % 4) tgt.push_back(0);  // 16-byte aligned tile segments (cp.async)
+        while (ent.size() % 8) ent.push_back(0);
+        tile_tgt[jt] = (uint32_t)tgt.size();
+        tile_ent[jt] = (uint32_t)ent.size();
+        for (size_t i = 0; i < items.size(); ++i) {
+            ent.push_back(items[i].second);
+            if (i + 1 == items.size() || items[i + 1].first != items[i].first) {
+                if (i + 1 > 0xFFFF) throw InvalidArgument("sigma_ab: tile segment overflow");
+                tgt.push_back((items[i].first << 16) | (uint32_t)(i + 1));
+            }
+        }
+    }
+    while (tgt.size() % 4) tgt.push_back(0);
+    while (ent.size() % 8) ent.push_back(0);
+    tile_tgt[ntiles] = (uint32_t)tgt.size();
+    tile_ent[ntiles] = (uint32_t)ent.size();
+}
+
+void launch_sigma_ab(const AbPlan& pl, const AbScatter& sc, const double* x_full, double* y_local, const double* Vp,
                      int64_t row_lo, int64_t row_hi, double e_core, int accumulate, int grid, cudaStream_t st) {
     ensure_binomials();
     if (row_hi <= row_lo) return;
@@ -254,25 +363,31 @@ void launch_sigma_ab(const AbPlan& pl, const double* x_full, double* y_local, co
     prm.x = x_full;
     prm.y = y_local;
     prm.Vp = Vp;
-    prm.codes = codes;
+    prm.tgt = sc.tgt;
+    prm.ent = sc.ent;
+    prm.tile_tgt = sc.tile_tgt;
+    prm.tile_ent = sc.tile_ent;
     prm.norb = pl.norb;
     prm.na_el = pl.na_el;
     prm.npair = pl.npair;
-    prm.npad = pl.npad;
     prm.mb16 = pl.mb16;
     prm.extra = pl.extra;
     prm.K = pl.K;
     prm.KP = pl.KS * 4;
+    prm.grows = pl.npad;
+    prm.maxT = pl.maxT;
+    prm.maxE = pl.maxE;
     prm.NB = pl.NB;
     prm.ld = pl.ld;
     prm.row_lo = row_lo;
     prm.row_hi = row_hi;
     prm.e_core = e_core;
     prm.accumulate = accumulate;
+    prm.dbg = getenv("SBG_AB_DEBUG") ? atoi(getenv("SBG_AB_DEBUG")) : 0;
     grid = (int)std::min<int64_t>(grid, row_hi - row_lo);
     switch (pl.KS) {
 #define SBG_KS(n) \
-    case n: launch_ks<n>(pl, prm, grid, st); break;
+    case n: if (pl.nt == 32) launch_ks<n, 32>(pl, prm, grid, st); else launch_ks<n, 16>(pl, prm, grid, st); break;
         SBG_KS(1) SBG_KS(2) SBG_KS(3) SBG_KS(4) SBG_KS(5) SBG_KS(6) SBG_KS(7) SBG_KS(8) SBG_KS(9) SBG_KS(10)
         SBG_KS(11) SBG_KS(12) SBG_KS(13) SBG_KS(14) SBG_KS(15) SBG_KS(16) SBG_KS(17) SBG_KS(18) SBG_KS(19)
         SBG_KS(20) SBG_KS(21) SBG_KS(22) SBG_KS(23) SBG_KS(24)

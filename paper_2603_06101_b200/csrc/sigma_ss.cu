@@ -38,8 +38,8 @@ __global__ void __launch_bounds__(128) k_sigma_ss(const SsParams p) {
     extern __shared__ __align__(16) double smem[];
     double* Xs = smem;                        // [KPP][XSTRIDE]
     const int ysrows = max(KPP, 16 * (int)(blockDim.x >> 5));
-    double* Ys = Xs + KPP * XSTRIDE;          // [ysrows][NTS]
-    int* sJ = reinterpret_cast<int*>(Ys + ysrows * NTS);
+    double* Ys = Xs;                          // [ysrows][NTS], aliases Xs once the MMAs are done
+    int* sJ = reinterpret_cast<int*>(Xs + max(KPP * XSTRIDE, ysrows * NTS));
     int* sPi = sJ + KPP;
     double* sPhi = reinterpret_cast<double*>(sPi + KPP);
 
@@ -97,7 +97,10 @@ __global__ void __launch_bounds__(128) k_sigma_ss(const SsParams p) {
         if (c0 >= p.col_hi) break;
         for (int c = tid; c < KPP * (NTS / 2); c += nthr) {
             const int k = c / (NTS / 2), part = c % (NTS / 2);
-            cp_async16(Xs + k * XSTRIDE + part * 2, p.x + (int64_t)sJ[k] * p.ldx + c0 + part * 2);
+            // the last tile may overhang the padded row (ld is a multiple of 32, not of NTS):
+            // those columns are never reduced, so they are simply not loaded
+            if (c0 + part * 2 < p.ldx)
+                cp_async16(Xs + k * XSTRIDE + part * 2, p.x + (int64_t)sJ[k] * p.ldx + c0 + part * 2);
         }
         cp_async_commit();
         cp_async_wait<0>();
@@ -113,6 +116,7 @@ __global__ void __launch_bounds__(128) k_sigma_ss(const SsParams p) {
 #pragma unroll
             for (int nb = 0; nb < NTS / 8; ++nb) dmma_16x8x4(acc[nb], a0[j], a1[j], Xk[nb * 8]);
         }
+        __syncthreads();  // Ys aliases Xs
 #pragma unroll
         for (int nb = 0; nb < NTS / 8; ++nb) {
             const int col = nb * 8 + 2 * t;
@@ -208,7 +212,7 @@ SsPlan plan_sigma_ss(int norb, int nel) {
     pl.warps = (pl.P + 15) / 16;
     const int KPP = pl.KSS * 4;
     const int rows = std::max(KPP, 16 * pl.warps);
-    pl.smem = (size_t)KPP * XSTRIDE * 8 + (size_t)rows * NTS * 8 + (size_t)KPP * 8 + (size_t)KPP * 8 + 16;
+    pl.smem = (size_t)std::max(KPP * XSTRIDE, rows * NTS) * 8 + (size_t)KPP * 8 + (size_t)KPP * 8 + 16;
     if (pl.KSS > 16 || pl.warps > 4) throw InvalidArgument("sigma_ss: orbital space too large for this build");
     return pl;
 }

@@ -1,0 +1,235 @@
+"""GPU parity: the CUDA product path (libsbg.so through the C ABI) against the oracle and the
+reference's golden outputs. Bars (north star): bit-exact strings / link tables / diagonal;
+sigma within 1e-12 relative (max|d| / max|sigma|); converged energies within 1e-8 Eh."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2603_06101_b200 as P
+from paper_2603_06101_b200 import _lib
+from oracle import Problem, baseline_problem
+
+pytestmark = pytest.mark.gpu
+SIGMA_RTOL = 1e-12
+E_TOL = 1e-8
+
+
+def gold(gold_dir, tag):
+    with open(os.path.join(gold_dir, f"golden_{tag}.json")) as f:
+        return json.load(f)
+
+
+def seeded(n, seed=7):
+    x = np.random.default_rng(seed).uniform(-1.0, 1.0, n)
+    return x / np.linalg.norm(x)
+
+
+def to_product(q):
+    return P.FciProblem(q.norb, q.nelec, q.ms2, q.e_core, q.h1.copy(), q.eri.copy())
+
+
+def fixture(gold_dir, name):
+    p = P.parse_fcidump_file(os.path.join(gold_dir, f"{name}.fcidump"))
+    return p, Problem(p.norb, p.nelec, p.ms2, p.e_core, p.h1, p.eri, name)
+
+
+ODD = [(4, 1, 1, -0.75, 5), (5, 5, 1, 0.3, 9), (7, 5, -1, 0.0, 11), (6, 2, 2, 0.1, 13), (8, 6, 0, 1.0, 17)]
+
+
+def odd_problem(rest, spec):
+    norb, nelec, ms2, ecore, seed = spec
+    h1, eri = rest.synthetic(norb, seed, 0.06)
+    return Problem(norb, nelec, ms2, ecore, h1, eri, f"{norb}o{nelec}e{ms2}")
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if _lib.lib().sbg_device_count() < 1:
+        pytest.fail("no CUDA device visible to libsbg")
+    return 0
+
+
+def test_dmma_fragment_selftest(dev):
+    _lib.check(_lib.lib().sbg_selftest())
+
+
+def _check_tables_diag(rest, q):
+    op = P.FciOperator(to_product(q), max_determinants=2 ** 62)
+    try:
+        for spin, k in ((0, q.n_alpha), (1, q.n_beta)):
+            s, l = op.string_tables(spin)
+            assert np.array_equal(s, rest.strings(q.norb, k))
+            rp, rq, rt, rs = rest.links(q.norb, k)
+            assert np.array_equal(l["p"], rp) and np.array_equal(l["q"], rq)
+            assert np.array_equal(l["target"], rt) and np.array_equal(l["sign"], rs)
+        assert np.array_equal(op.diagonal(), rest.diag(q))   # bit-exact (no FMA, same order)
+    finally:
+        op.close()
+
+
+@pytest.mark.parametrize("which", ["h4_2e", "h6_4e", "c0", "c1", "c2", "odd0", "odd1", "odd2", "odd3"])
+def test_tables_and_diagonal_bit_exact(dev, rest, gold_dir, which):
+    if which.startswith("h"):
+        q = fixture(gold_dir, which)[1]
+    elif which.startswith("odd"):
+        q = odd_problem(rest, ODD[int(which[3:])])
+    else:
+        q = baseline_problem(int(which[1]), rest)
+    _check_tables_diag(rest, q)
+
+
+@pytest.mark.parametrize("which", ["h4_2e", "h6_4e", "c0", "c1", "odd0", "odd1", "odd2", "odd3", "odd4"])
+def test_sigma_matches_oracle(dev, rest, gold_dir, which):
+    if which.startswith("h"):
+        q = fixture(gold_dir, which)[1]
+    elif which.startswith("odd"):
+        q = odd_problem(rest, ODD[int(which[3:])])
+    else:
+        q = baseline_problem(int(which[1]), rest)
+    op = P.FciOperator(to_product(q), max_determinants=2 ** 62)
+    n = op.dim()
+    X = np.stack([seeded(n, s) for s in (7, 8, 9)])
+    Y = op.apply(X)
+    assert op.apply_count() == 3
+    for x, y in zip(X, Y):
+        ref = rest.sigma(q, x, exact=True)
+        assert np.abs(y - ref).max() <= SIGMA_RTOL * np.abs(ref).max()
+    if which.startswith("h"):   # reference's own sigma on the fixture (golden)
+        ref = np.load(os.path.join(gold_dir, f"{which}_sigma.npy"))
+        assert np.abs(Y[0] - ref).max() <= SIGMA_RTOL * np.abs(ref).max()
+    # exact columns of H == Slater-Condon dense oracle (test_sigma.cpp:39-52: abs <= 1e-12)
+    if n <= 400:
+        H = rest.dense_h(q)
+        cols = op.apply(np.eye(n)[: min(n, 64)])
+        assert np.abs(cols - H[: min(n, 64)]).max() <= 1e-12 * max(1.0, np.abs(H).max())
+    op.close()
+
+
+def test_sigma_c2_against_reference_golden(dev, rest, gold_dir):
+    q = baseline_problem(2, rest)
+    g = gold(gold_dir, "c2")
+    op = P.FciOperator(to_product(q), max_determinants=2 ** 62)
+    x = seeded(op.dim())
+    y = op.apply(x)
+    rows = np.load(os.path.join(gold_dir, "c2_sigma_rows.npy"))
+    ref = np.load(os.path.join(gold_dir, "c2_sigma_vals.npy"))
+    assert np.abs(y[rows] - ref).max() <= SIGMA_RTOL * np.abs(ref).max()
+    assert abs(float(y @ x) - g["sigma_dot_x"]) <= 1e-12 * abs(g["sigma_dot_x"])
+    assert abs(float(np.linalg.norm(y)) - g["sigma_norm"]) <= 1e-12 * g["sigma_norm"]
+    d = op.diagonal()
+    assert np.array_equal(d[rows], np.load(os.path.join(gold_dir, "c2_diag_vals.npy")))
+    assert np.lexsort((np.arange(len(d)), d))[:8].tolist() == g["diag_lowest"]
+    op.close()
+
+
+@pytest.mark.parametrize("idx", [3, 4])
+def test_sigma_full_size_properties(dev, rest, idx):
+    """(14e,14o) and (16e,16o): sampled rows vs the Slater-Condon row oracle, hermiticity,
+    linearity and the diagonal (size-independent checks; the serial oracle cannot run a full sigma)."""
+    q = baseline_problem(idx, rest)
+    op = P.FciOperator(to_product(q), max_determinants=2 ** 62)
+    n = op.dim()
+    rng = np.random.default_rng(idx)
+    x = rng.uniform(-1, 1, n)
+    y = op.apply(x)
+    rows = np.sort(rng.choice(n, 48, replace=False))
+    ref = rest.sigma_rows(q, x, rows)
+    scale = np.abs(ref).max()
+    assert np.abs(y[rows] - ref).max() <= SIGMA_RTOL * scale
+    # diagonal rows: sigma(e_i)_i == D_i
+    d = op.diagonal()
+    i0 = int(np.argmin(d))
+    e = np.zeros(n)
+    e[i0] = 1.0
+    col = op.apply(e)
+    assert abs(col[i0] - d[i0]) <= 1e-13 * abs(d[i0])
+    # hermiticity and linearity (dots accumulated chunk-wise with fsum: a plain BLAS ddot over
+    # 1.7e8 terms carries O(1) rounding error at these magnitudes)
+    import math
+
+    def dot(u, v):
+        return math.fsum(float(np.dot(u[i:i + 65536], v[i:i + 65536])) for i in range(0, len(u), 65536))
+
+    b = rng.uniform(-1, 1, n)
+    hb = op.apply(b)
+    assert abs(dot(x, hb) - dot(y, b)) <= 1e-12 * np.linalg.norm(x) * np.linalg.norm(b) * scale
+    hz = op.apply(2.0 * x - 3.0 * b)
+    assert np.abs(hz - (2.0 * y - 3.0 * hb)).max() <= 1e-12 * scale * 5
+    op.close()
+
+
+@pytest.mark.parametrize("name", ["h4_2e", "h6_4e"])
+def test_sbci1_fixtures_match_reference(dev, gold_dir, name):
+    p, _ = fixture(gold_dir, name)
+    g = gold(gold_dir, name)
+    op = P.as_operator(p, p.ms2)
+    res = P.solve_n_states_sbci1(op, 3)
+    e = np.array([pp.energy for pp in res.pairs])
+    assert np.abs(e - np.array(g["sbci1"]["energies"])).max() <= E_TOL
+    assert np.abs(e - np.array(g["dense_eigs"][:3])).max() <= 1e-10        # test_sigma.cpp:109-119
+    assert [pp.iterations for pp in res.pairs] == g["sbci1"]["iterations"]
+    assert res.summary.matvecs == g["sbci1"]["matvecs"]
+    for pp in res.pairs:
+        assert abs(np.linalg.norm(pp.vector) - 1.0) <= 1e-12
+    V = np.stack([pp.vector for pp in res.pairs])
+    assert np.abs(V @ V.T - np.eye(3)).max() <= 1e-9                        # deflation orthogonality
+    op.close()
+
+
+@pytest.mark.parametrize("idx", [0, 1, 2])
+def test_sbci1_baseline_configs_match_reference(dev, rest, gold_dir, idx):
+    q = baseline_problem(idx, rest)
+    g = gold(gold_dir, q.name)["sbci1"]
+    op = P.FciOperator(to_product(q), max_determinants=2 ** 62)
+    records = []
+    res = P.solve_n_states_sbci1(op, len(g["energies"]), sink=records.append)
+    e = np.array([pp.energy for pp in res.pairs])
+    assert np.abs(e - np.array(g["energies"])).max() <= E_TOL
+    # same trajectory as the reference: iterations, restarts and matvec budget
+    assert [pp.iterations for pp in res.pairs] == g["iterations"]
+    assert [pp.restarts for pp in res.pairs] == g["restarts"]
+    assert res.summary.matvecs == g["matvecs"]
+    assert len(records) == res.summary.total_iterations
+    assert all(r.matvecs <= res.summary.matvecs for r in records)
+    op.close()
+
+
+@pytest.mark.parametrize("k", [0, 1, 2, 3, 4])
+def test_sbci1_odd_sectors_vs_dense(dev, rest, k):
+    q = odd_problem(rest, ODD[k])
+    H = rest.dense_h(q)
+    ev = np.linalg.eigvalsh(0.5 * (H + H.T))
+    op = P.FciOperator(to_product(q), max_determinants=2 ** 62)
+    nr = min(2, op.dim())
+    res = P.solve_n_states_sbci1(op, nr)
+    assert np.abs(np.array([pp.energy for pp in res.pairs]) - ev[:nr]).max() <= 1e-9
+    op.close()
+
+
+def test_operator_contract(dev, gold_dir):
+    p, _ = fixture(gold_dir, "h4_2e")
+    op = P.as_operator(p, p.ms2)
+    v = np.ones(op.dim())
+    for _ in range(5):
+        op.apply(v)
+    assert op.apply_count() == 5                                            # test_sigma.cpp:133-139
+    op.reset_apply_count()
+    assert op.apply_count() == 0
+    with pytest.raises(ValueError, match="dimension mismatch"):
+        op.apply(np.ones(op.dim() + 1))
+    with pytest.raises(P.NonConvergenceError):
+        P.solve_n_states_sbci1(op, 1, P.SolverConfig(t_max=2))
+    op.close()
+
+
+def test_kernel_launch_accounting(dev, rest):
+    q = baseline_problem(1, rest)
+    op = P.FciOperator(to_product(q), max_determinants=2 ** 62)
+    before = op.kernel_launches()
+    op.apply(seeded(op.dim()))
+    assert op.kernel_launches() - before >= 4    # transpose, same-spin x2, transpose, alpha-beta
+    f = op.sigma_flops()
+    assert f["alpha_beta"] > 0 and f["same_spin"] > 0
+    op.close()
