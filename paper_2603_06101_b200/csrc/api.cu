@@ -251,11 +251,11 @@ int sbg_sigma(sbg_ctx* ctx, const double* x, double* y, int nvec) {
         require_ctx(ctx);
         if (nvec < 0 || (!x && nvec) || (!y && nvec)) throw std::invalid_argument("sbg_sigma: bad arguments");
         auto& c = *ctx->c;
-        sbg::DBuf dx = c.alloc_vec(), dy = c.alloc_vec();
+        double *dx = c.io_x(), *dy = c.io_y();
         for (int v = 0; v < nvec; ++v) {
-            c.upload_local(x + (size_t)v * c.ndet, dx.p, c.st);
-            c.sigma(dx, dy);
-            c.download_local(dy.p, y + (size_t)v * c.ndet + c.row_lo * c.NB, c.st);
+            c.upload_local(x + (size_t)v * c.ndet, dx, c.st);
+            c.sigma(dx, dy, c.st);
+            c.download_local(dy, y + (size_t)v * c.ndet + c.row_lo * c.NB, c.st);
         }
         SBG_CUDA(cudaStreamSynchronize(c.st));
     });
@@ -294,10 +294,10 @@ int sbg_sigma_device(sbg_ctx* ctx, const double* d_x, double* d_y, void* stream)
         require_ctx(ctx);
         auto& c = *ctx->c;
         cudaStream_t s = stream ? (cudaStream_t)stream : c.st;
-        sbg::DBuf px = c.alloc_vec(), py = c.alloc_vec();
-        c.pack_device(d_x, px.p, s);
-        c.sigma(px.p, py.p, s);
-        c.unpack_device(py.p, d_y + c.row_lo * c.NB, s);
+        double *px = c.io_x(), *py = c.io_y();
+        c.pack_device(d_x, px, s);
+        c.sigma(px, py, s);
+        c.unpack_device(py, d_y + c.row_lo * c.NB, s);
         SBG_CUDA(cudaStreamSynchronize(s));
     });
 }

@@ -13,7 +13,10 @@ namespace sbg {
 DBuf::DBuf(int64_t count) : n(count) {
     if (count > 0) {
         SBG_CUDA(cudaMalloc(&p, (size_t)count * sizeof(double)));
-        SBG_CUDA(cudaMemset(p, 0, (size_t)count * sizeof(double)));
+        // the library works on a non-blocking stream, which does not order against the legacy
+        // default stream a plain cudaMemset runs on: finish the zero-fill before handing out p
+        SBG_CUDA(cudaMemsetAsync(p, 0, (size_t)count * sizeof(double), cudaStreamLegacy));
+        SBG_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
     }
 }
 DBuf::~DBuf() {
@@ -190,10 +193,11 @@ void Context::build_tables(const double* h1, const double* eri) {
         d_sc_ent_ = dmalloc<uint16_t>(ent.size());
         d_sc_tt_ = dmalloc<uint32_t>(tt.size());
         d_sc_te_ = dmalloc<uint32_t>(te.size());
-        SBG_CUDA(cudaMemcpy(d_sc_tgt_, tgt.data(), tgt.size() * 4, cudaMemcpyHostToDevice));
-        SBG_CUDA(cudaMemcpy(d_sc_ent_, ent.data(), ent.size() * 2, cudaMemcpyHostToDevice));
-        SBG_CUDA(cudaMemcpy(d_sc_tt_, tt.data(), tt.size() * 4, cudaMemcpyHostToDevice));
-        SBG_CUDA(cudaMemcpy(d_sc_te_, te.data(), te.size() * 4, cudaMemcpyHostToDevice));
+        SBG_CUDA(cudaMemcpyAsync(d_sc_tgt_, tgt.data(), tgt.size() * 4, cudaMemcpyHostToDevice, st));
+        SBG_CUDA(cudaMemcpyAsync(d_sc_ent_, ent.data(), ent.size() * 2, cudaMemcpyHostToDevice, st));
+        SBG_CUDA(cudaMemcpyAsync(d_sc_tt_, tt.data(), tt.size() * 4, cudaMemcpyHostToDevice, st));
+        SBG_CUDA(cudaMemcpyAsync(d_sc_te_, te.data(), te.size() * 4, cudaMemcpyHostToDevice, st));
+        SBG_CUDA(cudaStreamSynchronize(st));
     }
     // same-spin antisymmetrized pair integrals W(pr,qs) = (pq|rs) - (ps|rq), p<r, q<s
     if (norb >= 2) {

@@ -52,6 +52,15 @@ public:
 
     int64_t padded_len() const { return nrows * ld; }
     DBuf alloc_vec() const;  // zero-initialised padded local vector
+    // persistent staging vectors of the host-pointer entry points (sbg_sigma, sbg_sigma_device)
+    double* io_x() {
+        if (io_x_.empty()) io_x_ = alloc_vec();
+        return io_x_.p;
+    }
+    double* io_y() {
+        if (io_y_.empty()) io_y_ = alloc_vec();
+        return io_y_.p;
+    }
 
     // y = H x on padded local vectors (counts one application)
     void sigma(const double* x_local, double* y_local, cudaStream_t s);
@@ -98,7 +107,7 @@ private:
     uint16_t* d_sc_ent_ = nullptr;
     DBuf diag_;
     // sigma workspaces
-    DBuf xfull_, xT_, sT_, saa_, a2a_send_, a2a_recv_;
+    DBuf xfull_, xT_, sT_, saa_, a2a_send_, a2a_recv_, io_x_, io_y_;
     AbPlan ab_{};
     SsPlan ssa_{}, ssb_{};
     bool have_ab_ = false;

@@ -228,7 +228,10 @@ __global__ void __launch_bounds__(256, 1) k_sigma_ab(const AbParams p) {
                             const double gv = G[en & 0x7FFF];
                             v += (en & 0x8000) ? -gv : gv;
                         }
-                        srow[tg >> 16] += v;
+                        // the 16-byte padding that ends a tile's segment (zeros) is an empty
+                        // segment: skip it, or its +0 read-modify-write of srow[0] would race
+                        // with the real update of target 0 by another thread
+                        if (end > beg) srow[tg >> 16] += v;
                     }
                 }
             };
