@@ -140,7 +140,7 @@ def profile_traffic(cfg_name):
     path = os.path.join(ROOT, "profiles", "ab_kernel_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get(cfg_name)
+            return json.load(f)[cfg_name]["dram_bytes_per_launch"]   # ncu --set full, per launch
     except Exception:
         return None
 

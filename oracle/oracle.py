@@ -220,3 +220,25 @@ def baseline_problem(idx, rest=None):
     rest = rest or Restatement()
     h1, eri = rest.synthetic(c["norb"], BASELINE_SEED, c["offdiag"])
     return Problem(c["norb"], c["nelec"], 0, 0.0, h1, eri, name=c["name"])
+
+
+class RefGpu:
+    """oracle/_ref/libsbci_ref_gpu.so: the reference's own drivers on the B200 sigma."""
+
+    PATH = os.path.join(HERE, "_ref", "libsbci_ref_gpu.so")
+
+    @classmethod
+    def available(cls):
+        return os.path.exists(cls.PATH)
+
+    def __init__(self):
+        self.lib = C.CDLL(self.PATH)
+        self.lib.refgpu_last_error.restype = C.c_char_p
+
+    def solve(self, P, nroots, method=1):
+        e = np.zeros(nroots); it = np.zeros(nroots, np.int32); mv = np.zeros(1, np.uint64)
+        rc = self.lib.refgpu_solve(*P.args(), method, nroots, _dp(e), it.ctypes.data_as(C.c_void_p),
+                                   mv.ctypes.data_as(C.c_void_p))
+        if rc != 0:
+            raise RuntimeError(self.lib.refgpu_last_error().decode())
+        return dict(energies=e, iterations=it, matvecs=int(mv[0]))

@@ -233,3 +233,20 @@ def test_kernel_launch_accounting(dev, rest):
     f = op.sigma_flops()
     assert f["alpha_beta"] > 0 and f["same_spin"] > 0
     op.close()
+
+
+@pytest.mark.parametrize("name,method", [("h6_4e", 1), ("h6_4e", 2), ("h6_4e", 3), ("c1", 1)])
+def test_reference_drivers_run_on_gpu_sigma(dev, rest, gold_dir, name, method):
+    """Drop-in: the reference's own solve_n_states_sbci1/_sbci2/davidson_solve (compiled unmodified)
+    with a SymmetricOperator whose apply_impl calls sbg_sigma (oracle/ref_gpu_shim.cpp)."""
+    from oracle import RefGpu
+    if not RefGpu.available():
+        pytest.skip("oracle/_ref/libsbci_ref_gpu.so not built")
+    q = fixture(gold_dir, name)[1] if name.startswith("h") else baseline_problem(1, rest)
+    g = gold(gold_dir, name)
+    key = {1: "sbci1", 2: "sbci2", 3: "davidson"}[method]
+    nroots = len(g[key]["energies"])
+    r = RefGpu().solve(q, nroots, method)
+    assert np.abs(r["energies"] - np.array(g[key]["energies"])).max() <= E_TOL
+    if method == 1:
+        assert r["iterations"].tolist() == g[key]["iterations"] and r["matvecs"] == g[key]["matvecs"]
