@@ -6,20 +6,18 @@
 // is the reference's spin-summed contraction (fci/sigma.hpp:86-137) restricted to its alpha-beta
 // cross terms plus both one-body terms; the same-spin two-body terms come from sigma_ss.cu.
 // One CTA owns one alpha row Ia at a time (persistent over rows) and keeps sigma(Ia,:) in shared
-// memory. Per NT-column tile of beta strings Jb:
+// memory. Per 32-column tile of beta strings Jb:
 //   gather  D[k][Jb] = c(J_k, Jb) for the K = 1 + n_a(norb-n_a) distinct alpha strings J_k linked
-//           to Ia (k=0 is Ia itself carrying all occupation entries; sigma.hpp:33-35);
+//           to Ia (k=0 is Ia itself carrying all occupation entries; sigma.hpp:33-35) — cp.async,
+//           3-stage pipeline;
 //   DGEMM   G[rs][Jb] = sum_k A[rs][k] D[k][Jb], A[rs][k] = sign_k V'(pair_k, rs), M = npair =
 //           norb(norb+1)/2 packed symmetric pairs, A resident in registers for the whole row —
-//           mma.sync m16n8k4 / m8n8k4 f64 (SASS DMMA.8x8x4);
-//   scatter sigma(Ia, Ib) += sum over the tile's (rs, Jb) with E_rs Jb = Ib of sign * G[rs][Jb],
-//           through per-tile target-sorted segment lists precomputed once (build_ab_scatter):
-//           every target of a tile is reduced by one thread in a fixed order — no atomics,
-//           bit-reproducible sums.
-// Warp specialisation: warps 0..7 only issue DMMAs (A in registers) and stage G; warps 8..11
-// gather D tiles and scatter lists with cp.async (3 stages) and run the scatter. The two groups
-// hand tiles over with named barriers (bar.arrive / bar.sync), so the FP64 tensor pipe never waits
-// for the scatter. The row is written once: y(Ia,:) = [y(Ia,:)] + sigma_row + e_core c(Ia,:).
+//           mma.sync m16n8k4 / m8n8k4 f64 (SASS DMMA.8x8x4); G staged once in shared memory;
+//   scatter sigma(Ia, Ib) += sum over the tile's (rs, Jb) with E_rs Jb = Ib of sign * G[rs][Jb].
+//           The (rs,Jb) -> Ib map depends only on the tile, so it is precomputed once as a
+//           target-sorted segment list (build_ab_scatter): every target of a tile is reduced by
+//           one thread in a fixed order — no atomics, bit-reproducible sums.
+// The row is then written once: y(Ia,:) = [y(Ia,:)] + sigma_row + e_core c(Ia,:).
 #include <algorithm>
 #include <cstdlib>
 #include <vector>
@@ -30,26 +28,13 @@ namespace sbg {
 
 namespace {
 
-constexpr int MMA_WARPS = 8, HELPER_WARPS = 4;
-constexpr int THREADS = 32 * (MMA_WARPS + HELPER_WARPS);
-constexpr int MMA_THREADS = 32 * MMA_WARPS, HELPER_THREADS = 32 * HELPER_WARPS;
-constexpr int SD = 3;         // D tile / scatter-list stages
-constexpr int SG = 2;         // staged G tiles
-// named barriers (0 is __syncthreads)
-constexpr int BAR_DFULL = 1;  // + stage (SD of them)
-constexpr int BAR_GFULL = 4;  // + G buffer
-constexpr int BAR_GEMPTY = 6; // + G buffer
-constexpr int BAR_MMA = 8;    // DMMA warps only
-constexpr int BAR_HELPER = 9; // load / scatter warps only
-
+// NT: beta-string tile width (16 or 32 columns); chosen per sector by shared-memory budget.
 template <int NT> struct Tile {
     static constexpr int NBT = NT / 8;         // n8 blocks per tile
     static constexpr int DSTRIDE = NT + 4;     // D row stride: bank-conflict-free B fragments (== 4 mod 16)
     static constexpr int GSTRIDE = NT + 1;     // staged G row stride
 };
-
-__device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
+constexpr int STAGES = 2;     // D tiles, G tiles and scatter lists are double buffered
 
 struct AbParams {
     const double* x;
@@ -57,45 +42,44 @@ struct AbParams {
     const double* Vp;
     const uint32_t* tgt;        // per tile: (target << 16) | segment end, concatenated
     const uint16_t* ent;        // per tile: (G offset) | (negative << 15), target-sorted
-    const uint32_t* tile_tgt;   // [ntiles+1] offsets into tgt (16-byte aligned segments)
+    const uint32_t* tile_tgt;   // [ntiles+1] offsets into tgt
     const uint32_t* tile_ent;   // [ntiles+1] offsets into ent
     int norb, na_el, npair, mb16, extra, K, KP, grows, maxT, maxE;
     int64_t NB, ld, row_lo, row_hi;
     double e_core;
     int accumulate;
-    int dbg;  // profiling experiments only (SBG_AB_DEBUG): 1 = skip scatter, 4 = scatter without FP64 adds
+    int dbg;  // profiling experiments only: 1 = skip scatter, 2 = skip MMA
 };
 
+// Software pipeline per alpha row, one __syncthreads per tile: iteration `it` prefetches D(it+1)
+// and the scatter lists of tile it, runs the DMMAs of tile it into G[it&1], and scatters tile it-1
+// from G[(it-1)&1] — so warps that finish their MMAs scatter while the others still feed the
+// FP64 tensor pipe.
 template <int KS, int NT>
-__global__ void __launch_bounds__(THREADS, 1) k_sigma_ab(const AbParams p) {
+__global__ void __launch_bounds__(256, 1) k_sigma_ab(const AbParams p) {
     constexpr int NBT = Tile<NT>::NBT, DSTRIDE = Tile<NT>::DSTRIDE, GSTRIDE = Tile<NT>::GSTRIDE;
-    constexpr int KP = KS * 4;
-    constexpr int KH = (KS + 1) / 2;  // k-steps of the first half (extra rows are split in k)
     extern __shared__ __align__(16) double smem[];
+    const int KP = KS * 4;
     const int ntiles = (int)(p.ld / NT);
     double* srow = smem;                                             // [ld]
-    double* Ds = srow + p.ld;                                        // [SD][KP][DSTRIDE]
-    double* sAe = Ds + SD * KP * DSTRIDE;                            // [KP][8] A of the extra m8 rows
-    double* Gs = sAe + KP * 8;                                       // [SG][grows][GSTRIDE]
-    uint32_t* Lt = reinterpret_cast<uint32_t*>(Gs + SG * p.grows * GSTRIDE);  // [SD][maxT]
-    uint16_t* Le = reinterpret_cast<uint16_t*>(Lt + SD * p.maxT);             // [SD][maxE]
-    uint32_t* sTT = reinterpret_cast<uint32_t*>(Le + SD * p.maxE);            // [ntiles+1]
-    uint32_t* sTE = sTT + ntiles + 1;                                         // [ntiles+1]
-    int* sJ = reinterpret_cast<int*>(sTE + ntiles + 1);                       // [KP]
+    double* Ds = srow + p.ld;                                        // [STAGES][KP][DSTRIDE]
+    double* sAe = Ds + STAGES * KP * DSTRIDE;                        // [KP][8] A of the extra m8 rows
+    double* Gs = sAe + KP * 8;                                       // [STAGES][grows][GSTRIDE]
+    uint32_t* Lt = reinterpret_cast<uint32_t*>(Gs + STAGES * p.grows * GSTRIDE);  // [STAGES][maxT]
+    uint16_t* Le = reinterpret_cast<uint16_t*>(Lt + STAGES * p.maxT);             // [STAGES][maxE]
+    uint32_t* sTT = reinterpret_cast<uint32_t*>(Le + STAGES * p.maxE);            // [ntiles+1]
+    uint32_t* sTE = sTT + ntiles + 1;                                             // [ntiles+1]
+    int* sJ = reinterpret_cast<int*>(sTE + ntiles + 1);                           // [KP]
     int* sPair = sJ + KP;                                 // [KP]  -1 = occupation row, -2 = padding
     double* sSign = reinterpret_cast<double*>(sPair + KP);  // [KP] (8-byte aligned: KP % 4 == 0)
 
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, nthr = blockDim.x;
     const int w = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
     const int norb = p.norb, npair = p.npair;
-    const bool is_mma = w < MMA_WARPS;
     const bool main_ok = w < p.mb16;
-    // extra m8 rows (npair % 16 <= 8): warps 0..2*NBT-1, n8 block (w % NBT), k half (w / NBT)
-    const bool do_extra = p.extra && w < 2 * NBT;
-    const int ex_nb = w % NBT, ex_half = w / NBT;
-    const int r0 = 16 * w + g, re = 16 * p.mb16;
+    const bool do_extra = p.extra && w < NBT;  // extra m8 rows: one n8 block per warp
 
-    for (int i = tid; i <= ntiles; i += THREADS) {
+    for (int i = tid; i <= ntiles; i += nthr) {
         sTT[i] = p.tile_tgt[i];
         sTE[i] = p.tile_ent[i];
     }
@@ -104,7 +88,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_sigma_ab(const AbParams p) {
         __syncthreads();  // previous row fully written out
         const uint64_t sa = string_unrank((uint64_t)ia, p.na_el, norb);
         // ---- K-list: k=0 the row itself (occupation entries), k>=1 singles (q occ asc, p virt asc)
-        for (int k = tid; k < KP; k += THREADS) {
+        for (int k = tid; k < KP; k += nthr) {
             int J = (int)ia, pr = -2;
             double sg = 0.0;
             if (k == 0) {
@@ -128,9 +112,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_sigma_ab(const AbParams p) {
             sPair[k] = pr;
             sSign[k] = sg;
         }
-        for (int64_t c = tid; c < p.ld; c += THREADS) srow[c] = 0.0;
+        for (int64_t c = tid; c < p.ld; c += nthr) srow[c] = 0.0;
         __syncthreads();
 
+        // ---- A fragments: rows rs of the packed pair space, columns k of the K-list
         auto aval = [&](int rs, int k) -> double {
             if (rs >= npair || k >= p.K) return 0.0;
             const int pr = sPair[k];
@@ -144,152 +129,129 @@ __global__ void __launch_bounds__(THREADS, 1) k_sigma_ab(const AbParams p) {
             }
             return sSign[k] * p.Vp[(size_t)pr * npair + rs];
         };
+        double a0[KS], a1[KS];
+        const int r0 = 16 * w + g, re = 16 * p.mb16;
+#pragma unroll
+        for (int j = 0; j < KS; ++j) {
+            const int k = 4 * j + t;
+            a0[j] = main_ok ? aval(r0, k) : 0.0;
+            a1[j] = main_ok ? aval(r0 + 8, k) : 0.0;
+        }
+        if (p.extra)
+            for (int i = tid; i < KP * 8; i += nthr) sAe[i] = aval(re + (i & 7), i >> 3);
 
-        if (is_mma) {
-            // =============================== DMMA warps ===============================
-            double a0[KS], a1[KS];
-#pragma unroll
-            for (int j = 0; j < KS; ++j) {
-                const int k = 4 * j + t;
-                a0[j] = main_ok ? aval(r0, k) : 0.0;
-                a1[j] = main_ok ? aval(r0 + 8, k) : 0.0;
+        auto load_d = [&](int stage, int jt) {
+            double* dst = Ds + stage * KP * DSTRIDE;
+            for (int c = tid; c < KP * (NT / 2); c += nthr) {
+                const int k = c / (NT / 2), part = c % (NT / 2);
+                cp_async16(dst + k * DSTRIDE + part * 2, p.x + (int64_t)sJ[k] * p.ld + (int64_t)jt * NT + part * 2);
             }
-            if (p.extra)
-                for (int i = tid; i < KP * 8; i += MMA_THREADS) sAe[i] = aval(re + (i & 7), i >> 3);
-            nbar_sync(BAR_MMA, MMA_THREADS);  // sAe complete among the DMMA warps
+        };
+        auto load_lists = [&](int stage, int jt) {  // 16-byte aligned, padded segments
+            const uint32_t t0 = sTT[jt], nt4 = (sTT[jt + 1] - t0 + 3) / 4;
+            const uint32_t e0 = sTE[jt], ne8 = (sTE[jt + 1] - e0 + 7) / 8;
+            for (uint32_t c = tid; c < nt4; c += nthr) cp_async16(Lt + stage * p.maxT + 4 * c, p.tgt + t0 + 4 * c);
+            for (uint32_t c = tid; c < ne8; c += nthr) cp_async16(Le + stage * p.maxE + 8 * c, p.ent + e0 + 8 * c);
+        };
+        load_d(0, 0);
+        cp_async_commit();
 
-            for (int it = 0; it < ntiles; ++it) {
-                const int sd = it % SD, sg = it & 1;
-                nbar_sync(BAR_DFULL + sd, THREADS);
-                const double* D = Ds + sd * KP * DSTRIDE;
-                double acc[NBT][4];
-                double ace[2] = {0.0, 0.0};
-#pragma unroll
-                for (int nb = 0; nb < NBT; ++nb)
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) acc[nb][e] = 0.0;
-                if (main_ok) {
-                    double b[2][NBT];
-#pragma unroll
-                    for (int nb = 0; nb < NBT; ++nb) b[0][nb] = D[t * DSTRIDE + g + nb * 8];
-#pragma unroll
-                    for (int j = 0; j < KS; ++j) {
-                        const int cur = j & 1;
-                        if (j + 1 < KS) {
-#pragma unroll
-                            for (int nb = 0; nb < NBT; ++nb) b[cur ^ 1][nb] = D[(4 * (j + 1) + t) * DSTRIDE + g + nb * 8];
-                        }
-#pragma unroll
-                        for (int nb = 0; nb < NBT; ++nb) dmma_16x8x4(acc[nb], a0[j], a1[j], b[cur][nb]);
-                    }
-                }
-                if (do_extra) {
-                    const int j0 = ex_half ? KH : 0, j1 = ex_half ? KS : KH;
-                    for (int j = j0; j < j1; ++j) {
-                        const double ae = sAe[(4 * j + t) * 8 + g];
-                        const double be = D[(4 * j + t) * DSTRIDE + g + ex_nb * 8];
-                        dmma_8x8x4(ace, ae, be);
-                    }
-                }
-                if (it >= SG) nbar_sync(BAR_GEMPTY + sg, THREADS);  // scatter of tile it-2 done
-                double* G = Gs + sg * p.grows * GSTRIDE;
-                if (main_ok) {
-#pragma unroll
-                    for (int nb = 0; nb < NBT; ++nb) {
-                        const int col = nb * 8 + 2 * t;
-                        G[r0 * GSTRIDE + col] = acc[nb][0];
-                        G[r0 * GSTRIDE + col + 1] = acc[nb][1];
-                        G[(r0 + 8) * GSTRIDE + col] = acc[nb][2];
-                        G[(r0 + 8) * GSTRIDE + col + 1] = acc[nb][3];
-                    }
-                }
-                if (do_extra) {  // the two k halves land in rows re.. and re+8.. (summed by the scatter lists)
-                    const int row = re + 8 * ex_half + g;
-                    G[row * GSTRIDE + ex_nb * 8 + 2 * t] = ace[0];
-                    G[row * GSTRIDE + ex_nb * 8 + 2 * t + 1] = ace[1];
-                }
-                nbar_arrive(BAR_GFULL + sg, THREADS);
-            }
-        } else {
-            // ============================ load / scatter warps =========================
-            const int ht = tid - MMA_THREADS;
-            auto load_tile = [&](int jt) {
-                const int s = jt % SD;
-                double* dst = Ds + s * KP * DSTRIDE;
-                for (int c = ht; c < KP * (NT / 2); c += HELPER_THREADS) {
-                    const int k = c / (NT / 2), part = c % (NT / 2);
-                    cp_async16(dst + k * DSTRIDE + part * 2, p.x + (int64_t)sJ[k] * p.ld + (int64_t)jt * NT + part * 2);
-                }
-                const uint32_t t0 = sTT[jt], nt4 = (sTT[jt + 1] - t0 + 3) / 4;
-                const uint32_t e0 = sTE[jt], ne8 = (sTE[jt + 1] - e0 + 7) / 8;
-                for (uint32_t c = ht; c < nt4; c += HELPER_THREADS) cp_async16(Lt + s * p.maxT + 4 * c, p.tgt + t0 + 4 * c);
-                for (uint32_t c = ht; c < ne8; c += HELPER_THREADS) cp_async16(Le + s * p.maxE + 8 * c, p.ent + e0 + 8 * c);
-            };
-            auto scatter = [&](int jt) {
-                const double* G = Gs + (jt & 1) * p.grows * GSTRIDE;
-                const uint32_t* lt = Lt + (jt % SD) * p.maxT;
-                const uint16_t* le = Le + (jt % SD) * p.maxE;
-                const uint32_t nt = sTT[jt + 1] - sTT[jt];
-                for (uint32_t i = ht; i < nt; i += HELPER_THREADS) {
-                    const uint32_t tg = lt[i];
-                    const uint32_t beg = (i == 0) ? 0u : (lt[i - 1] & 0xFFFFu);
-                    const uint32_t end = tg & 0xFFFFu;
-                    // the zero padding that ends a tile's segment is an empty segment: skip it,
-                    // or its +0 read-modify-write of srow[0] would race with the real target 0
-                    if (end <= beg) continue;
-                    // signs are applied by flipping the sign bit (integer pipe): the FP64 pipe,
-                    // shared with the DMMA warps, only sees the (entries - 1) + 1 real additions
-                    auto signed_g = [&](uint32_t e) {
-                        const uint16_t en = le[e];
-                        const long long bits = __double_as_longlong(G[en & 0x7FFF]);
-                        return __longlong_as_double(bits ^ ((long long)(en & 0x8000) << 48));
-                    };
-                    if (p.dbg & 4) {  // profiling experiment: same memory traffic, no FP64 adds
-                        long long v = __double_as_longlong(signed_g(beg));
-                        for (uint32_t e = beg + 1; e < end; ++e) v ^= __double_as_longlong(signed_g(e));
-                        srow[tg >> 16] = __longlong_as_double(v);
-                        continue;
-                    }
-                    double v = signed_g(beg);
-                    for (uint32_t e = beg + 1; e < end; ++e) v += signed_g(e);
-                    srow[tg >> 16] += v;
-                }
-            };
-            // cp.async groups: g0..g2 = tiles 0..2, then iteration i commits g(3+i) holding tile i+2
-            // (empty at i = 0), so tile k >= 3 lives in g(k+1) and waiting until <= 1 group is
-            // pending at iteration it always covers tile it.
-#pragma unroll 1
-            for (int s = 0; s < SD; ++s) {
-                if (s < ntiles) load_tile(s);
-                cp_async_commit();
-            }
-            for (int it = 0; it < ntiles; ++it) {
-                cp_async_wait<1>();                // tile it (and its lists) landed (see group numbering below)
-                nbar_arrive(BAR_DFULL + it % SD, THREADS);
-                if (it >= 1) {
-                    const int jt = it - 1;
-                    nbar_sync(BAR_GFULL + (jt & 1), THREADS);   // G(jt) staged (and D(jt) consumed)
-                    if (!(p.dbg & 1)) scatter(jt);
-                    if (jt + SG < ntiles) nbar_arrive(BAR_GEMPTY + (jt & 1), THREADS);
-                    // D stage and list stage of tile jt are free once every helper finished the
-                    // scatter of jt: prefetch tile jt + SD into them
-                    nbar_sync(BAR_HELPER, HELPER_THREADS);
-                    if (jt + SD < ntiles) load_tile(jt + SD);
-                }
-                cp_async_commit();
-            }
-            if (ntiles >= 1) {
-                const int jt = ntiles - 1;
-                nbar_sync(BAR_GFULL + (jt & 1), THREADS);
-                scatter(jt);
-            }
+        for (int it = 0; it <= ntiles; ++it) {
             cp_async_wait<0>();
+            __syncthreads();
+            if (it + 1 < ntiles) load_d((it + 1) & 1, it + 1);
+            if (it < ntiles) load_lists(it & 1, it);
+            cp_async_commit();
+            // warps w and w+4 share an SM sub-partition: one issues its DMMAs while the other
+            // scatters, so the FP64 tensor pipe is not idle during the scatter phase
+            auto do_mma = [&]() {
+            if (it < ntiles) {
+                    const double* D = Ds + (it & 1) * KP * DSTRIDE;
+                    double* G = Gs + (it & 1) * p.grows * GSTRIDE;
+                    double acc[NBT][4];
+                    double ace0[2] = {0.0, 0.0}, ace1[2] = {0.0, 0.0};
+    #pragma unroll
+                    for (int nb = 0; nb < NBT; ++nb)
+    #pragma unroll
+                        for (int e = 0; e < 4; ++e) acc[nb][e] = 0.0;
+                    if (main_ok) {
+                        // B fragments double-buffered in registers: loads of k-step j+1 are in flight
+                        // while the DMMAs of step j issue
+                        double b[2][NBT];
+    #pragma unroll
+                        for (int nb = 0; nb < NBT; ++nb) b[0][nb] = D[t * DSTRIDE + g + nb * 8];
+    #pragma unroll
+                        for (int j = 0; j < KS; ++j) {
+                            const int cur = j & 1;
+                            if (j + 1 < KS) {
+    #pragma unroll
+                                for (int nb = 0; nb < NBT; ++nb) b[cur ^ 1][nb] = D[(4 * (j + 1) + t) * DSTRIDE + g + nb * 8];
+                            }
+    #pragma unroll
+                            for (int nb = 0; nb < NBT; ++nb) dmma_16x8x4(acc[nb], a0[j], a1[j], b[cur][nb]);
+                            if (do_extra) {
+                                const double ae = sAe[(4 * j + t) * 8 + g];
+                                const double be = D[(4 * j + t) * DSTRIDE + g + w * 8];
+                                if (cur) dmma_8x8x4(ace1, ae, be);
+                                else dmma_8x8x4(ace0, ae, be);
+                            }
+                        }
+    #pragma unroll
+                        for (int nb = 0; nb < NBT; ++nb) {
+                            const int col = nb * 8 + 2 * t;
+                            G[r0 * GSTRIDE + col] = acc[nb][0];
+                            G[r0 * GSTRIDE + col + 1] = acc[nb][1];
+                            G[(r0 + 8) * GSTRIDE + col] = acc[nb][2];
+                            G[(r0 + 8) * GSTRIDE + col + 1] = acc[nb][3];
+                        }
+                        if (do_extra) {
+                            G[(re + g) * GSTRIDE + w * 8 + 2 * t] = ace0[0] + ace1[0];
+                            G[(re + g) * GSTRIDE + w * 8 + 2 * t + 1] = ace0[1] + ace1[1];
+                        }
+                    }
+                }
+            };
+            auto do_scatter = [&]() {
+            if (it >= 1) {  // segmented scatter of tile it-1: one thread per distinct target
+                    const int jt = it - 1;
+                    const double* G = Gs + (jt & 1) * p.grows * GSTRIDE;
+                    const uint32_t* lt = Lt + (jt & 1) * p.maxT;
+                    const uint16_t* le = Le + (jt & 1) * p.maxE;
+                    const uint32_t nt = sTT[jt + 1] - sTT[jt];
+                    for (uint32_t i = tid; i < nt; i += nthr) {
+                        const uint32_t tg = lt[i];
+                        const uint32_t beg = (i == 0) ? 0u : (lt[i - 1] & 0xFFFFu);
+                        const uint32_t end = tg & 0xFFFFu;
+                        // the 16-byte padding that ends a tile's segment (zeros) is an empty
+                        // segment: skip it, or its +0 read-modify-write of srow[0] would race
+                        // with the real update of target 0 by another thread
+                        if (end <= beg) continue;
+                        // signs flip the sign bit (integer pipe): the FP64 pipe, shared with the
+                        // other warps' DMMAs, only sees the (entries - 1) + 1 real additions
+                        auto signed_g = [&](uint32_t e) {
+                            const uint16_t en = le[e];
+                            const long long bits = __double_as_longlong(G[en & 0x7FFF]);
+                            return __longlong_as_double(bits ^ ((long long)(en & 0x8000) << 48));
+                        };
+                        double v = signed_g(beg);
+                        for (uint32_t e = beg + 1; e < end; ++e) v += signed_g(e);
+                        srow[tg >> 16] += v;
+                    }
+                }
+            };
+            if (((w >> 2) & 1) == 0) {
+                if (!(p.dbg & 2)) do_mma();
+                if (!(p.dbg & 1)) do_scatter();
+            } else {
+                if (!(p.dbg & 1)) do_scatter();
+                if (!(p.dbg & 2)) do_mma();
+            }
         }
         __syncthreads();
         // ---- write the row: y = [y] + sigma_ab + e_core * x
         const double* xr = p.x + ia * p.ld;
         double* yr = p.y + (ia - p.row_lo) * p.ld;
-        for (int64_t c = tid; c < p.ld; c += THREADS) {
+        for (int64_t c = tid; c < p.ld; c += nthr) {
             double v = 0.0;
             if (c < p.NB) {
                 v = srow[c] + p.e_core * xr[c];
@@ -310,7 +272,7 @@ void launch_ks(const AbPlan& pl, const AbParams& prm, int grid, cudaStream_t st)
         SBG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         configured[dev] = 1;
     }
-    kern<<<grid, THREADS, pl.smem, st>>>(prm);
+    kern<<<grid, pl.threads, pl.smem, st>>>(prm);
     SBG_LAUNCH_CHECK();
 }
 
@@ -335,43 +297,39 @@ AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int
         if (rem == 0) {
             pl.mb16 = full;
             pl.extra = 0;
-        } else if (rem <= 8 && full >= 2 * nbt) {
-            pl.mb16 = full;  // the last 8 rows: m8n8k4 on warps 0..2*nbt-1 (n8 block x k half)
+        } else if (rem <= 8 && full >= nbt) {
+            pl.mb16 = full;  // the last 8 rows ride on m8n8k4 in warps 0..nbt-1
             pl.extra = 1;
         } else {
             pl.mb16 = full + 1;
             pl.extra = 0;
         }
         pl.npad = pl.extra ? 16 * pl.mb16 + 8 : 16 * pl.mb16;
-        pl.threads = THREADS;
+        pl.threads = 32 * pl.mb16;
         pl.nt = nt;
-        const int grows = pl.npad + (pl.extra ? 8 : 0);  // + the second k half of the extra rows
-        // scatter-list buffers: bounded by the tile's valid (rs, column) entries (+ extra-row halves)
+        // scatter-list buffers: bounded by the tile's valid (rs, column) entries
         pl.maxT = 4 * ((nt * (1 + nb_el * (norb - nb_el)) + 3) / 4);
-        pl.maxE = 8 * ((nt * (nb_el + nb_el * (norb - nb_el) + (pl.extra ? 8 : 0)) + 7) / 8);
+        pl.maxE = 8 * ((nt * (nb_el + nb_el * (norb - nb_el)) + 7) / 8);
         const int64_t ntiles = ld / nt;
-        pl.smem = (size_t)ld * 8 + (size_t)SD * KP * (nt + 4) * 8 + (size_t)KP * 8 * 8 +
-                  (size_t)SG * grows * (nt + 1) * 8 + (size_t)SD * (pl.maxT * 4 + pl.maxE * 2) +
+        pl.smem = (size_t)ld * 8 + (size_t)STAGES * KP * (nt + 4) * 8 + (size_t)KP * 8 * 8 +
+                  (size_t)STAGES * pl.npad * (nt + 1) * 8 + (size_t)STAGES * (pl.maxT * 4 + pl.maxE * 2) +
                   (size_t)(ntiles + 1) * 8 + (size_t)KP * 16 + 16;
     };
     configure(32);
     if (pl.smem > 227 * 1024) configure(16);
     if (NB > 32767) throw InvalidArgument("sigma_ab: more than 32767 beta strings is not supported by this build");
-    if ((size_t)(pl.npad + 8) * (pl.nt + 1) >= 32768) throw InvalidArgument("sigma_ab: pair space too large for this build");
+    if ((size_t)pl.npad * (pl.nt + 1) >= 32768) throw InvalidArgument("sigma_ab: pair space too large for this build");
     if (pl.smem > 227 * 1024) throw InvalidArgument("sigma_ab: beta row does not fit in shared memory");
-    if (pl.KS > 24 || pl.mb16 > MMA_WARPS) throw InvalidArgument("sigma_ab: orbital space too large for this build");
+    if (pl.KS > 24 || pl.threads > 256) throw InvalidArgument("sigma_ab: orbital space too large for this build");
     return pl;
 }
 
 // Per-tile target-sorted scatter lists from the (rs, Jb) -> (Ib, sign) codes ([ld][npad] u16,
-// 0xFFFF = none). Sort key: target, then (rs, column) — a fixed summation order per target. The
-// extra m8 rows are produced as two k halves (rows rs and rs+8 of the staged tile): both enter
-// the segment of the target.
+// 0xFFFF = none). Sort key: target, then (rs, column) — a fixed summation order per target.
 void build_ab_scatter(const AbPlan& pl, const std::vector<uint16_t>& codes, std::vector<uint32_t>& tgt,
                       std::vector<uint16_t>& ent, std::vector<uint32_t>& tile_tgt, std::vector<uint32_t>& tile_ent) {
     const int NT = pl.nt, GSTRIDE = pl.nt + 1;
     const int64_t ntiles = pl.ld / NT;
-    const int re = 16 * pl.mb16;
     tgt.clear();
     ent.clear();
     tile_tgt.assign(ntiles + 1, 0);
@@ -384,8 +342,6 @@ void build_ab_scatter(const AbPlan& pl, const std::vector<uint16_t>& codes, std:
                 const uint16_t code = codes[(size_t)(jt * NT + c) * pl.npad + rs];
                 if (code == 0xFFFF) continue;
                 items.push_back({(uint32_t)(code & 0x7FFF), (uint16_t)((rs * GSTRIDE + c) | (code & 0x8000))});
-                if (pl.extra && rs >= re)
-                    items.push_back({(uint32_t)(code & 0x7FFF), (uint16_t)(((rs + 8) * GSTRIDE + c) | (code & 0x8000))});
             }
         std::stable_sort(items.begin(), items.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
         while (tgt.size() % 4) tgt.push_back(0);  // 16-byte aligned tile segments (cp.async)
@@ -399,8 +355,6 @@ void build_ab_scatter(const AbPlan& pl, const std::vector<uint16_t>& codes, std:
                 tgt.push_back((items[i].first << 16) | (uint32_t)(i + 1));
             }
         }
-        if ((int64_t)(tgt.size() - tile_tgt[jt]) > pl.maxT || (int64_t)(ent.size() - tile_ent[jt]) > pl.maxE)
-            throw InvalidArgument("sigma_ab: tile scatter list exceeds its buffer");
     }
     while (tgt.size() % 4) tgt.push_back(0);
     while (ent.size() % 8) ent.push_back(0);
@@ -427,7 +381,7 @@ void launch_sigma_ab(const AbPlan& pl, const AbScatter& sc, const double* x_full
     prm.extra = pl.extra;
     prm.K = pl.K;
     prm.KP = pl.KS * 4;
-    prm.grows = pl.npad + (pl.extra ? 8 : 0);
+    prm.grows = pl.npad;
     prm.maxT = pl.maxT;
     prm.maxE = pl.maxE;
     prm.NB = pl.NB;
