@@ -20,9 +20,10 @@ namespace sbg {
 
 namespace {
 
-constexpr int NTS = 64;         // batch columns per tile
+constexpr int NTS = 32;         // batch columns per tile (one warp-wide reduction segment)
 constexpr int XSTRIDE = NTS + 4;
-constexpr int TILES_PER_CTA = 4;
+constexpr int YSTRIDE = NTS + 4;
+constexpr int TILES_PER_CTA = 8;
 
 struct SsParams {
     const double* x;
@@ -33,13 +34,13 @@ struct SsParams {
 };
 
 template <int KSS>
-__global__ void __launch_bounds__(128) k_sigma_ss(const SsParams p) {
+__global__ void __launch_bounds__(128, 4) k_sigma_ss(const SsParams p) {
     constexpr int KPP = KSS * 4;
     extern __shared__ __align__(16) double smem[];
-    double* Xs = smem;                        // [KPP][XSTRIDE]
+    double* Xs = smem;                        // [2][KPP][XSTRIDE]
     const int ysrows = max(KPP, 16 * (int)(blockDim.x >> 5));
-    double* Ys = Xs;                          // [ysrows][NTS], aliases Xs once the MMAs are done
-    int* sJ = reinterpret_cast<int*>(Xs + max(KPP * XSTRIDE, ysrows * NTS));
+    double* Ys = Xs + 2 * KPP * XSTRIDE;      // [ysrows][YSTRIDE]
+    int* sJ = reinterpret_cast<int*>(Ys + ysrows * YSTRIDE);
     int* sPi = sJ + KPP;
     double* sPhi = reinterpret_cast<double*>(sPi + KPP);
 
@@ -91,20 +92,29 @@ __global__ void __launch_bounds__(128) k_sigma_ss(const SsParams p) {
     }
     __syncthreads();
 
+    // column tiles of this CTA, X tiles double-buffered with cp.async (tile tt+1 lands while the
+    // DMMAs of tile tt run); Ys is a separate staging tile for the coalesced reductions
     const int64_t c_begin = p.col_lo + (int64_t)blockIdx.y * TILES_PER_CTA * NTS;
-    for (int tt = 0; tt < TILES_PER_CTA; ++tt) {
+    const int ntt = (int)std::min<int64_t>(TILES_PER_CTA, (p.col_hi - c_begin + NTS - 1) / NTS);
+    auto load = [&](int tt) {
         const int64_t c0 = c_begin + (int64_t)tt * NTS;
-        if (c0 >= p.col_hi) break;
+        double* dst = Xs + (tt & 1) * KPP * XSTRIDE;
         for (int c = tid; c < KPP * (NTS / 2); c += nthr) {
             const int k = c / (NTS / 2), part = c % (NTS / 2);
-            // the last tile may overhang the padded row (ld is a multiple of 32, not of NTS):
-            // those columns are never reduced, so they are simply not loaded
+            // the last tile may overhang the padded row: those columns are never reduced
             if (c0 + part * 2 < p.ldx)
-                cp_async16(Xs + k * XSTRIDE + part * 2, p.x + (int64_t)sJ[k] * p.ldx + c0 + part * 2);
+                cp_async16(dst + k * XSTRIDE + part * 2, p.x + (int64_t)sJ[k] * p.ldx + c0 + part * 2);
         }
+    };
+    if (ntt > 0) load(0);
+    cp_async_commit();
+    for (int tt = 0; tt < ntt; ++tt) {
+        const int64_t c0 = c_begin + (int64_t)tt * NTS;
+        if (tt + 1 < ntt) load(tt + 1);
         cp_async_commit();
-        cp_async_wait<0>();
-        __syncthreads();
+        cp_async_wait<1>();
+        __syncthreads();  // X(tt) visible; the reductions of tile tt-1 finished reading Ys
+        const double* X = Xs + (tt & 1) * KPP * XSTRIDE;
         double acc[NTS / 8][4];
 #pragma unroll
         for (int nb = 0; nb < NTS / 8; ++nb)
@@ -112,27 +122,25 @@ __global__ void __launch_bounds__(128) k_sigma_ss(const SsParams p) {
             for (int e = 0; e < 4; ++e) acc[nb][e] = 0.0;
 #pragma unroll
         for (int j = 0; j < KSS; ++j) {
-            const double* Xk = Xs + (4 * j + t) * XSTRIDE + g;
+            const double* Xk = X + (4 * j + t) * XSTRIDE + g;
 #pragma unroll
             for (int nb = 0; nb < NTS / 8; ++nb) dmma_16x8x4(acc[nb], a0[j], a1[j], Xk[nb * 8]);
         }
-        __syncthreads();  // Ys aliases Xs
 #pragma unroll
         for (int nb = 0; nb < NTS / 8; ++nb) {
             const int col = nb * 8 + 2 * t;
-            Ys[i0 * NTS + col] = acc[nb][0];
-            Ys[i0 * NTS + col + 1] = acc[nb][1];
-            Ys[(i0 + 8) * NTS + col] = acc[nb][2];
-            Ys[(i0 + 8) * NTS + col + 1] = acc[nb][3];
+            Ys[i0 * YSTRIDE + col] = acc[nb][0];
+            Ys[i0 * YSTRIDE + col + 1] = acc[nb][1];
+            Ys[(i0 + 8) * YSTRIDE + col] = acc[nb][2];
+            Ys[(i0 + 8) * YSTRIDE + col + 1] = acc[nb][3];
         }
         __syncthreads();
-        const int64_t ncol = std::min<int64_t>(NTS, p.col_hi - c0);
-        for (int idx = tid; idx < P * NTS; idx += nthr) {
-            const int i = idx / NTS, c = idx % NTS;
-            if (c < ncol) red_add_f64(p.y + (int64_t)sJ[i] * p.ldx + c0 + c, Ys[idx]);
-        }
-        __syncthreads();
+        // one warp reduces one 32-column row segment per step: coalesced 256-byte reductions
+        if (c0 + lane < p.col_hi)
+            for (int i = w; i < P; i += nthr >> 5)
+                red_add_f64(p.y + (int64_t)sJ[i] * p.ldx + c0 + lane, Ys[i * YSTRIDE + lane]);
     }
+    cp_async_wait<0>();
 }
 
 template <int KSS>
@@ -212,7 +220,7 @@ SsPlan plan_sigma_ss(int norb, int nel) {
     pl.warps = (pl.P + 15) / 16;
     const int KPP = pl.KSS * 4;
     const int rows = std::max(KPP, 16 * pl.warps);
-    pl.smem = (size_t)std::max(KPP * XSTRIDE, rows * NTS) * 8 + (size_t)KPP * 8 + (size_t)KPP * 8 + 16;
+    pl.smem = (size_t)(2 * KPP * XSTRIDE + rows * YSTRIDE) * 8 + (size_t)KPP * 8 + (size_t)KPP * 8 + 16;
     if (pl.KSS > 16 || pl.warps > 4) throw InvalidArgument("sigma_ss: orbital space too large for this build");
     return pl;
 }
