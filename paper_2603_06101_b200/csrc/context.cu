@@ -93,7 +93,7 @@ Context::Context(int norb_, int nelec_, int ms2_, double e_core_, const double* 
                                  " determinants, above the guard of " + std::to_string(max_det) +
                                  " (pass a larger bound to override)");
     if (world < 1 || rank < 0 || rank >= world) throw InvalidArgument("sbg_create_dist: bad rank/world");
-    ld = round_up(NB, ab_ld_multiple());  // 512-byte rows: whole alpha-beta pair-tiles
+    ld = round_up(NB, 32);
     ldT = round_up(NA, 32);
     shard_range(NA, rank, world, &row_lo, &row_hi);
     nrows = row_hi - row_lo;
@@ -188,9 +188,7 @@ void Context::build_tables(const double* h1, const double* eri) {
         SBG_CUDA(cudaStreamSynchronize(st));  // Vp host buffer, codes
         std::vector<uint32_t> tgt, tt, te;
         std::vector<uint16_t> ent;
-        int maxT = 0, maxE = 0;
-        build_ab_scatter(ab_, codes, tgt, ent, tt, te, &maxT, &maxE);
-        finalize_sigma_ab(ab_, maxT, maxE);
+        build_ab_scatter(ab_, codes, tgt, ent, tt, te);
         d_sc_tgt_ = dmalloc<uint32_t>(tgt.size());
         d_sc_ent_ = dmalloc<uint16_t>(ent.size());
         d_sc_tt_ = dmalloc<uint32_t>(tt.size());

@@ -37,12 +37,9 @@ struct AbScatter {  // device pointers of the per-tile segment lists (build_ab_s
     const uint32_t* tile_tgt;
     const uint32_t* tile_ent;
 };
-int ab_ld_multiple();  // row length granularity the alpha-beta kernel needs (pair-tiles)
 AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int64_t ld, int nsm);
 void build_ab_scatter(const AbPlan& pl, const std::vector<uint16_t>& codes, std::vector<uint32_t>& tgt,
-                      std::vector<uint16_t>& ent, std::vector<uint32_t>& seg_tgt, std::vector<uint32_t>& seg_ent,
-                      int* maxT, int* maxE);
-void finalize_sigma_ab(AbPlan& pl, int maxT, int maxE);  // list buffer sizes -> shared memory plan
+                      std::vector<uint16_t>& ent, std::vector<uint32_t>& tile_tgt, std::vector<uint32_t>& tile_ent);
 void launch_sigma_ab(const AbPlan& pl, const AbScatter& sc, const double* x_full, double* y_local, const double* Vp,
                      int64_t row_lo, int64_t row_hi, double e_core, int accumulate, int grid, cudaStream_t st);
 
