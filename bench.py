@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-tte", action="store_true", help="skip the time-to-energy solves")
     return ap.parse_args()
 
 
@@ -143,6 +144,31 @@ def profile_traffic(cfg_name):
             return json.load(f)[cfg_name]["dram_bytes_per_launch"]   # ncu --set full, per launch
     except Exception:
         return None
+
+
+def time_to_energy():
+    """Second half of the BASELINE metric: SBCI1 solves on the GPU through the public API
+    (solve_n_states_sbci1, reference SolverConfig defaults), wall time from solver start with the
+    operator built, energies vs the reference's own converged energies (tests/golden, produced by
+    the compiled reference on the same pinned integrals)."""
+    import numpy as np
+    import paper_2603_06101_b200 as P
+    out = {}
+    for tag, (norb, ne, sc), nroots in (("c1", (10, 10, 0.05), 4), ("c2", (12, 12, 0.05), 1)):
+        with open(os.path.join(ROOT, "tests", "golden", f"golden_{tag}.json")) as f:
+            ref = json.load(f)["sbci1"]
+        op = P.FciOperator(P.synthetic_problem(norb, ne, SEED, sc), max_determinants=2 ** 62)
+        P.solve_n_states_sbci1(op, 1, want_vectors=False)          # warm-up (module load, first launches)
+        t0 = time.perf_counter()
+        res = P.solve_n_states_sbci1(op, nroots, want_vectors=False)
+        wall = time.perf_counter() - t0
+        e = np.array([p.energy for p in res.pairs])
+        out[tag] = {"nroots": nroots, "seconds": wall, "sigma_builds": res.summary.matvecs,
+                    "iterations": res.summary.total_iterations,
+                    "max_abs_dE_vs_reference_Eh": float(np.abs(e - np.array(ref["energies"])).max()),
+                    "reference_seconds_1core": ref["wall_s"], "reference_sigma_builds": ref["matvecs"]}
+        op.close()
+    return out
 
 
 def run_reference(args):
@@ -280,6 +306,8 @@ def run_ours(args):
             "sigma_tflops": flops["total"] / (ms_step * 1e-3) / 1e12,
             "clocks": clocks,
         }
+        if world == 1 and not args.no_tte:
+            out["time_to_energy"] = time_to_energy()
         if world == 1 and not args.no_cpu_baseline:
             cb = cpu_baseline(args.config)
             out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}

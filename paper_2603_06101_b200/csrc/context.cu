@@ -19,18 +19,49 @@ DBuf::DBuf(int64_t count) : n(count) {
         SBG_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
     }
 }
-DBuf::~DBuf() {
-    if (p) cudaFree(p);
+DBuf::DBuf(VecPool& vp, int64_t count, cudaStream_t zero_on) : n(count), pool(&vp) {
+    if (count > 0) {
+        p = vp.take(count);
+        SBG_CUDA(cudaMemsetAsync(p, 0, (size_t)count * sizeof(double), zero_on));
+    }
 }
+void DBuf::release() {
+    if (p) {
+        if (pool) pool->give(p);
+        else cudaFree(p);
+    }
+    p = nullptr;
+    n = 0;
+    pool = nullptr;
+}
+DBuf::~DBuf() { release(); }
 DBuf& DBuf::operator=(DBuf&& o) noexcept {
     if (this != &o) {
-        if (p) cudaFree(p);
+        release();
         p = o.p;
         n = o.n;
+        pool = o.pool;
         o.p = nullptr;
         o.n = 0;
+        o.pool = nullptr;
     }
     return *this;
+}
+
+double* VecPool::take(int64_t count) {
+    if (n == 0) n = count;
+    if (count != n) throw std::invalid_argument("VecPool: all pooled vectors have the padded local length");
+    if (!free_.empty()) {
+        double* p = free_.back();
+        free_.pop_back();
+        return p;
+    }
+    double* p = nullptr;
+    SBG_CUDA(cudaMalloc(&p, (size_t)count * sizeof(double)));
+    return p;
+}
+VecPool::~VecPool() {
+    for (double* p : free_) cudaFree(p);
 }
 
 // ------------------------------------------------------------------ NCCL plumbing
@@ -111,7 +142,7 @@ Context::Context(int norb_, int nelec_, int ms2_, double e_core_, const double* 
         SBG_NCCL(ncclCommInitRank(&comm_->comm, world, id, rank));
     }
 
-    rws.grid = 2 * nsm;
+    rws.grid = 16 * nsm;
     rws.partial = dmalloc<double>((size_t)rws.grid * kMaxDot);
     rws.result = dmalloc<double>(kMaxDot);
     SBG_CUDA(cudaMallocHost(&rws.host, kMaxDot * sizeof(double)));

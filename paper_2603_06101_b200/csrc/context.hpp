@@ -21,17 +21,38 @@
 
 namespace sbg {
 
+// Recycles the padded solver vectors of one Context (all the same length). cudaMalloc/cudaFree of
+// ~100 MB vectors cost milliseconds and cudaFree synchronises the device, so the solver's per-state
+// allocations (sbci1.hpp keeps 7 + n_deflated vectors live) come from here instead. Buffers are
+// reused in stream order: every user of a pooled buffer works on the Context stream.
+struct VecPool {
+    std::vector<double*> free_;
+    int64_t n = 0;
+    ~VecPool();
+    double* take(int64_t count);
+    void give(double* p) { free_.push_back(p); }
+};
+
 struct DBuf {
     double* p = nullptr;
     int64_t n = 0;
+    VecPool* pool = nullptr;
     DBuf() = default;
-    explicit DBuf(int64_t count);
+    explicit DBuf(int64_t count);                          // cudaMalloc + zero fill, synchronous
+    DBuf(VecPool& vp, int64_t count, cudaStream_t zero_on);  // pooled, zero fill ordered on zero_on
     ~DBuf();
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
-    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), pool(o.pool) {
+        o.p = nullptr;
+        o.n = 0;
+        o.pool = nullptr;
+    }
     DBuf& operator=(DBuf&& o) noexcept;
     bool empty() const { return p == nullptr; }
+
+private:
+    void release();
 };
 
 struct Comm;  // NCCL plumbing (dist.cu); null for a single GPU
@@ -52,6 +73,8 @@ public:
 
     int64_t padded_len() const { return nrows * ld; }
     DBuf alloc_vec() const;  // zero-initialised padded local vector
+    // pooled zero-initialised padded local vector; the zero fill is ordered on st (solver work)
+    DBuf vec() { return DBuf(*pool_, padded_len(), st); }
     // persistent staging vectors of the host-pointer entry points (sbg_sigma, sbg_sigma_device)
     double* io_x() {
         if (io_x_.empty()) io_x_ = alloc_vec();
@@ -92,6 +115,7 @@ public:
     double flops_ab = 0, flops_ss = 0;
 
 private:
+    std::unique_ptr<VecPool> pool_ = std::make_unique<VecPool>();  // declared first: destroyed last
     void build_tables(const double* h1, const double* eri);
     void ensure_links();
     void gather_full(const double* x_local, cudaStream_t s);

@@ -71,12 +71,13 @@ struct LinArgs {
     // out[j] may be null (value only used by later outputs / dots)
     double coef[kMaxOut][kMaxIn + kMaxOut];
     unsigned char da[kMaxDot], db[kMaxDot];  // dot slots
+    unsigned int dmask;                       // slots read by the dots (set by launch_lincomb)
 };
 struct ReduceWs {
     double* partial;  // [grid][kMaxDot]
     double* result;   // [kMaxDot] device
     double* host;     // pinned [kMaxDot]
-    int grid;
+    int grid;         // capacity of partial in blocks; each pass launches min(grid, resident blocks)
 };
 // returns nothing; results land in ws.result (device). Caller copies to host after collectives.
 void launch_lincomb(const LinArgs& a, const ReduceWs& ws, cudaStream_t st);
@@ -105,7 +106,7 @@ struct SubArgs {
 };
 void launch_subspace(const SubArgs& a, const ReduceWs& ws, cudaStream_t st);
 // generic deterministic dot/norm reductions finish: partials -> result
-void launch_reduce_finish(const ReduceWs& ws, int ndot, cudaStream_t st);
+void launch_reduce_finish(const ReduceWs& ws, int nblk, int ndot, cudaStream_t st);
 // argmin with index tie-break over a padded matrix (valid cols < ncols), excluding (value,index) <= prev
 void launch_argmin_after(const double* D, int64_t nrows, int64_t ncols, int64_t ld, int64_t row_lo, double prev_v,
                          int64_t prev_i, double* out_v, int64_t* out_i, double* part_v, int64_t* part_i, int grid,

@@ -6,6 +6,8 @@
 
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <optional>
@@ -15,6 +17,10 @@ namespace sbg {
 namespace {
 
 constexpr int kSbci1DefaultMaxCycle = 20;
+double g_lin_ms = 0, g_ph[8] = {0};
+long g_lin_n = 0;
+using Clk = std::chrono::steady_clock;
+inline double ms_since(Clk::time_point t) { return std::chrono::duration<double, std::milli>(Clk::now() - t).count(); }
 
 // ------------------------------------------------------------------ fused pass builder
 struct Lin {
@@ -38,6 +44,7 @@ struct Lin {
     }
     std::vector<double> run(Context& c) {
         a.n = c.padded_len();
+        const auto t0 = std::chrono::steady_clock::now();
         launch_lincomb(a, c.rws, c.st);
         c.launches += 1 + (a.ndot > 0);
         std::vector<double> r(a.ndot);
@@ -45,6 +52,8 @@ struct Lin {
             const double* h = c.finish_dots(a.ndot);
             std::copy(h, h + a.ndot, r.begin());
         }
+        g_lin_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        g_lin_n++;
         return r;
     }
 };
@@ -83,7 +92,7 @@ public:
         SBG_CUDA(cudaMemcpyAsync(dst.p, src.p, c_.padded_len() * 8, cudaMemcpyDeviceToDevice, c_.st));
     }
     DBuf clone(const DBuf& src) {
-        DBuf d(c_.padded_len());
+        DBuf d = c_.vec();
         copy(d, src);
         return d;
     }
@@ -250,7 +259,7 @@ std::optional<RestartReason> check_restart(int alpha, double b, double dE, doubl
 class Driver {
 public:
     Driver(Context& c, const SolverConfig& cfg, const std::function<void(const TraceRec&)>& trace)
-        : c_(c), o_(c), cfg_(cfg), trace_(trace), z_(c.padded_len()), hz_(c.padded_len()) {}
+        : c_(c), o_(c), cfg_(cfg), trace_(trace), z_(c.vec()), hz_(c.vec()) {}
 
     // z = (1 - sum x_c x_c^T)(D - E0)^-1 zres with the Gram-Schmidt dots (precond.hpp:106-111)
     std::vector<double> make_z(const State& st, const Precond& pre, const Deflation& defl, bool with_y) {
@@ -284,7 +293,9 @@ public:
     StepData step(State& st, const Precond& pre, Deflation& defl, int max_cycle) {
         StepData out;
         bool use_three = st.t >= 1;
+        auto tp = Clk::now();
         const auto d = make_z(st, pre, defl, use_three);
+        g_ph[0] += ms_since(tp);
         const double nxx = d[0], nxz = d[1], nzz = d[2];
         if (std::sqrt(nzz) < cfg_.lindep * std::sqrt(nxx)) {
             const double xhx = o_.dot(st.x, st.hx);
@@ -312,7 +323,10 @@ public:
                 return out;
             }
         }
+        tp = Clk::now();
         o_.apply(z_, hz_);
+        g_ph[1] += ms_since(tp);
+        tp = Clk::now();
 
         SubArgs sa{};
         sa.n = c_.padded_len();
@@ -336,7 +350,11 @@ public:
         SmallMatrix v(m);
         for (int i = 0; i < m; ++i)
             for (int j = i; j < m; ++j) v(i, j) = v(j, i) = 0.5 * (h[i * m + j] + h[j * m + i]);
+        g_ph[2] += ms_since(tp);
+        tp = Clk::now();
         const SmallEigResult eig = jacobi_symmetric_eig(v);
+        g_ph[3] += ms_since(tp);
+        tp = Clk::now();
 
         const double vx = eig.eigenvectors(0, 0), vy = use_three ? eig.eigenvectors(1, 0) : 0.0,
                      vz = eig.eigenvectors(m - 1, 0);
@@ -399,6 +417,7 @@ public:
             xx2 = r[1];
             ovl.assign(r.begin() + 2, r.end());
         }
+        g_ph[4] += ms_since(tp);
         out.committed = true;
         out.dE = std::abs(e_new - st.energy);
         out.dz = std::sqrt(zz2);
@@ -448,8 +467,8 @@ public:
     // z, Hz: x_t = x - b y, y_t = y + c z, s = sx x_t + sy y_t + sz z (same summation order)
     Seed second_ritz(const State& st, const StepData& s) {
         Seed r;
-        r.x = DBuf(c_.padded_len());
-        r.hx = DBuf(c_.padded_len());
+        r.x = c_.vec();
+        r.hx = c_.vec();
         for (int pass = 0; pass < 2; ++pass) {
             Lin L;
             const int sx = L.in(pass ? st.hx.p : st.x.p), sy = L.in(pass ? st.hy.p : st.y.p),
@@ -496,9 +515,9 @@ Sbci1Result solve_state(Driver& dr, Precond& pre, Deflation& defl, Seed seed, in
     st.alpha = alpha;
     st.x = std::move(seed.x);
     st.hx = std::move(seed.hx);
-    st.y = DBuf(c.padded_len());
-    st.hy = DBuf(c.padded_len());
-    st.zres = DBuf(c.padded_len());
+    st.y = c.vec();
+    st.hy = c.vec();
+    st.zres = c.vec();
     st.energy = o.dot(st.x, st.hx);
     o.combine(st.zres, 1.0, st.hx, -st.energy, st.x);
 
@@ -518,6 +537,7 @@ Sbci1Result solve_state(Driver& dr, Precond& pre, Deflation& defl, Seed seed, in
     while (st.total_iterations < cfg.t_max) {
         StepData step = dr.step(st, pre, defl, max_cycle);
         ++st.total_iterations;
+        auto tq = Clk::now();
         if (dr.trace_) {
             TraceRec rec;
             rec.state = alpha;
@@ -535,6 +555,8 @@ Sbci1Result solve_state(Driver& dr, Precond& pre, Deflation& defl, Seed seed, in
             rec.restart_reason = step.outcome.kind == StepOutcome::Kind::Restart ? (int)step.outcome.reason : -1;
             dr.trace_(rec);
         }
+        g_ph[5] += ms_since(tq);
+        tq = Clk::now();
         if (track) pre.update_shift(st.energy);
         switch (step.outcome.kind) {
             case StepOutcome::Kind::Converged: {
@@ -578,6 +600,7 @@ Sbci1Result solve_state(Driver& dr, Precond& pre, Deflation& defl, Seed seed, in
                 }
                 o.combine(st.zres, 1.0, st.hx, -st.energy, st.x);
                 st.t = 0;
+                g_ph[6] += ms_since(tq);
                 break;
             }
             case StepOutcome::Kind::Continue:
@@ -594,10 +617,10 @@ std::vector<Seed> init_guess(Context& c, Ops& o, int n) {
     const auto idx = o.lowest_diagonal(n);
     std::vector<DBuf> images;
     {
-        DBuf e(c.padded_len());
+        DBuf e = c.vec();
         for (int k = 0; k < n; ++k) {
             o.set_unit(e, idx[k]);
-            images.emplace_back(c.padded_len());
+            images.push_back(c.vec());
             o.apply(e, images.back());
         }
     }
@@ -614,8 +637,8 @@ std::vector<Seed> init_guess(Context& c, Ops& o, int n) {
     std::vector<Seed> seeds(m);
     for (int a = 0; a < m; ++a) {
         Seed& s = seeds[a];
-        s.x = DBuf(c.padded_len());
-        s.hx = DBuf(c.padded_len());
+        s.x = c.vec();
+        s.hx = c.vec();
         for (int i = 0; i < m; ++i) {
             const int64_t gi = idx[i];
             const int64_t row = gi / c.NB, col = gi % c.NB;
@@ -669,7 +692,12 @@ MultiStateResult solve_n_states_sbci1(Context& c, int n, const SolverConfig& cfg
     const uint64_t applies_before = c.applies().load();
     Ops o(c);
     Driver dr(c, cfg, trace);
+    g_lin_ms = 0;
+    g_lin_n = 0;
+    for (double& v : g_ph) v = 0;
+    auto tp = Clk::now();
     std::vector<Seed> guesses = init_guess(c, o, n);
+    const double t_init = ms_since(tp);
     Precond pre{&c.diagonal(), guesses.front().energy, cfg.clamp_delta};
     if (!(pre.clamp > 0.0)) throw std::invalid_argument("clamp_delta must be positive");
     Deflation defl;
@@ -680,7 +708,9 @@ MultiStateResult solve_n_states_sbci1(Context& c, int n, const SolverConfig& cfg
         if (carried) cands.push_back(&*carried);
         for (int b = alpha; b < (int)guesses.size(); ++b) cands.push_back(&guesses[b]);
         for (int b = 0; b < alpha && b < (int)guesses.size(); ++b) cands.push_back(&guesses[b]);
+        tp = Clk::now();
         Seed seed = select_seed(c, o, cands, defl, cfg.lindep);
+        g_ph[7] += ms_since(tp);
         carried.reset();
         Sbci1Result res = solve_state(dr, pre, defl, std::move(seed), alpha, alpha == 0);
         if (alpha == 0) pre.update_shift(res.pair.energy);
@@ -699,6 +729,11 @@ MultiStateResult solve_n_states_sbci1(Context& c, int n, const SolverConfig& cfg
     out.peak_vectors = 7 + (int)defl.size();
     SBG_CUDA(cudaStreamSynchronize(c.st));
     out.wall_time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (std::getenv("SBG_SOLVER_TIMING"))
+        std::fprintf(stderr,
+                     "[sbg timing] wall %.3f ms init %.3f | make_z %.3f apply %.3f subspace %.3f jacobi %.3f "
+                     "guard+commit %.3f trace %.3f restart %.3f select %.3f | lincomb calls %ld %.3f ms\n",
+                     out.wall_time_s * 1e3, t_init, g_ph[0], g_ph[1], g_ph[2], g_ph[3], g_ph[4], g_ph[5], g_ph[6], g_ph[7], g_lin_n, g_lin_ms);
     return out;
 }
 

@@ -4,6 +4,8 @@
 // updated element is bit-identical to the reference's combine/axpy/scale for the same inputs;
 // only the order of the dot-product sums differs (fixed-order tree: deterministic run to run).
 #include <cfloat>
+#include <map>
+#include <mutex>
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -33,40 +35,65 @@ __device__ __forceinline__ void block_reduce_store(double (&acc)[ND], int ndot, 
     }
 }
 
+// One fused pass: up to NI inputs, NO outputs (each a linear combination of inputs and earlier
+// outputs), ND dot products between any two slots. Two elements per thread per trip (16-byte
+// loads/stores: n is even and every vector base is 16-byte aligned). Slots read by dots are staged
+// in shared memory so the runtime slot indices never force the slot array into local memory.
+template <int NI, int NO, int ND>
 __global__ void __launch_bounds__(kThreads) k_lincomb(const LinArgs a, double* partial) {
-    double acc[kMaxDot];
+    constexpr int NDS = ND > 0 ? ND : 1;
+    __shared__ double stage[ND > 0 ? kMaxIn + kMaxOut : 1][kThreads];
+    double acc[NDS];
 #pragma unroll
-    for (int d = 0; d < kMaxDot; ++d) acc[d] = 0.0;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += stride) {
-        double s[kMaxIn + kMaxOut];
+    for (int d = 0; d < NDS; ++d) acc[d] = 0.0;
+    const int64_t n2 = a.n >> 1, stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += stride) {
+        double2 in[NI];
 #pragma unroll
-        for (int k = 0; k < kMaxIn; ++k) s[k] = (k < a.nin) ? a.in[k][i] : 0.0;
+        for (int k = 0; k < NI; ++k)
+            if (k < a.nin) in[k] = reinterpret_cast<const double2*>(a.in[k])[i];
+        double2 outv[NO];
 #pragma unroll
-        for (int j = 0; j < kMaxOut; ++j) {
-            if (j >= a.nout) break;
-            double v = 0.0;
-            bool first = true;
+        for (int h = 0; h < 2; ++h) {
+            double s[NI + NO];
 #pragma unroll
-            for (int k = 0; k < kMaxIn + kMaxOut; ++k) {
-                if (k >= kMaxIn && k - kMaxIn >= j) break;
-                const double c = a.coef[j][k];
-                if (c != 0.0) {
-                    const double term = __dmul_rn(c, s[k]);
-                    v = first ? term : __dadd_rn(v, term);
-                    first = false;
+            for (int k = 0; k < NI; ++k) s[k] = (k < a.nin) ? (h ? in[k].y : in[k].x) : 0.0;
+#pragma unroll
+            for (int j = 0; j < NO; ++j) {
+                if (j >= a.nout) break;
+                double v = 0.0;
+                bool first = true;
+#pragma unroll
+                for (int k = 0; k < NI + j; ++k) {
+                    const double c = a.coef[j][k < NI ? k : kMaxIn + (k - NI)];
+                    if (c != 0.0) {
+                        const double term = __dmul_rn(c, s[k]);
+                        v = first ? term : __dadd_rn(v, term);
+                        first = false;
+                    }
+                }
+                s[NI + j] = v;
+                if (h) outv[j].y = v;
+                else outv[j].x = v;
+            }
+            if constexpr (ND > 0) {
+#pragma unroll
+                for (int k = 0; k < NI + NO; ++k) {
+                    const int sid = k < NI ? k : kMaxIn + (k - NI);
+                    if ((a.dmask >> sid) & 1u) stage[sid][threadIdx.x] = s[k];
+                }
+#pragma unroll
+                for (int d = 0; d < ND; ++d) {
+                    if (d >= a.ndot) break;
+                    acc[d] = fma(stage[a.da[d]][threadIdx.x], stage[a.db[d]][threadIdx.x], acc[d]);
                 }
             }
-            s[kMaxIn + j] = v;
-            if (a.out[j]) a.out[j][i] = v;
         }
 #pragma unroll
-        for (int d = 0; d < kMaxDot; ++d) {
-            if (d >= a.ndot) break;
-            acc[d] = fma(s[a.da[d]], s[a.db[d]], acc[d]);
-        }
+        for (int j = 0; j < NO; ++j)
+            if (j < a.nout && a.out[j]) reinterpret_cast<double2*>(a.out[j])[i] = outv[j];
     }
-    block_reduce_store<kMaxDot>(acc, a.ndot, partial);
+    if constexpr (ND > 0) block_reduce_store<NDS>(acc, a.ndot, partial);
 }
 
 __device__ __forceinline__ double precond_den(double d, double shift, double clamp) {
@@ -75,34 +102,58 @@ __device__ __forceinline__ double precond_den(double d, double shift, double cla
     return den < 0.0 ? -clamp : clamp;
 }
 
+template <class T>
+__device__ __forceinline__ double comp(const T& v, int h) {
+    return h ? v.y : v.x;
+}
+__device__ __forceinline__ const double2* v2(const double* p) { return reinterpret_cast<const double2*>(p); }
+
 // mode 0: overlaps o_c = xc_c . (zres / den)
 // mode 1: z = zres/den - sum_c o_c xc_c ; dots xx, xz, zz [, xy, yy, yz]
 __global__ void __launch_bounds__(kThreads) k_precond(const PrecArgs a, double* partial) {
     double acc[8];
 #pragma unroll
     for (int d = 0; d < 8; ++d) acc[d] = 0.0;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += stride) {
-        double v = a.zres[i] / precond_den(a.D[i], a.shift, a.clamp);
+    const int64_t n2 = a.n >> 1, stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += stride) {
+        const double2 zr = v2(a.zres)[i], D = v2(a.D)[i];
+        double2 xc[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+            if (c < a.nxc) xc[c] = v2(a.xc[c])[i];
         if (a.mode == 0) {
 #pragma unroll
-            for (int c = 0; c < 8; ++c)
-                if (c < a.nxc) acc[c] = fma(a.xc[c][i], v, acc[c]);
-        } else {
+            for (int h = 0; h < 2; ++h) {
+                const double v = comp(zr, h) / precond_den(comp(D, h), a.shift, a.clamp);
 #pragma unroll
-            for (int c = 0; c < 8; ++c)
-                if (c < a.nxc) v = __dadd_rn(v, __dmul_rn(-a.o[c], a.xc[c][i]));
-            a.z[i] = v;
-            const double x = a.x[i];
-            acc[0] = fma(x, x, acc[0]);
-            acc[1] = fma(x, v, acc[1]);
-            acc[2] = fma(v, v, acc[2]);
-            if (a.y) {
-                const double y = a.y[i];
-                acc[3] = fma(x, y, acc[3]);
-                acc[4] = fma(y, y, acc[4]);
-                acc[5] = fma(y, v, acc[5]);
+                for (int c = 0; c < 8; ++c)
+                    if (c < a.nxc) acc[c] = fma(comp(xc[c], h), v, acc[c]);
             }
+        } else {
+            const double2 x2 = v2(a.x)[i];
+            double2 y2 = make_double2(0.0, 0.0);
+            if (a.y) y2 = v2(a.y)[i];
+            double2 z2;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                double v = comp(zr, h) / precond_den(comp(D, h), a.shift, a.clamp);
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    if (c < a.nxc) v = __dadd_rn(v, __dmul_rn(-a.o[c], comp(xc[c], h)));
+                if (h) z2.y = v;
+                else z2.x = v;
+                const double x = comp(x2, h);
+                acc[0] = fma(x, x, acc[0]);
+                acc[1] = fma(x, v, acc[1]);
+                acc[2] = fma(v, v, acc[2]);
+                if (a.y) {
+                    const double y = comp(y2, h);
+                    acc[3] = fma(x, y, acc[3]);
+                    acc[4] = fma(y, y, acc[4]);
+                    acc[5] = fma(y, v, acc[5]);
+                }
+            }
+            reinterpret_cast<double2*>(a.z)[i] = z2;
         }
     }
     const int nd = a.mode == 0 ? a.nxc : (a.y ? 6 : 3);
@@ -114,29 +165,38 @@ __global__ void __launch_bounds__(kThreads) k_subspace(const SubArgs a, double* 
     double acc[9];
 #pragma unroll
     for (int d = 0; d < 9; ++d) acc[d] = 0.0;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += stride) {
-        const double x = a.x[i], z = a.z[i], hx = a.hx[i], hz = a.hz[i];
-        double b[3], B[3];
-        b[0] = __dmul_rn(x, a.Ax);
-        B[0] = __dmul_rn(hx, a.Ax);
+    const int64_t n2 = a.n >> 1, stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += stride) {
+        const double2 x2 = v2(a.x)[i], z2 = v2(a.z)[i], hx2 = v2(a.hx)[i], hz2 = v2(a.hz)[i];
+        double2 y2 = make_double2(0.0, 0.0), hy2 = make_double2(0.0, 0.0);
         if (a.three) {
-            const double y = a.y[i], hy = a.hy[i];
-            b[1] = __dadd_rn(__dmul_rn(a.Bx, x), __dmul_rn(a.By, y));
-            B[1] = __dadd_rn(__dmul_rn(a.Bx, hx), __dmul_rn(a.By, hy));
-            b[2] = __dadd_rn(__dadd_rn(__dmul_rn(a.Cx, x), __dmul_rn(a.Cz, z)), __dmul_rn(a.Cy, y));
-            B[2] = __dadd_rn(__dadd_rn(__dmul_rn(a.Cx, hx), __dmul_rn(a.Cz, hz)), __dmul_rn(a.Cy, hy));
+            y2 = v2(a.y)[i];
+            hy2 = v2(a.hy)[i];
+        }
 #pragma unroll
-            for (int p = 0; p < 3; ++p)
+        for (int h = 0; h < 2; ++h) {
+            const double x = comp(x2, h), z = comp(z2, h), hx = comp(hx2, h), hz = comp(hz2, h);
+            double b[3], B[3];
+            b[0] = __dmul_rn(x, a.Ax);
+            B[0] = __dmul_rn(hx, a.Ax);
+            if (a.three) {
+                const double y = comp(y2, h), hy = comp(hy2, h);
+                b[1] = __dadd_rn(__dmul_rn(a.Bx, x), __dmul_rn(a.By, y));
+                B[1] = __dadd_rn(__dmul_rn(a.Bx, hx), __dmul_rn(a.By, hy));
+                b[2] = __dadd_rn(__dadd_rn(__dmul_rn(a.Cx, x), __dmul_rn(a.Cz, z)), __dmul_rn(a.Cy, y));
+                B[2] = __dadd_rn(__dadd_rn(__dmul_rn(a.Cx, hx), __dmul_rn(a.Cz, hz)), __dmul_rn(a.Cy, hy));
 #pragma unroll
-                for (int q = 0; q < 3; ++q) acc[p * 3 + q] = fma(b[p], B[q], acc[p * 3 + q]);
-        } else {
-            b[1] = __dadd_rn(__dmul_rn(a.Cx, x), __dmul_rn(a.Cz, z));
-            B[1] = __dadd_rn(__dmul_rn(a.Cx, hx), __dmul_rn(a.Cz, hz));
+                for (int p = 0; p < 3; ++p)
 #pragma unroll
-            for (int p = 0; p < 2; ++p)
+                    for (int q = 0; q < 3; ++q) acc[p * 3 + q] = fma(b[p], B[q], acc[p * 3 + q]);
+            } else {
+                b[1] = __dadd_rn(__dmul_rn(a.Cx, x), __dmul_rn(a.Cz, z));
+                B[1] = __dadd_rn(__dmul_rn(a.Cx, hx), __dmul_rn(a.Cz, hz));
 #pragma unroll
-                for (int q = 0; q < 2; ++q) acc[p * 2 + q] = fma(b[p], B[q], acc[p * 2 + q]);
+                for (int p = 0; p < 2; ++p)
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) acc[p * 2 + q] = fma(b[p], B[q], acc[p * 2 + q]);
+            }
         }
     }
     block_reduce_store<9>(acc, a.three ? 9 : 4, partial);
@@ -193,9 +253,15 @@ __global__ void k_argmin_after(const double* D, int64_t nrows, int64_t ncols, in
 __global__ void __launch_bounds__(kThreads) k_kinetic(const double* y, const double* D, double shift, int64_t n,
                                                       double* partial) {
     double acc[1] = {0.0};
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
-        acc[0] += __dmul_rn(__dmul_rn(y[i], y[i]), __dsub_rn(D[i], shift));
+    const int64_t n2 = n >> 1, stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += stride) {
+        const double2 yv = v2(y)[i], Dv = v2(D)[i];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const double yy = comp(yv, h);
+            acc[0] += __dmul_rn(__dmul_rn(yy, yy), __dsub_rn(comp(Dv, h), shift));
+        }
+    }
     block_reduce_store<1>(acc, 1, partial);
 }
 
@@ -206,29 +272,82 @@ __global__ void k_fill(double* p, int64_t n, double v) {
 
 __global__ void k_set(double* p, int64_t idx, double v) { p[idx] = v; }
 
+// resident-block grid of one kernel, capped by the partial-sum capacity
+int grid_of(const void* fn, const ReduceWs& ws) {
+    static std::mutex mu;
+    static std::map<const void*, int> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(fn);
+    if (it == cache.end()) {
+        int dev = 0, nsm = 0, nb = 0;
+        SBG_CUDA(cudaGetDevice(&dev));
+        SBG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        SBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, 0));
+        it = cache.emplace(fn, std::max(1, nb) * nsm).first;
+    }
+    return std::min(it->second, ws.grid);
+}
+
+void check_aligned(const void* p) {
+    if (reinterpret_cast<uintptr_t>(p) & 15u) throw InvalidArgument("vector pass: device vectors must be 16-byte aligned");
+}
+
+template <int NI, int NO, int ND>
+void run_lincomb(const LinArgs& a, const ReduceWs& ws, cudaStream_t st) {
+    const void* fn = reinterpret_cast<const void*>(&k_lincomb<NI, NO, ND>);
+    const int g = grid_of(fn, ws);
+    k_lincomb<NI, NO, ND><<<g, kThreads, 0, st>>>(a, ws.partial);
+    SBG_LAUNCH_CHECK();
+    if (a.ndot > 0) launch_reduce_finish(ws, g, a.ndot, st);
+}
+
+template <int NI, int NO>
+void run_lincomb_nd(const LinArgs& a, const ReduceWs& ws, cudaStream_t st) {
+    if (a.ndot == 0) run_lincomb<NI, NO, 0>(a, ws, st);
+    else if (a.ndot <= 4) run_lincomb<NI, NO, 4>(a, ws, st);
+    else run_lincomb<NI, NO, kMaxDot>(a, ws, st);
+}
+template <int NI>
+void run_lincomb_no(const LinArgs& a, const ReduceWs& ws, cudaStream_t st) {
+    if (a.nout <= 2) run_lincomb_nd<NI, 2>(a, ws, st);
+    else run_lincomb_nd<NI, kMaxOut>(a, ws, st);
+}
+
 }  // namespace
 
-void launch_lincomb(const LinArgs& a, const ReduceWs& ws, cudaStream_t st) {
-    k_lincomb<<<ws.grid, kThreads, 0, st>>>(a, ws.partial);
-    SBG_LAUNCH_CHECK();
-    if (a.ndot > 0) launch_reduce_finish(ws, a.ndot, st);
+void launch_lincomb(const LinArgs& args, const ReduceWs& ws, cudaStream_t st) {
+    if (args.nin < 0 || args.nin > kMaxIn || args.nout < 0 || args.nout > kMaxOut || args.ndot < 0 ||
+        args.ndot > kMaxDot || (args.n & 1))
+        throw InvalidArgument("launch_lincomb: bad pass shape");
+    LinArgs a = args;
+    a.dmask = 0;
+    for (int d = 0; d < a.ndot; ++d) a.dmask |= (1u << a.da[d]) | (1u << a.db[d]);
+    for (int k = 0; k < a.nin; ++k) check_aligned(a.in[k]);
+    for (int j = 0; j < a.nout; ++j) check_aligned(a.out[j]);
+    if (a.nin <= 3) run_lincomb_no<3>(a, ws, st);
+    else if (a.nin <= 6) run_lincomb_no<6>(a, ws, st);
+    else run_lincomb_no<kMaxIn>(a, ws, st);
 }
 
 void launch_precond(const PrecArgs& a, const ReduceWs& ws, cudaStream_t st) {
-    k_precond<<<ws.grid, kThreads, 0, st>>>(a, ws.partial);
+    if (a.n & 1) throw InvalidArgument("launch_precond: odd length");
+    const int g = grid_of(reinterpret_cast<const void*>(&k_precond), ws);
+    k_precond<<<g, kThreads, 0, st>>>(a, ws.partial);
     SBG_LAUNCH_CHECK();
     const int nd = a.mode == 0 ? a.nxc : (a.y ? 6 : 3);
-    if (nd > 0) launch_reduce_finish(ws, nd, st);
+    if (nd > 0) launch_reduce_finish(ws, g, nd, st);
 }
 
 void launch_subspace(const SubArgs& a, const ReduceWs& ws, cudaStream_t st) {
-    k_subspace<<<ws.grid, kThreads, 0, st>>>(a, ws.partial);
+    if (a.n & 1) throw InvalidArgument("launch_subspace: odd length");
+    const int g = grid_of(reinterpret_cast<const void*>(&k_subspace), ws);
+    k_subspace<<<g, kThreads, 0, st>>>(a, ws.partial);
     SBG_LAUNCH_CHECK();
-    launch_reduce_finish(ws, a.three ? 9 : 4, st);
+    launch_reduce_finish(ws, g, a.three ? 9 : 4, st);
 }
 
-void launch_reduce_finish(const ReduceWs& ws, int ndot, cudaStream_t st) {
-    k_reduce_finish<<<1, 32 * kMaxDot, 0, st>>>(ws.partial, ws.grid, ndot, ws.result);
+void launch_reduce_finish(const ReduceWs& ws, int nblk, int ndot, cudaStream_t st) {
+    k_reduce_finish<<<1, 32 * kMaxDot, 0, st>>>(ws.partial, nblk, ndot, ws.result);
     SBG_LAUNCH_CHECK();
 }
 
@@ -242,9 +361,11 @@ void launch_argmin_after(const double* D, int64_t nrows, int64_t ncols, int64_t 
 }
 
 void launch_kinetic(const double* y, const double* D, double shift, int64_t n, const ReduceWs& ws, cudaStream_t st) {
-    k_kinetic<<<ws.grid, kThreads, 0, st>>>(y, D, shift, n, ws.partial);
+    if (n & 1) throw InvalidArgument("launch_kinetic: odd length");
+    const int g = grid_of(reinterpret_cast<const void*>(&k_kinetic), ws);
+    k_kinetic<<<g, kThreads, 0, st>>>(y, D, shift, n, ws.partial);
     SBG_LAUNCH_CHECK();
-    launch_reduce_finish(ws, 1, st);
+    launch_reduce_finish(ws, g, 1, st);
 }
 
 void launch_fill(double* p, int64_t n, double v, cudaStream_t st) {
