@@ -77,13 +77,17 @@ typedef struct sbg_stats {
     uint64_t kernel_launches;   /* kernels launched by the library during the call */
 } sbg_stats;
 
-/* Per-iteration trace record (TraceRecord trace.hpp:22-44, sbci1 fields). */
+/* Per-iteration trace record (TraceRecord trace.hpp:22-44). Fields a method does not produce are NaN. */
 typedef struct sbg_trace_record {
     int32_t state, t;
     double energy, dE, res_norm, x_norm, kinetic;
     uint64_t matvecs;
     int32_t restart_reason; /* -1 none, else RestartReason (0 stall_small_b, 1 norm_out_of_range, 2 residual_blowup, 3 max_cycle) */
-    double b, c;
+    double b, c;            /* sbci2: the diagonal (alpha,alpha) coefficients */
+    int32_t method;         /* 1 sbci1, 2 sbci2, 3 davidson */
+    int32_t pair_partner;   /* alpha+1 for sbci2 rows, else -1 */
+    double b_ab, b_ba, b_bb, c_ab, c_ba, c_bb, a_ab, a_ba;
+    double energy_partner, x_norm_partner, res_norm_partner;
 } sbg_trace_record;
 typedef void (*sbg_trace_fn)(const sbg_trace_record* rec, void* user);
 
@@ -149,7 +153,7 @@ int sbg_profile_read(sbg_ctx* ctx, double* ms, int64_t* calls);
 int sbg_sigma_flops(const sbg_ctx* ctx, double* alpha_beta, double* same_spin, double* total);
 
 /* ---- solvers (drivers of sbci1.hpp:526-579 / sbci2.hpp:527-623 on device-resident vectors) ----
- * method: 1 = SBCI1. energies[nroots] ascending; vectors (nullable) nroots x n_det host buffer,
+ * method: 1 = SBCI1 (solve_n_states_sbci1), 2 = SBCI2 (solve_n_states_sbci2); nroots <= 9. energies[nroots] ascending; vectors (nullable) nroots x n_det host buffer,
  * unit norm. trace may be NULL. */
 int sbg_solve(sbg_ctx* ctx, int method, int nroots, const sbg_config* cfg, double* energies,
               double* vectors, sbg_stats* stats, sbg_trace_fn trace, void* trace_user);

@@ -117,6 +117,23 @@ def c2(solve):
     print("c2", sc, flush=True)
 
 
+def methods():
+    """Adds the reference's SBCI2 and Davidson records for c0/c1 to their golden JSON files."""
+    F = Reference()
+    R = Restatement()
+    for idx in (0, 1):
+        c = CONFIGS[idx]
+        P = baseline_problem(idx, R)
+        path = os.path.join(GOLD, f"golden_{c['name']}.json")
+        with open(path) as f:
+            sc = json.load(f)
+        sc["sbci2"] = solve_record(F, P, c["nroots"], 2)
+        sc["davidson"] = solve_record(F, P, c["nroots"], 3)
+        with open(path, "w") as f:
+            json.dump(sc, f, indent=1, sort_keys=True)
+        print(c["name"], sc["sbci2"], sc["davidson"], flush=True)
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "fast"
     if what == "fast":
@@ -125,3 +142,5 @@ if __name__ == "__main__":
         c2(False)
     elif what == "c2solve":
         c2(True)
+    elif what == "methods":
+        methods()

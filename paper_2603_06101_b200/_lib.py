@@ -36,7 +36,11 @@ class Stats(C.Structure):
 class TraceRecordC(C.Structure):
     _fields_ = [("state", C.c_int32), ("t", C.c_int32), ("energy", C.c_double), ("dE", C.c_double),
                 ("res_norm", C.c_double), ("x_norm", C.c_double), ("kinetic", C.c_double),
-                ("matvecs", C.c_uint64), ("restart_reason", C.c_int32), ("b", C.c_double), ("c", C.c_double)]
+                ("matvecs", C.c_uint64), ("restart_reason", C.c_int32), ("b", C.c_double), ("c", C.c_double),
+                ("method", C.c_int32), ("pair_partner", C.c_int32),
+                ("b_ab", C.c_double), ("b_ba", C.c_double), ("b_bb", C.c_double), ("c_ab", C.c_double),
+                ("c_ba", C.c_double), ("c_bb", C.c_double), ("a_ab", C.c_double), ("a_ba", C.c_double),
+                ("energy_partner", C.c_double), ("x_norm_partner", C.c_double), ("res_norm_partner", C.c_double)]
 
 
 TRACE_FN = C.CFUNCTYPE(None, C.POINTER(TraceRecordC), C.c_void_p)

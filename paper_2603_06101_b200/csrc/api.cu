@@ -335,8 +335,9 @@ int sbg_solve(sbg_ctx* ctx, int method, int nroots, const sbg_config* cfg, doubl
               sbg_stats* stats, sbg_trace_fn trace, void* trace_user) {
     return guarded([&] {
         require_ctx(ctx);
-        if (method != 1) throw std::invalid_argument("sbg_solve: method must be 1 (sbci1)");
-        if (nroots < 1 || nroots > SBG_MAX_ROOTS) throw std::invalid_argument("sbg_solve: nroots out of range");
+        if (method != 1 && method != 2) throw std::invalid_argument("sbg_solve: method must be 1 (sbci1) or 2 (sbci2)");
+        if (nroots < 1 || nroots > sbg::detail_max_roots)
+            throw std::invalid_argument("sbg_solve: nroots must be in 1..9 (at most 8 deflated states)");
         auto& c = *ctx->c;
         std::function<void(const sbg::TraceRec&)> tf;
         if (trace)
@@ -353,11 +354,25 @@ int sbg_solve(sbg_ctx* ctx, int method, int nroots, const sbg_config* cfg, doubl
                 rec.restart_reason = r.restart_reason;
                 rec.b = r.b;
                 rec.c = r.c;
+                rec.method = r.method;
+                rec.pair_partner = r.pair_partner;
+                rec.b_ab = r.b_ab;
+                rec.b_ba = r.b_ba;
+                rec.b_bb = r.b_bb;
+                rec.c_ab = r.c_ab;
+                rec.c_ba = r.c_ba;
+                rec.c_bb = r.c_bb;
+                rec.a_ab = r.a_ab;
+                rec.a_ba = r.a_ba;
+                rec.energy_partner = r.energy_partner;
+                rec.x_norm_partner = r.x_norm_partner;
+                rec.res_norm_partner = r.res_norm_partner;
                 trace(&rec, trace_user);
             };
         const uint64_t launches0 = c.launches;
         try {
-            sbg::MultiStateResult r = sbg::solve_n_states_sbci1(c, nroots, to_cfg(cfg), tf);
+            sbg::MultiStateResult r = method == 1 ? sbg::solve_n_states_sbci1(c, nroots, to_cfg(cfg), tf)
+                                                  : sbg::solve_n_states_sbci2(c, nroots, to_cfg(cfg), tf);
             for (int k = 0; k < nroots; ++k) {
                 energies[k] = r.pairs[k].energy;
                 if (vectors) c.download_local(r.pairs[k].vector.p, vectors + (size_t)k * c.ndet + c.row_lo * c.NB, c.st);

@@ -143,9 +143,9 @@ Context::Context(int norb_, int nelec_, int ms2_, double e_core_, const double* 
     }
 
     rws.grid = 16 * nsm;
-    rws.partial = dmalloc<double>((size_t)rws.grid * kMaxDot);
-    rws.result = dmalloc<double>(kMaxDot);
-    SBG_CUDA(cudaMallocHost(&rws.host, kMaxDot * sizeof(double)));
+    rws.partial = dmalloc<double>((size_t)rws.grid * kMaxRed);
+    rws.result = dmalloc<double>(kMaxRed);
+    SBG_CUDA(cudaMallocHost(&rws.host, kMaxRed * sizeof(double)));
 
     build_tables(h1, eri);
 }

@@ -174,4 +174,34 @@ inline GramSchmidtCoeffs gram_schmidt_from_dots(double nxx, double nxy, double n
     return g;
 }
 
+// Canonical orthogonalization P = U s^{-1/2} from a precomputed overlap matrix (ortho.hpp:155-184):
+// Jacobi on s, keep modes with eigenvalue >= cutoff in descending order, coeff(i, c) = U(i, m)/sqrt(l_m).
+// Throws std::runtime_error when every mode is discarded, as the reference does.
+struct OrthoTransform {
+    int n_inputs = 0, rank = 0;
+    std::vector<double> p;  // [n_inputs][rank]
+    double coeff(int i, int c) const { return p[(size_t)i * rank + c]; }
+    double& coeff(int i, int c) { return p[(size_t)i * rank + c]; }
+};
+
+inline OrthoTransform canonical_orthogonalize_overlap(const SmallMatrix& s, double cutoff = 1e-14) {
+    const int k = s.n;
+    if (k < 1) throw std::invalid_argument("canonical_orthogonalize: need at least one vector");
+    const SmallEigResult eig = jacobi_symmetric_eig(s);
+    OrthoTransform t;
+    t.n_inputs = k;
+    std::vector<int> kept;
+    for (int m = k - 1; m >= 0; --m)
+        if (eig.eigenvalues[m] >= cutoff) kept.push_back(m);
+    if (kept.empty()) throw std::runtime_error("canonical_orthogonalize: all overlap modes below cutoff");
+    t.rank = (int)kept.size();
+    t.p.assign((size_t)k * t.rank, 0.0);
+    for (int c = 0; c < t.rank; ++c) {
+        const int m = kept[c];
+        const double inv_sqrt = 1.0 / std::sqrt(eig.eigenvalues[m]);
+        for (int i = 0; i < k; ++i) t.coeff(i, c) = eig.eigenvectors(i, m) * inv_sqrt;
+    }
+    return t;
+}
+
 }  // namespace sbg

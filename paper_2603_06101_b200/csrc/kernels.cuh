@@ -61,22 +61,23 @@ void launch_onebody(const double* x, double* y, const Excitation* la, int La, co
                     cudaStream_t st);
 
 // ---- vec.cu: fused HBM passes of the SBCI update (K7-K9) ----
-constexpr int kMaxIn = 10, kMaxOut = 5, kMaxDot = 16;
+constexpr int kMaxIn = 10, kMaxOut = 6, kMaxDot = 16;
+constexpr int kMaxRed = 64;  // dot products per reduction workspace (pair subspace: 36 cross dots)
 struct LinArgs {
     int64_t n;  // doubles per vector (padded local length, even)
     int nin, nout, ndot;
     const double* in[kMaxIn];
     double* out[kMaxOut];
-    // out[j] = sum_s coef[j][s] * slot[s], slots 0..9 = inputs, 10..14 = outputs already computed (j' < j);
+    // out[j] = sum_s coef[j][s] * slot[s], slots 0..9 = inputs, 10..15 = outputs already computed (j' < j);
     // out[j] may be null (value only used by later outputs / dots)
     double coef[kMaxOut][kMaxIn + kMaxOut];
     unsigned char da[kMaxDot], db[kMaxDot];  // dot slots
     unsigned int dmask;                       // slots read by the dots (set by launch_lincomb)
 };
 struct ReduceWs {
-    double* partial;  // [grid][kMaxDot]
-    double* result;   // [kMaxDot] device
-    double* host;     // pinned [kMaxDot]
+    double* partial;  // [grid][kMaxRed]
+    double* result;   // [kMaxRed] device
+    double* host;     // pinned [kMaxRed]
     int grid;         // capacity of partial in blocks; each pass launches min(grid, resident blocks)
 };
 // returns nothing; results land in ws.result (device). Caller copies to host after collectives.
@@ -107,6 +108,20 @@ struct SubArgs {
 void launch_subspace(const SubArgs& a, const ReduceWs& ws, cudaStream_t st);
 // generic deterministic dot/norm reductions finish: partials -> result
 void launch_reduce_finish(const ReduceWs& ws, int nblk, int ndot, cudaStream_t st);
+// Gram matrix of up to 6 vectors: dots v_i . v_j for i <= j, row-major upper triangle
+void launch_gram(const double* const* v, int m, int64_t n, const ReduceWs& ws, cudaStream_t st);
+// SBCI2 subspace matrix over the materialized orthonormal basis (sbci2.hpp:144-176): w_i = v_i/|v_i|
+// (inv_n[i] = 0 drops v_i), b_c = sum_i P[i][c] w_i, B_c likewise from the images; returns the r x r
+// cross dots b_c . B_d (row-major)
+struct PairSubArgs {
+    int64_t n;
+    int m, r;
+    const double* v[6];
+    const double* h[6];
+    double inv_n[6];
+    double P[6][6];
+};
+void launch_pair_subspace(const PairSubArgs& a, const ReduceWs& ws, cudaStream_t st);
 // argmin with index tie-break over a padded matrix (valid cols < ncols), excluding (value,index) <= prev
 void launch_argmin_after(const double* D, int64_t nrows, int64_t ncols, int64_t ld, int64_t row_lo, double prev_v,
                          int64_t prev_i, double* out_v, int64_t* out_i, double* part_v, int64_t* part_i, int grid,

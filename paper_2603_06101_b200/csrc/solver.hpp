@@ -5,6 +5,7 @@
 #pragma once
 
 #include <functional>
+#include <limits>
 #include <optional>
 #include <vector>
 
@@ -13,12 +14,19 @@
 
 namespace sbg {
 
+// TraceRecord (trace.hpp:22-44); fields a method does not produce stay NaN
 struct TraceRec {
+    static constexpr double absent = std::numeric_limits<double>::quiet_NaN();
+    int method = 1;         // 1 sbci1, 2 sbci2, 3 davidson
     int state = 0, t = 0;
-    double energy = 0, dE = 0, res_norm = 0, x_norm = 0, kinetic = 0;
+    int pair_partner = -1;  // alpha+1 for sbci2 rows
+    double energy = absent, dE = absent, res_norm = absent, x_norm = absent, kinetic = absent;
     uint64_t matvecs = 0;
     int restart_reason = -1;
-    double b = 0, c = 0;
+    double b = absent, c = absent;
+    double b_ab = absent, b_ba = absent, b_bb = absent, c_ab = absent, c_ba = absent, c_bb = absent;
+    double a_ab = absent, a_ba = absent;
+    double energy_partner = absent, x_norm_partner = absent, res_norm_partner = absent;
 };
 
 struct StateResult {
@@ -37,7 +45,12 @@ struct MultiStateResult {
     double wall_time_s = 0.0;
 };
 
+constexpr int detail_max_roots = 9;  // deflation sets of up to 8 states (precondition pass)
+
 MultiStateResult solve_n_states_sbci1(Context& ctx, int n, const SolverConfig& cfg,
+                                      const std::function<void(const TraceRec&)>& trace);
+// solve_n_states_sbci2 (sbci2.hpp:527-623): pair-sequential lowest-n driver
+MultiStateResult solve_n_states_sbci2(Context& ctx, int n, const SolverConfig& cfg,
                                       const std::function<void(const TraceRec&)>& trace);
 
 }  // namespace sbg

@@ -17,7 +17,8 @@ constexpr int kThreads = 256;
 
 template <int ND>
 __device__ __forceinline__ void block_reduce_store(double (&acc)[ND], int ndot, double* partial) {
-    __shared__ double red[kThreads / 32][kMaxDot];
+    static_assert(ND <= kMaxRed, "reduction width");
+    __shared__ double red[kThreads / 32][ND];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
     for (int d = 0; d < ND; ++d) {
@@ -31,7 +32,7 @@ __device__ __forceinline__ void block_reduce_store(double (&acc)[ND], int ndot, 
     if (threadIdx.x < ndot) {
         double s = 0.0;
         for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i][threadIdx.x];
-        partial[blockIdx.x * kMaxDot + threadIdx.x] = s;
+        partial[blockIdx.x * kMaxRed + threadIdx.x] = s;
     }
 }
 
@@ -203,13 +204,101 @@ __global__ void __launch_bounds__(kThreads) k_subspace(const SubArgs a, double* 
 }
 
 __global__ void k_reduce_finish(const double* partial, int nblk, int ndot, double* result) {
-    const int d = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (d >= ndot) return;
-    double s = 0.0;
-    for (int b = lane; b < nblk; b += 32) s += partial[b * kMaxDot + d];
+    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int d = threadIdx.x >> 5; d < ndot; d += nw) {
+        double s = 0.0;
+        for (int b = lane; b < nblk; b += 32) s += partial[b * kMaxRed + d];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) result[d] = s;
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) result[d] = s;
+    }
+}
+
+// all dots v_i . v_j (i <= j) of up to 6 vectors in one pass
+__global__ void __launch_bounds__(kThreads) k_gram(const PairSubArgs a, double* partial) {
+    double acc[21];
+#pragma unroll
+    for (int d = 0; d < 21; ++d) acc[d] = 0.0;
+    const int64_t n2 = a.n >> 1, stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += stride) {
+        double2 v[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k)
+            if (k < a.m) v[k] = reinterpret_cast<const double2*>(a.v[k])[i];
+        int d = 0;
+#pragma unroll
+        for (int p = 0; p < 6; ++p)
+#pragma unroll
+            for (int q = p; q < 6; ++q, ++d)
+                if (q < a.m) acc[d] = fma(v[p].y, v[q].y, fma(v[p].x, v[q].x, acc[d]));
+    }
+    // compact the m(m+1)/2 used accumulators to the front (row-major upper triangle of size m)
+    double out[21];
+    int d = 0, o = 0;
+#pragma unroll
+    for (int p = 0; p < 6; ++p)
+#pragma unroll
+        for (int q = p; q < 6; ++q, ++d)
+            if (q < a.m) out[o++] = acc[d];
+#pragma unroll
+    for (int k = 0; k < 21; ++k)
+        if (k >= o) out[k] = 0.0;
+    block_reduce_store<21>(out, a.m * (a.m + 1) / 2, partial);
+}
+
+// sbci2.hpp:144-176 per element: w_i = v_i * inv_n_i (scaled copy), basis b_c = sum_i P[i][c] w_i
+// accumulated in input order from zero (apply_transform, ortho.hpp:220-230), images likewise;
+// cross dots b_c . B_d for c, d < r
+__global__ void __launch_bounds__(kThreads) k_pair_subspace(const PairSubArgs a, double* partial) {
+    double acc[36];
+#pragma unroll
+    for (int d = 0; d < 36; ++d) acc[d] = 0.0;
+    const int64_t n2 = a.n >> 1, stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += stride) {
+        double2 v[6], h[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k)
+            if (k < a.m) {
+                v[k] = reinterpret_cast<const double2*>(a.v[k])[i];
+                h[k] = reinterpret_cast<const double2*>(a.h[k])[i];
+            }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            double w[6], wh[6];
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+                w[k] = k < a.m ? __dmul_rn(e ? v[k].y : v[k].x, a.inv_n[k]) : 0.0;
+                wh[k] = k < a.m ? __dmul_rn(e ? h[k].y : h[k].x, a.inv_n[k]) : 0.0;
+            }
+            double b[6], B[6];
+#pragma unroll
+            for (int c = 0; c < 6; ++c) {
+                double s = 0.0, S = 0.0;
+#pragma unroll
+                for (int k = 0; k < 6; ++k)
+                    if (k < a.m) {
+                        s = __dadd_rn(s, __dmul_rn(a.P[k][c], w[k]));
+                        S = __dadd_rn(S, __dmul_rn(a.P[k][c], wh[k]));
+                    }
+                b[c] = s;
+                B[c] = S;
+            }
+#pragma unroll
+            for (int c = 0; c < 6; ++c)
+#pragma unroll
+                for (int d2 = 0; d2 < 6; ++d2)
+                    if (c < a.r && d2 < a.r) acc[c * 6 + d2] = fma(b[c], B[d2], acc[c * 6 + d2]);
+        }
+    }
+    double out[36];
+#pragma unroll
+    for (int k = 0; k < 36; ++k) out[k] = 0.0;
+#pragma unroll
+    for (int c = 0; c < 6; ++c)
+#pragma unroll
+        for (int d2 = 0; d2 < 6; ++d2)
+            if (c < a.r && d2 < a.r) out[c * a.r + d2] = acc[c * 6 + d2];
+    block_reduce_store<36>(out, a.r * a.r, partial);
 }
 
 __device__ __forceinline__ bool lex_less(double v1, int64_t i1, double v2, int64_t i2) {
@@ -347,8 +436,36 @@ void launch_subspace(const SubArgs& a, const ReduceWs& ws, cudaStream_t st) {
 }
 
 void launch_reduce_finish(const ReduceWs& ws, int nblk, int ndot, cudaStream_t st) {
-    k_reduce_finish<<<1, 32 * kMaxDot, 0, st>>>(ws.partial, nblk, ndot, ws.result);
+    if (ndot < 1 || ndot > kMaxRed) throw InvalidArgument("reduce: bad dot count");
+    k_reduce_finish<<<1, 32 * std::min(ndot, 32), 0, st>>>(ws.partial, nblk, ndot, ws.result);
     SBG_LAUNCH_CHECK();
+}
+
+void launch_gram(const double* const* v, int m, int64_t n, const ReduceWs& ws, cudaStream_t st) {
+    if (m < 1 || m > 6 || (n & 1)) throw InvalidArgument("launch_gram: 1..6 vectors of even length");
+    PairSubArgs a{};
+    a.n = n;
+    a.m = m;
+    for (int k = 0; k < m; ++k) {
+        check_aligned(v[k]);
+        a.v[k] = v[k];
+    }
+    const int g = grid_of(reinterpret_cast<const void*>(&k_gram), ws);
+    k_gram<<<g, kThreads, 0, st>>>(a, ws.partial);
+    SBG_LAUNCH_CHECK();
+    launch_reduce_finish(ws, g, m * (m + 1) / 2, st);
+}
+
+void launch_pair_subspace(const PairSubArgs& a, const ReduceWs& ws, cudaStream_t st) {
+    if (a.m < 1 || a.m > 6 || a.r < 1 || a.r > a.m || (a.n & 1)) throw InvalidArgument("launch_pair_subspace: bad shape");
+    for (int k = 0; k < a.m; ++k) {
+        check_aligned(a.v[k]);
+        check_aligned(a.h[k]);
+    }
+    const int g = grid_of(reinterpret_cast<const void*>(&k_pair_subspace), ws);
+    k_pair_subspace<<<g, kThreads, 0, st>>>(a, ws.partial);
+    SBG_LAUNCH_CHECK();
+    launch_reduce_finish(ws, g, a.r * a.r, st);
 }
 
 void launch_argmin_after(const double* D, int64_t nrows, int64_t ncols, int64_t ld, int64_t row_lo, double prev_v,

@@ -96,6 +96,7 @@ class RunSummary:
 
 @dataclass
 class TraceRecord:
+    """TraceRecord (trace.hpp:22-44); fields a method does not produce are NaN."""
     method: str
     state: int
     t: int
@@ -108,6 +109,21 @@ class TraceRecord:
     restart_reason: str
     b: float
     c: float
+    pair_partner: int = -1
+    b_ab: float = float("nan")
+    b_ba: float = float("nan")
+    b_bb: float = float("nan")
+    c_ab: float = float("nan")
+    c_ba: float = float("nan")
+    c_bb: float = float("nan")
+    a_ab: float = float("nan")
+    a_ba: float = float("nan")
+    energy_partner: float = float("nan")
+    x_norm_partner: float = float("nan")
+    res_norm_partner: float = float("nan")
+
+
+METHODS = {1: "sbci1", 2: "sbci2", 3: "davidson"}
 
 
 @dataclass
@@ -116,13 +132,12 @@ class MultiStateResult:
     summary: RunSummary
 
 
-def solve_n_states_sbci1(op, n: int, cfg: SolverConfig | None = None, sink=None, want_vectors: bool = True):
-    """Sequential lowest-n SBCI1 driver (sbci1.hpp:526-579) on the GPU operator.
-    `sink` is a callable receiving TraceRecord per iteration (TraceSink::record)."""
+def _solve(op, method: int, n: int, cfg: SolverConfig | None, sink, want_vectors: bool):
     cfg = cfg or SolverConfig()
     cfg.validate()
+    name = METHODS[method]
     if n < 1:
-        raise ValueError("solve_n_states_sbci1: n must be >= 1")
+        raise ValueError(f"solve_n_states_{name}: n must be >= 1")
     dim = op.dim()
     e = np.zeros(n)
     vec = np.zeros((n, dim)) if want_vectors else None
@@ -132,10 +147,13 @@ def solve_n_states_sbci1(op, n: int, cfg: SolverConfig | None = None, sink=None,
     if sink is not None:
         def _cb(rec_p, _user):
             r = rec_p.contents
-            sink(TraceRecord("sbci1", r.state, r.t, r.energy, r.dE, r.res_norm, r.x_norm, r.kinetic, r.matvecs,
-                             RESTART_REASONS[r.restart_reason] if r.restart_reason >= 0 else "", r.b, r.c))
+            sink(TraceRecord(METHODS.get(r.method, name), r.state, r.t, r.energy, r.dE, r.res_norm, r.x_norm,
+                             r.kinetic, r.matvecs,
+                             RESTART_REASONS[r.restart_reason] if r.restart_reason >= 0 else "", r.b, r.c,
+                             r.pair_partner, r.b_ab, r.b_ba, r.b_bb, r.c_ab, r.c_ba, r.c_bb, r.a_ab, r.a_ba,
+                             r.energy_partner, r.x_norm_partner, r.res_norm_partner))
         cb = TRACE_FN(_cb)
-    rc = lib().sbg_solve(op.handle, 1, n, C.byref(cc), e.ctypes.data_as(C.POINTER(C.c_double)),
+    rc = lib().sbg_solve(op.handle, method, n, C.byref(cc), e.ctypes.data_as(C.POINTER(C.c_double)),
                          vec.ctypes.data_as(C.POINTER(C.c_double)) if vec is not None else None, C.byref(st), cb, None)
     if rc == 2:
         raise NonConvergenceError(lib().sbg_last_error().decode(), st.failed_state, st.best_energy, st.best_residual)
@@ -145,6 +163,20 @@ def solve_n_states_sbci1(op, n: int, cfg: SolverConfig | None = None, sink=None,
         pairs.append(ConvergedEigenpair(k, float(e[k]), vec[k] if vec is not None else None, st.iterations[k],
                                         st.restarts[k], st.final_residual[k]))
         states.append(StateSummary(k, float(e[k]), st.iterations[k], st.restarts[k], st.final_residual[k]))
-    summ = RunSummary("sbci1", states, st.total_iterations, st.total_restarts, st.matvecs, st.hx_refreshes,
+    summ = RunSummary(name, states, st.total_iterations, st.total_restarts, st.matvecs, st.hx_refreshes,
                       st.peak_vectors, st.wall_time_s, st.kernel_launches)
     return MultiStateResult(pairs, summ)
+
+
+def solve_n_states_sbci1(op, n: int, cfg: SolverConfig | None = None, sink=None, want_vectors: bool = True):
+    """Sequential lowest-n SBCI1 driver (sbci1.hpp:526-579) on the GPU operator.
+    `sink` is a callable receiving TraceRecord per iteration (TraceSink::record)."""
+    return _solve(op, 1, n, cfg, sink, want_vectors)
+
+
+def solve_n_states_sbci2(op, n: int, cfg: SolverConfig | None = None, sink=None, want_vectors: bool = True):
+    """Pair-sequential lowest-n SBCI2 driver (sbci2.hpp:527-623) on the GPU operator: pairs
+    (0,1), (1,2), ... with the upper iterate seeding the next pair; the last state runs SBCI1.
+    n = 1 routes to SBCI1 (the summary still says "sbci2", as the reference's does)."""
+    r = _solve(op, 2, n, cfg, sink, want_vectors)
+    return r

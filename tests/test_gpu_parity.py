@@ -196,6 +196,56 @@ def test_sbci1_baseline_configs_match_reference(dev, rest, gold_dir, idx):
     op.close()
 
 
+@pytest.mark.parametrize("name", ["h4_2e", "h6_4e"])
+def test_sbci2_fixtures_match_reference(dev, gold_dir, name):
+    """Device SBCI2 pair driver (sbci2.hpp:527-623) vs the reference's own SBCI2 run on the same
+    fixture: energies, the per-state iteration counts, and the matvec budget."""
+    p, _ = fixture(gold_dir, name)
+    g = gold(gold_dir, name)["sbci2"]
+    op = P.as_operator(p, p.ms2)
+    records = []
+    res = P.solve_n_states_sbci2(op, 3, sink=records.append)
+    assert res.summary.method == "sbci2"
+    e = np.array([pp.energy for pp in res.pairs])
+    assert np.abs(e - np.array(g["energies"])).max() <= E_TOL
+    assert np.abs(e - np.array(gold(gold_dir, name)["dense_eigs"][:3])).max() <= 1e-10
+    assert [pp.iterations for pp in res.pairs] == g["iterations"]
+    assert [pp.restarts for pp in res.pairs] == g["restarts"]
+    assert res.summary.matvecs == g["matvecs"]
+    V = np.stack([pp.vector for pp in res.pairs])
+    assert np.abs(V @ V.T - np.eye(3)).max() <= 1e-9
+    pair_rows = [r for r in records if r.method == "sbci2"]
+    assert pair_rows and all(r.pair_partner == r.state + 1 for r in pair_rows)
+    assert all(r.method == "sbci1" and r.pair_partner == -1 for r in records if r.method != "sbci2")
+    op.close()
+
+
+@pytest.mark.parametrize("idx", [1])
+def test_sbci2_baseline_config_matches_reference(dev, rest, gold_dir, idx):
+    q = baseline_problem(idx, rest)
+    gg = gold(gold_dir, q.name)
+    if "sbci2" not in gg:
+        pytest.skip("golden SBCI2 record not generated (oracle/make_golden.py methods)")
+    g = gg["sbci2"]
+    op = P.FciOperator(to_product(q), max_determinants=2 ** 62)
+    res = P.solve_n_states_sbci2(op, len(g["energies"]))
+    e = np.array([pp.energy for pp in res.pairs])
+    assert np.abs(e - np.array(g["energies"])).max() <= E_TOL
+    assert [pp.iterations for pp in res.pairs] == g["iterations"]
+    assert res.summary.matvecs == g["matvecs"]
+    op.close()
+
+
+def test_sbci2_one_root_routes_to_sbci1(dev, gold_dir):
+    p, _ = fixture(gold_dir, "h6_4e")
+    op = P.as_operator(p, p.ms2)
+    r1 = P.solve_n_states_sbci1(op, 1)
+    r2 = P.solve_n_states_sbci2(op, 1)
+    assert r2.summary.method == "sbci2"
+    assert r1.pairs[0].energy == r2.pairs[0].energy and r1.summary.matvecs == r2.summary.matvecs
+    op.close()
+
+
 @pytest.mark.parametrize("k", [0, 1, 2, 3, 4])
 def test_sbci1_odd_sectors_vs_dense(dev, rest, k):
     q = odd_problem(rest, ODD[k])
