@@ -153,7 +153,8 @@ int sbg_profile_read(sbg_ctx* ctx, double* ms, int64_t* calls);
 int sbg_sigma_flops(const sbg_ctx* ctx, double* alpha_beta, double* same_spin, double* total);
 
 /* ---- solvers (drivers of sbci1.hpp:526-579 / sbci2.hpp:527-623 on device-resident vectors) ----
- * method: 1 = SBCI1 (solve_n_states_sbci1), 2 = SBCI2 (solve_n_states_sbci2); nroots <= 9. energies[nroots] ascending; vectors (nullable) nroots x n_det host buffer,
+ * method: 1 = SBCI1 (solve_n_states_sbci1), 2 = SBCI2 (solve_n_states_sbci2), 3 = block Davidson
+ * (davidson_solve(op, nroots, cfg), davidson.hpp:228-244); nroots <= 9. energies[nroots] ascending; vectors (nullable) nroots x n_det host buffer,
  * unit norm. trace may be NULL. */
 int sbg_solve(sbg_ctx* ctx, int method, int nroots, const sbg_config* cfg, double* energies,
               double* vectors, sbg_stats* stats, sbg_trace_fn trace, void* trace_user);

@@ -4,9 +4,11 @@ reached through the C ABI in include/sbg.h. No CPU fallback."""
 from .fci import (K_DEFAULT_DETERMINANT_GUARD, FciOperator, FciProblem, FcidumpError, as_operator, binomial,
                   determinant_count, parse_fcidump, parse_fcidump_file, sigma_apply, synthetic_problem)
 from .solver import (ConvergedEigenpair, MultiStateResult, NonConvergenceError, RunSummary, SolverConfig,
-                     StateSummary, TraceRecord, solve_n_states_sbci1, solve_n_states_sbci2)
+                     StateSummary, TraceRecord, solve_n_states_sbci1, solve_n_states_sbci2,
+                     davidson_solve)
 
 __all__ = ["K_DEFAULT_DETERMINANT_GUARD", "FciOperator", "FciProblem", "FcidumpError", "as_operator", "binomial",
            "determinant_count", "parse_fcidump", "parse_fcidump_file", "sigma_apply", "synthetic_problem",
            "ConvergedEigenpair", "MultiStateResult", "NonConvergenceError", "RunSummary", "SolverConfig",
-           "StateSummary", "TraceRecord", "solve_n_states_sbci1", "solve_n_states_sbci2"]
+           "StateSummary", "TraceRecord", "solve_n_states_sbci1", "solve_n_states_sbci2",
+           "davidson_solve"]

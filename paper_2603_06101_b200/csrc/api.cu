@@ -335,7 +335,8 @@ int sbg_solve(sbg_ctx* ctx, int method, int nroots, const sbg_config* cfg, doubl
               sbg_stats* stats, sbg_trace_fn trace, void* trace_user) {
     return guarded([&] {
         require_ctx(ctx);
-        if (method != 1 && method != 2) throw std::invalid_argument("sbg_solve: method must be 1 (sbci1) or 2 (sbci2)");
+        if (method < 1 || method > 3)
+            throw std::invalid_argument("sbg_solve: method must be 1 (sbci1), 2 (sbci2) or 3 (davidson)");
         if (nroots < 1 || nroots > sbg::detail_max_roots)
             throw std::invalid_argument("sbg_solve: nroots must be in 1..9 (at most 8 deflated states)");
         auto& c = *ctx->c;
@@ -371,8 +372,9 @@ int sbg_solve(sbg_ctx* ctx, int method, int nroots, const sbg_config* cfg, doubl
             };
         const uint64_t launches0 = c.launches;
         try {
-            sbg::MultiStateResult r = method == 1 ? sbg::solve_n_states_sbci1(c, nroots, to_cfg(cfg), tf)
-                                                  : sbg::solve_n_states_sbci2(c, nroots, to_cfg(cfg), tf);
+            sbg::MultiStateResult r = method == 1   ? sbg::solve_n_states_sbci1(c, nroots, to_cfg(cfg), tf)
+                                      : method == 2 ? sbg::solve_n_states_sbci2(c, nroots, to_cfg(cfg), tf)
+                                                    : sbg::davidson_solve(c, nroots, to_cfg(cfg), tf);
             for (int k = 0; k < nroots; ++k) {
                 energies[k] = r.pairs[k].energy;
                 if (vectors) c.download_local(r.pairs[k].vector.p, vectors + (size_t)k * c.ndet + c.row_lo * c.NB, c.st);

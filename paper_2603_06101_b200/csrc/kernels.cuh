@@ -122,6 +122,22 @@ struct PairSubArgs {
     double P[6][6];
 };
 void launch_pair_subspace(const PairSubArgs& a, const ReduceWs& ws, cudaStream_t st);
+// Davidson Ritz vectors (davidson.hpp:96-105, 109-111) over one chunk of <= kRitzChunk basis vectors:
+// ritz_k (+)= sum_i coef[i][k] b_i and ritz_im_k likewise from the images, accumulated in basis order
+// (first: from zero); on the last chunk also res_k = ritz_im_k - theta_k ritz_k and |res_k|^2
+constexpr int kRitzChunk = 16, kMaxRoots = 9;
+struct RitzArgs {
+    int64_t n;
+    int m, k, first, last;
+    const double* b[kRitzChunk];
+    const double* h[kRitzChunk];
+    double coef[kRitzChunk][kMaxRoots];
+    double theta[kMaxRoots];
+    double* ritz[kMaxRoots];
+    double* ritz_im[kMaxRoots];
+    double* res[kMaxRoots];
+};
+void launch_ritz(const RitzArgs& a, const ReduceWs& ws, cudaStream_t st);
 // argmin with index tie-break over a padded matrix (valid cols < ncols), excluding (value,index) <= prev
 void launch_argmin_after(const double* D, int64_t nrows, int64_t ncols, int64_t ld, int64_t row_lo, double prev_v,
                          int64_t prev_i, double* out_v, int64_t* out_i, double* part_v, int64_t* part_i, int grid,

@@ -49,6 +49,9 @@ constexpr int detail_max_roots = 9;  // deflation sets of up to 8 states (precon
 
 MultiStateResult solve_n_states_sbci1(Context& ctx, int n, const SolverConfig& cfg,
                                       const std::function<void(const TraceRec&)>& trace);
+// davidson_solve(op, nroots, cfg) (davidson.hpp:53-244): block Davidson cross-check
+MultiStateResult davidson_solve(Context& ctx, int nroots, const SolverConfig& cfg,
+                                const std::function<void(const TraceRec&)>& trace);
 // solve_n_states_sbci2 (sbci2.hpp:527-623): pair-sequential lowest-n driver
 MultiStateResult solve_n_states_sbci2(Context& ctx, int n, const SolverConfig& cfg,
                                       const std::function<void(const TraceRec&)>& trace);

@@ -301,6 +301,55 @@ __global__ void __launch_bounds__(kThreads) k_pair_subspace(const PairSubArgs a,
     block_reduce_store<36>(out, a.r * a.r, partial);
 }
 
+__global__ void __launch_bounds__(kThreads) k_ritz(const RitzArgs a, double* partial) {
+    double acc[kMaxRoots];
+#pragma unroll
+    for (int r = 0; r < kMaxRoots; ++r) acc[r] = 0.0;
+    const int64_t n2 = a.n >> 1, stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n2; e += stride) {
+        double2 R[kMaxRoots], H[kMaxRoots];
+#pragma unroll
+        for (int r = 0; r < kMaxRoots; ++r) {
+            if (r >= a.k) break;
+            if (a.first) {
+                R[r] = make_double2(0.0, 0.0);
+                H[r] = make_double2(0.0, 0.0);
+            } else {
+                R[r] = reinterpret_cast<const double2*>(a.ritz[r])[e];
+                H[r] = reinterpret_cast<const double2*>(a.ritz_im[r])[e];
+            }
+        }
+        for (int i = 0; i < a.m; ++i) {
+            const double2 b = reinterpret_cast<const double2*>(a.b[i])[e];
+            const double2 h = reinterpret_cast<const double2*>(a.h[i])[e];
+#pragma unroll
+            for (int r = 0; r < kMaxRoots; ++r) {
+                if (r >= a.k) break;
+                const double c = a.coef[i][r];
+                R[r].x = __dadd_rn(R[r].x, __dmul_rn(c, b.x));
+                R[r].y = __dadd_rn(R[r].y, __dmul_rn(c, b.y));
+                H[r].x = __dadd_rn(H[r].x, __dmul_rn(c, h.x));
+                H[r].y = __dadd_rn(H[r].y, __dmul_rn(c, h.y));
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < kMaxRoots; ++r) {
+            if (r >= a.k) break;
+            reinterpret_cast<double2*>(a.ritz[r])[e] = R[r];
+            reinterpret_cast<double2*>(a.ritz_im[r])[e] = H[r];
+            if (a.last) {
+                const double t = -a.theta[r];
+                double2 z;
+                z.x = __dadd_rn(H[r].x, __dmul_rn(t, R[r].x));
+                z.y = __dadd_rn(H[r].y, __dmul_rn(t, R[r].y));
+                reinterpret_cast<double2*>(a.res[r])[e] = z;
+                acc[r] = fma(z.y, z.y, fma(z.x, z.x, acc[r]));
+            }
+        }
+    }
+    block_reduce_store<kMaxRoots>(acc, a.last ? a.k : 0, partial);
+}
+
 __device__ __forceinline__ bool lex_less(double v1, int64_t i1, double v2, int64_t i2) {
     return v1 < v2 || (v1 == v2 && i1 < i2);
 }
@@ -454,6 +503,19 @@ void launch_gram(const double* const* v, int m, int64_t n, const ReduceWs& ws, c
     k_gram<<<g, kThreads, 0, st>>>(a, ws.partial);
     SBG_LAUNCH_CHECK();
     launch_reduce_finish(ws, g, m * (m + 1) / 2, st);
+}
+
+void launch_ritz(const RitzArgs& a, const ReduceWs& ws, cudaStream_t st) {
+    if (a.m < 1 || a.m > kRitzChunk || a.k < 1 || a.k > kMaxRoots || (a.n & 1))
+        throw InvalidArgument("launch_ritz: bad shape");
+    for (int i = 0; i < a.m; ++i) {
+        check_aligned(a.b[i]);
+        check_aligned(a.h[i]);
+    }
+    const int g = grid_of(reinterpret_cast<const void*>(&k_ritz), ws);
+    k_ritz<<<g, kThreads, 0, st>>>(a, ws.partial);
+    SBG_LAUNCH_CHECK();
+    if (a.last) launch_reduce_finish(ws, g, a.k, st);
 }
 
 void launch_pair_subspace(const PairSubArgs& a, const ReduceWs& ws, cudaStream_t st) {

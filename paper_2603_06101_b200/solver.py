@@ -180,3 +180,9 @@ def solve_n_states_sbci2(op, n: int, cfg: SolverConfig | None = None, sink=None,
     n = 1 routes to SBCI1 (the summary still says "sbci2", as the reference's does)."""
     r = _solve(op, 2, n, cfg, sink, want_vectors)
     return r
+
+
+def davidson_solve(op, nroots: int, cfg: SolverConfig | None = None, sink=None, want_vectors: bool = True):
+    """Block Davidson (davidson.hpp:228-244: eps0/r0/lindep from cfg, max_space 12*nroots, 400
+    iterations) on the GPU operator, with the SBCI solvers' (D - E0)^-1 preconditioner."""
+    return _solve(op, 3, nroots, cfg, sink, want_vectors)

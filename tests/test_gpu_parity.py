@@ -246,6 +246,52 @@ def test_sbci2_one_root_routes_to_sbci1(dev, gold_dir):
     op.close()
 
 
+@pytest.mark.parametrize("name", ["h4_2e", "h6_4e"])
+def test_davidson_fixtures_match_reference(dev, gold_dir, name):
+    """Device block Davidson (davidson.hpp:53-244) vs the reference's davidson_solve on the fixture."""
+    p, _ = fixture(gold_dir, name)
+    g = gold(gold_dir, name)["davidson"]
+    op = P.as_operator(p, p.ms2)
+    records = []
+    res = P.davidson_solve(op, 3, sink=records.append)
+    assert res.summary.method == "davidson"
+    e = np.array([pp.energy for pp in res.pairs])
+    assert np.abs(e - np.array(g["energies"])).max() <= E_TOL
+    assert np.abs(e - np.array(gold(gold_dir, name)["dense_eigs"][:3])).max() <= 1e-10
+    assert [pp.iterations for pp in res.pairs] == g["iterations"]
+    assert res.summary.matvecs == g["matvecs"]
+    assert all(r.method == "davidson" for r in records) and len(records) == 3 * g["iterations"][0]
+    V = np.stack([pp.vector for pp in res.pairs])
+    assert np.abs(V @ V.T - np.eye(3)).max() <= 1e-9
+    op.close()
+
+
+@pytest.mark.parametrize("idx", [1])
+def test_davidson_baseline_config_matches_reference(dev, rest, gold_dir, idx):
+    q = baseline_problem(idx, rest)
+    gg = gold(gold_dir, q.name)
+    if "davidson" not in gg:
+        pytest.skip("golden Davidson record not generated (oracle/make_golden.py methods)")
+    g = gg["davidson"]
+    op = P.FciOperator(to_product(q), max_determinants=2 ** 62)
+    res = P.davidson_solve(op, len(g["energies"]))
+    e = np.array([pp.energy for pp in res.pairs])
+    assert np.abs(e - np.array(g["energies"])).max() <= E_TOL
+    op.close()
+
+
+def test_sbci1_vs_davidson_c3(dev, rest):
+    """above (12e,12o) the serial reference cannot produce energy goldens; the GPU SBCI1
+    energies are cross-checked against GPU block Davidson (acceptance.cpp:126-163 pattern)."""
+    q = baseline_problem(3, rest)
+    op = P.FciOperator(to_product(q), max_determinants=2 ** 62)
+    e1 = np.array([pp.energy for pp in P.solve_n_states_sbci1(op, 2, want_vectors=False).pairs])
+    e2 = np.array([pp.energy for pp in P.solve_n_states_sbci2(op, 2, want_vectors=False).pairs])
+    ed = np.array([pp.energy for pp in P.davidson_solve(op, 2, want_vectors=False).pairs])
+    assert np.abs(e1 - ed).max() <= E_TOL and np.abs(e2 - ed).max() <= E_TOL
+    op.close()
+
+
 @pytest.mark.parametrize("k", [0, 1, 2, 3, 4])
 def test_sbci1_odd_sectors_vs_dense(dev, rest, k):
     q = odd_problem(rest, ODD[k])
