@@ -75,6 +75,8 @@ typedef struct sbg_stats {
     /* device-side accounting for the bench */
     double sigma_seconds;       /* summed sigma time (CUDA events) */
     uint64_t kernel_launches;   /* kernels launched by the library during the call */
+    /* <S^2> of each returned state (fci/spin.hpp:17-51, the CLI summary's s_squared column) */
+    double s_squared[SBG_MAX_ROOTS];
 } sbg_stats;
 
 /* Per-iteration trace record (TraceRecord trace.hpp:22-44). Fields a method does not produce are NaN. */
@@ -156,6 +158,10 @@ int sbg_sigma_flops(const sbg_ctx* ctx, double* alpha_beta, double* same_spin, d
  * method: 1 = SBCI1 (solve_n_states_sbci1), 2 = SBCI2 (solve_n_states_sbci2), 3 = block Davidson
  * (davidson_solve(op, nroots, cfg), davidson.hpp:228-244); nroots <= 9. energies[nroots] ascending; vectors (nullable) nroots x n_det host buffer,
  * unit norm. trace may be NULL. */
+/* <S^2> = |S+ x|^2/|x|^2 + S_z(S_z+1) (fci/spin.hpp:17-51). x: full n_det host vector. */
+int sbg_spin_squared(sbg_ctx* ctx, const double* x, double* out);
+/* same on a padded local device vector (every rank passes its rows; collective when world > 1) */
+int sbg_spin_squared_padded(sbg_ctx* ctx, const double* d_x_padded_local, double* out);
 int sbg_solve(sbg_ctx* ctx, int method, int nroots, const sbg_config* cfg, double* energies,
               double* vectors, sbg_stats* stats, sbg_trace_fn trace, void* trace_user);
 

@@ -30,7 +30,8 @@ class Stats(C.Structure):
                 ("matvecs", C.c_uint64), ("total_iterations", C.c_int64), ("total_restarts", C.c_int32),
                 ("hx_refreshes", C.c_int32), ("peak_vectors", C.c_int32), ("wall_time_s", C.c_double),
                 ("failed_state", C.c_int32), ("best_energy", C.c_double), ("best_residual", C.c_double),
-                ("sigma_seconds", C.c_double), ("kernel_launches", C.c_uint64)]
+                ("sigma_seconds", C.c_double), ("kernel_launches", C.c_uint64),
+                ("s_squared", C.c_double * SBG_MAX_ROOTS)]
 
 
 class TraceRecordC(C.Structure):
@@ -91,6 +92,8 @@ def lib() -> C.CDLL:
         "sbg_sigma_flops": (C.c_int, [P, D, D, D]),
         "sbg_profile_reset": (C.c_int, [P]),
         "sbg_profile_read": (C.c_int, [P, D, C.POINTER(C.c_int64)]),
+        "sbg_spin_squared": (C.c_int, [P, D, D]),
+        "sbg_spin_squared_padded": (C.c_int, [P, P, D]),
         "sbg_solve": (C.c_int, [P, C.c_int, C.c_int, C.POINTER(Config), D, D, C.POINTER(Stats), TRACE_FN, P]),
         "sbg_selftest": (C.c_int, []),
     }
@@ -109,7 +112,7 @@ EXPORTED = ["sbg_last_error", "sbg_version", "sbg_binomial", "sbg_determinant_co
             "sbg_diagonal", "sbg_table_sizes", "sbg_string_tables", "sbg_sigma", "sbg_sigma_device",
             "sbg_padded_len", "sbg_pack", "sbg_unpack", "sbg_sigma_padded", "sbg_apply_count",
             "sbg_reset_apply_count", "sbg_kernel_launches", "sbg_sigma_flops", "sbg_profile_reset", "sbg_profile_read",
-            "sbg_solve", "sbg_selftest"]
+            "sbg_spin_squared", "sbg_spin_squared_padded", "sbg_solve", "sbg_selftest"]
 
 
 class SbgError(RuntimeError):

@@ -22,7 +22,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
 SOURCES = ["tables.cu", "sigma_ab.cu", "sigma_ss.cu", "vec.cu", "selftest.cu", "context.cu", "solver.cu", "sbci2.cu",
-           "davidson.cu", "api.cu"]
+           "davidson.cu", "spin.cu", "api.cu"]
 PER_FILE = {"tables.cu": ["--fmad=false"]}
 
 

@@ -331,6 +331,25 @@ int sbg_sigma_flops(const sbg_ctx* ctx, double* ab, double* ss, double* total) {
     });
 }
 
+int sbg_spin_squared(sbg_ctx* ctx, const double* x, double* out) {
+    return guarded([&] {
+        require_ctx(ctx);
+        if (!x || !out) throw std::invalid_argument("sbg_spin_squared: null argument");
+        auto& c = *ctx->c;
+        double* dx = c.io_x();
+        c.upload_local(x, dx, c.st);
+        *out = c.spin_squared(dx);
+    });
+}
+
+int sbg_spin_squared_padded(sbg_ctx* ctx, const double* d_x, double* out) {
+    return guarded([&] {
+        require_ctx(ctx);
+        if (!d_x || !out) throw std::invalid_argument("sbg_spin_squared_padded: null argument");
+        *out = ctx->c->spin_squared(d_x);
+    });
+}
+
 int sbg_solve(sbg_ctx* ctx, int method, int nroots, const sbg_config* cfg, double* energies, double* vectors,
               sbg_stats* stats, sbg_trace_fn trace, void* trace_user) {
     return guarded([&] {
@@ -375,6 +394,8 @@ int sbg_solve(sbg_ctx* ctx, int method, int nroots, const sbg_config* cfg, doubl
             sbg::MultiStateResult r = method == 1   ? sbg::solve_n_states_sbci1(c, nroots, to_cfg(cfg), tf)
                                       : method == 2 ? sbg::solve_n_states_sbci2(c, nroots, to_cfg(cfg), tf)
                                                     : sbg::davidson_solve(c, nroots, to_cfg(cfg), tf);
+            std::vector<double> s2(nroots);
+            for (int k = 0; k < nroots; ++k) s2[k] = c.spin_squared(r.pairs[k].vector.p);
             for (int k = 0; k < nroots; ++k) {
                 energies[k] = r.pairs[k].energy;
                 if (vectors) c.download_local(r.pairs[k].vector.p, vectors + (size_t)k * c.ndet + c.row_lo * c.NB, c.st);
@@ -396,6 +417,7 @@ int sbg_solve(sbg_ctx* ctx, int method, int nroots, const sbg_config* cfg, doubl
                 stats->wall_time_s = r.wall_time_s;
                 stats->failed_state = -1;
                 stats->kernel_launches = c.launches - launches0;
+                for (int k = 0; k < nroots; ++k) stats->s_squared[k] = s2[k];
             }
         } catch (const sbg::NonConvergenceError& e) {
             if (stats) {

@@ -323,6 +323,33 @@ void Context::gather_full(const double* x_local, cudaStream_t s) {
                            comm_->comm, s));
 }
 
+double Context::spin_squared(const double* x_local) {
+    const double* v[1] = {x_local};
+    launch_gram(v, 1, padded_len(), rws, st);
+    launches += 2;
+    const double xx = finish_dots(1)[0];
+    if (!(xx > 0.0)) throw std::invalid_argument("spin_squared: zero vector");
+    const double sz = 0.5 * (na_el - nb_el);
+    double raised_sq = 0.0;
+    if (nb_el > 0 && na_el < norb) {
+        const double* xf = x_local;
+        if (world > 1) {
+            gather_full(x_local, st);
+            xf = xfull_.p;
+        }
+        int64_t lo, hi;
+        shard_range((int64_t)binom_host_calc(norb, na_el + 1), rank, world, &lo, &hi);
+        if (hi > lo) {
+            launch_spin_raise(xf, ld, na_el, nb_el, norb, lo, hi, rws, st);
+            launches += 2;
+        } else {
+            SBG_CUDA(cudaMemsetAsync(rws.result, 0, 8, st));
+        }
+        raised_sq = finish_dots(1)[0];
+    }
+    return raised_sq / xx + sz * (sz + 1.0);
+}
+
 void Context::allreduce_inplace_device(double* d, int count) {
     if (world > 1 && count > 0) SBG_NCCL(ncclAllReduce(d, d, count, ncclDouble, ncclSum, comm_->comm, st));
 }

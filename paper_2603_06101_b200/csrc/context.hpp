@@ -88,6 +88,8 @@ public:
     // y = H x on padded local vectors (counts one application)
     void sigma(const double* x_local, double* y_local, cudaStream_t s);
     void sigma(const DBuf& x, DBuf& y) { sigma(x.p, y.p, st); }
+    // <S^2> of a padded local vector (fci/spin.hpp:17-51); collective over ranks
+    double spin_squared(const double* x_local);
 
     // host <-> padded device conversions (dense local rows = rows [row_lo,row_hi) of the n_det vector)
     void upload_local(const double* host_dense_full, double* d_padded, cudaStream_t s) const;

@@ -146,6 +146,12 @@ void launch_kinetic(const double* y, const double* D, double shift, int64_t n, c
 void launch_fill(double* p, int64_t n, double v, cudaStream_t st);
 void launch_set_element(double* p, int64_t idx, double v, cudaStream_t st);
 
+// ---- spin.cu ----
+// |S+ x|^2 over raised-sector alpha strings [ja_lo, ja_hi) (fci/spin.hpp:17-51); x_full is the whole
+// padded vector; the result lands in ws.result[0]
+void launch_spin_raise(const double* x_full, int64_t ld, int na, int nb, int norb, int64_t ja_lo, int64_t ja_hi,
+                       const ReduceWs& ws, cudaStream_t st);
+
 // ---- selftest.cu ----
 int run_mma_selftest();
 

@@ -238,6 +238,15 @@ class FciOperator:
             self._diag = d
         return self._diag
 
+    def spin_squared(self, x) -> float:
+        """<S^2> of a CI vector (fci/spin.hpp:17-51), computed on the GPU."""
+        x = np.ascontiguousarray(x, np.float64)
+        if x.shape != (self.dim(),):
+            raise ValueError("spin_squared: vector length mismatch")
+        out = C.c_double()
+        check(lib().sbg_spin_squared(self._h, _dp(x), C.byref(out)))
+        return out.value
+
     def apply_count(self) -> int:
         return int(lib().sbg_apply_count(self._h))
 

@@ -162,7 +162,8 @@ def _solve(op, method: int, n: int, cfg: SolverConfig | None, sink, want_vectors
     for k in range(n):
         pairs.append(ConvergedEigenpair(k, float(e[k]), vec[k] if vec is not None else None, st.iterations[k],
                                         st.restarts[k], st.final_residual[k]))
-        states.append(StateSummary(k, float(e[k]), st.iterations[k], st.restarts[k], st.final_residual[k]))
+        states.append(StateSummary(k, float(e[k]), st.iterations[k], st.restarts[k], st.final_residual[k],
+                                   float(st.s_squared[k])))
     summ = RunSummary(name, states, st.total_iterations, st.total_restarts, st.matvecs, st.hx_refreshes,
                       st.peak_vectors, st.wall_time_s, st.kernel_launches)
     return MultiStateResult(pairs, summ)

@@ -331,6 +331,35 @@ def test_kernel_launch_accounting(dev, rest):
     op.close()
 
 
+@pytest.mark.parametrize("spec", [(6, 6, 0, 0.0, 3), (10, 10, 0, 0.0, 5), (5, 5, 1, 0.3, 9), (7, 5, -1, 0.0, 11),
+                                  (6, 2, 2, 0.1, 13), (4, 4, 0, 0.0, 2)])
+def test_spin_squared_matches_reference(dev, rest, spec):
+    """<S^2> (fci/spin.hpp:17-51) on seeded vectors vs the compiled reference's spin_squared."""
+    from oracle import Reference
+    if not Reference.available():
+        pytest.skip("oracle/_ref/libsbci_ref.so not built")
+    q = odd_problem(rest, spec)
+    op = P.FciOperator(to_product(q), max_determinants=2 ** 62)
+    x = np.random.default_rng(spec[-1]).uniform(-1, 1, op.dim())
+    s_ref = Reference().spin_squared(q.norb, (q.nelec + q.ms2) // 2, (q.nelec - q.ms2) // 2, x)
+    s_gpu = op.spin_squared(x)
+    assert abs(s_gpu - s_ref) <= 1e-12 * max(1.0, abs(s_ref))
+    op.close()
+
+
+@pytest.mark.parametrize("name", ["h4_2e", "h6_4e"])
+def test_solve_reports_spin_squared(dev, gold_dir, name):
+    p, _ = fixture(gold_dir, name)
+    g = gold(gold_dir, name)["sbci1"]
+    op = P.as_operator(p, p.ms2)
+    res = P.solve_n_states_sbci1(op, 3)
+    s2 = np.array([s.s_squared for s in res.summary.states])
+    assert np.abs(s2 - np.array(g["s_squared"])).max() <= 1e-6
+    for pp, ss in zip(res.pairs, res.summary.states):
+        assert abs(op.spin_squared(pp.vector) - ss.s_squared) <= 1e-12
+    op.close()
+
+
 @pytest.mark.parametrize("name,method", [("h6_4e", 1), ("h6_4e", 2), ("h6_4e", 3), ("c1", 1)])
 def test_reference_drivers_run_on_gpu_sigma(dev, rest, gold_dir, name, method):
     """Drop-in: the reference's own solve_n_states_sbci1/_sbci2/davidson_solve (compiled unmodified)
