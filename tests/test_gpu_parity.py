@@ -277,6 +277,8 @@ def test_davidson_baseline_config_matches_reference(dev, rest, gold_dir, idx):
     res = P.davidson_solve(op, len(g["energies"]))
     e = np.array([pp.energy for pp in res.pairs])
     assert np.abs(e - np.array(g["energies"])).max() <= E_TOL
+    assert [pp.iterations for pp in res.pairs] == g["iterations"]
+    assert res.summary.matvecs == g["matvecs"]
     op.close()
 
 
