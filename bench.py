@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tte", action="store_true", help="skip the time-to-energy solves")
+    ap.add_argument("--tte-full", action="store_true", help="also solve c4 (3 roots, ~4 min) for time-to-energy")
     return ap.parse_args()
 
 
@@ -146,27 +147,46 @@ def profile_traffic(cfg_name):
         return None
 
 
-def time_to_energy():
-    """Second half of the BASELINE metric: SBCI1 solves on the GPU through the public API
-    (solve_n_states_sbci1, reference SolverConfig defaults), wall time from solver start with the
-    operator built, energies vs the reference's own converged energies (tests/golden, produced by
-    the compiled reference on the same pinned integrals)."""
+def time_to_energy(full=False):
+    """Second half of the BASELINE metric: solves on the GPU through the public API (reference
+    SolverConfig defaults), wall time of the solver call with the operator built. c1/c2: energies vs
+    the reference's own converged energies (tests/golden, produced by the compiled reference on the
+    same pinned integrals) and the reference's single-core wall time. c3 (and c4 with --tte-full),
+    where the serial reference has no energies: SBCI1 vs GPU block Davidson."""
     import numpy as np
     import paper_2603_06101_b200 as P
     out = {}
-    for tag, (norb, ne, sc), nroots in (("c1", (10, 10, 0.05), 4), ("c2", (12, 12, 0.05), 1)):
-        with open(os.path.join(ROOT, "tests", "golden", f"golden_{tag}.json")) as f:
-            ref = json.load(f)["sbci1"]
+    runs = [("c1", (10, 10, 0.05), 4, ("sbci1", "sbci2", "davidson")), ("c2", (12, 12, 0.05), 1, ("sbci1",)),
+            ("c3", (14, 14, 0.05), 2, ("sbci1", "davidson"))]
+    if full:
+        runs.append(("c4", (16, 16, 0.08), 3, ("sbci1", "davidson")))
+    solvers = {"sbci1": P.solve_n_states_sbci1, "sbci2": P.solve_n_states_sbci2, "davidson": P.davidson_solve}
+    for tag, (norb, ne, sc), nroots, methods in runs:
+        ref = {}
+        gpath = os.path.join(ROOT, "tests", "golden", f"golden_{tag}.json")
+        if os.path.exists(gpath):
+            with open(gpath) as f:
+                ref = json.load(f)
         op = P.FciOperator(P.synthetic_problem(norb, ne, SEED, sc), max_determinants=2 ** 62)
         P.solve_n_states_sbci1(op, 1, want_vectors=False)          # warm-up (module load, first launches)
-        t0 = time.perf_counter()
-        res = P.solve_n_states_sbci1(op, nroots, want_vectors=False)
-        wall = time.perf_counter() - t0
-        e = np.array([p.energy for p in res.pairs])
-        out[tag] = {"nroots": nroots, "seconds": wall, "sigma_builds": res.summary.matvecs,
-                    "iterations": res.summary.total_iterations,
-                    "max_abs_dE_vs_reference_Eh": float(np.abs(e - np.array(ref["energies"])).max()),
-                    "reference_seconds_1core": ref["wall_s"], "reference_sigma_builds": ref["matvecs"]}
+        rec = {"nroots": nroots}
+        energies = {}
+        for m in methods:
+            t0 = time.perf_counter()
+            res = solvers[m](op, nroots, want_vectors=False)
+            wall = time.perf_counter() - t0
+            e = np.array([p.energy for p in res.pairs])
+            energies[m] = e
+            r = {"seconds": wall, "sigma_builds": res.summary.matvecs, "iterations": res.summary.total_iterations,
+                 "energies": e.tolist(), "s_squared": [s.s_squared for s in res.summary.states]}
+            if m in ref:
+                r["max_abs_dE_vs_reference_Eh"] = float(np.abs(e - np.array(ref[m]["energies"])).max())
+                r["reference_seconds_1core"] = ref[m]["wall_s"]
+                r["reference_sigma_builds"] = ref[m]["matvecs"]
+            rec[m] = r
+        if "davidson" in energies and "sbci1" in energies and not ("sbci1" in ref):
+            rec["max_abs_dE_sbci1_vs_davidson_Eh"] = float(np.abs(energies["sbci1"] - energies["davidson"]).max())
+        out[tag] = rec
         op.close()
     return out
 
@@ -307,7 +327,7 @@ def run_ours(args):
             "clocks": clocks,
         }
         if world == 1 and not args.no_tte:
-            out["time_to_energy"] = time_to_energy()
+            out["time_to_energy"] = time_to_energy(args.tte_full)
         if world == 1 and not args.no_cpu_baseline:
             cb = cpu_baseline(args.config)
             out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
