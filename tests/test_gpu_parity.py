@@ -236,6 +236,27 @@ def test_sbci2_baseline_config_matches_reference(dev, rest, gold_dir, idx):
     op.close()
 
 
+def test_trace_csv_from_device_solves(dev, gold_dir, tmp_path):
+    """Solver records through the reference's CSV sink format (trace.hpp:68-118) and back."""
+    p, _ = fixture(gold_dir, "h6_4e")
+    op = P.as_operator(p, p.ms2)
+    path = tmp_path / "trace.csv"
+    mem = P.MemoryTraceSink()
+    with P.CsvTraceSink(str(path)) as csv_sink:
+        res = P.solve_n_states_sbci2(op, 3, sink=P.TeeTraceSink(csv_sink, mem))
+        P.davidson_solve(op, 2, sink=P.TeeTraceSink(csv_sink, mem))
+    back = P.read_trace_csv_file(str(path))
+    assert len(back) == len(mem.records) > res.summary.total_iterations
+    assert {r.method for r in back} == {"sbci1", "sbci2", "davidson"}
+    for a, b in zip(mem.records, back):
+        assert (a.method, a.state, a.pair_partner, a.t, a.matvecs, a.restart_reason) == \
+               (b.method, b.state, b.pair_partner, b.t, b.matvecs, b.restart_reason)
+        assert a.energy == b.energy and (a.dE == b.dE or (np.isnan(a.dE) and np.isnan(b.dE)))
+    assert all(np.isfinite(r.kinetic) for r in back if r.method != "davidson")
+    assert all(np.isnan(r.kinetic) and np.isnan(r.b) for r in back if r.method == "davidson")
+    op.close()
+
+
 def test_sbci2_one_root_routes_to_sbci1(dev, gold_dir):
     p, _ = fixture(gold_dir, "h6_4e")
     op = P.as_operator(p, p.ms2)
