@@ -118,6 +118,15 @@ int sbg_create_dist(int norb, int nelec, int ms2, double e_core, const double* h
                     int device, uint64_t max_det, int rank, int world, const void* nccl_unique_id,
                     sbg_ctx** out);
 int sbg_nccl_unique_id(void* out128);
+/* Testing aid for the sharded path without several GPUs: the ranks of a group are threads of one
+ * process (each calls the collective entry points — sbg_sigma*, sbg_solve, sbg_spin_squared — on
+ * its own context concurrently); collectives run through host barriers and device copies. Same
+ * partition and kernels as sbg_create_dist. */
+typedef struct sbg_local_group sbg_local_group;
+int sbg_local_group_create(int world, sbg_local_group** out);
+void sbg_local_group_destroy(sbg_local_group* group);
+int sbg_create_local(int norb, int nelec, int ms2, double e_core, const double* h1, const double* eri,
+                     int device, uint64_t max_det, sbg_local_group* group, int rank, sbg_ctx** out);
 void sbg_destroy(sbg_ctx* ctx);
 
 int64_t sbg_dim(const sbg_ctx* ctx);                                 /* SymmetricOperator::dim */

@@ -93,6 +93,10 @@ def lib() -> C.CDLL:
         "sbg_profile_reset": (C.c_int, [P]),
         "sbg_profile_read": (C.c_int, [P, D, C.POINTER(C.c_int64)]),
         "sbg_spin_squared": (C.c_int, [P, D, D]),
+        "sbg_local_group_create": (C.c_int, [C.c_int, C.POINTER(P)]),
+        "sbg_local_group_destroy": (None, [P]),
+        "sbg_create_local": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, D, D, C.c_int, C.c_uint64, P, C.c_int,
+                                       C.POINTER(P)]),
         "sbg_spin_squared_padded": (C.c_int, [P, P, D]),
         "sbg_solve": (C.c_int, [P, C.c_int, C.c_int, C.POINTER(Config), D, D, C.POINTER(Stats), TRACE_FN, P]),
         "sbg_selftest": (C.c_int, []),
@@ -112,7 +116,8 @@ EXPORTED = ["sbg_last_error", "sbg_version", "sbg_binomial", "sbg_determinant_co
             "sbg_diagonal", "sbg_table_sizes", "sbg_string_tables", "sbg_sigma", "sbg_sigma_device",
             "sbg_padded_len", "sbg_pack", "sbg_unpack", "sbg_sigma_padded", "sbg_apply_count",
             "sbg_reset_apply_count", "sbg_kernel_launches", "sbg_sigma_flops", "sbg_profile_reset", "sbg_profile_read",
-            "sbg_spin_squared", "sbg_spin_squared_padded", "sbg_solve", "sbg_selftest"]
+            "sbg_spin_squared", "sbg_spin_squared_padded", "sbg_local_group_create", "sbg_local_group_destroy",
+            "sbg_create_local", "sbg_solve", "sbg_selftest"]
 
 
 class SbgError(RuntimeError):

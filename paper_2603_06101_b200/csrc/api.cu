@@ -69,8 +69,11 @@ sbg::SolverConfig to_cfg(const sbg_config* c) {
     return s;
 }
 
+// every context entry point runs on the context's device (the calling thread may be a different
+// one than the creating thread, e.g. the ranks of a local group)
 void require_ctx(const sbg_ctx* ctx) {
     if (!ctx || !ctx->c) throw std::invalid_argument("null sbg_ctx");
+    SBG_CUDA(cudaSetDevice(ctx->c->device));
 }
 }  // namespace
 
@@ -180,6 +183,32 @@ int sbg_create_dist(int norb, int nelec, int ms2, double e_core, const double* h
         try {
             c->c = std::make_unique<sbg::Context>(norb, nelec, ms2, e_core, h1, eri, device, max_det, rank, world,
                                                   nccl_unique_id);
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
+    });
+}
+
+int sbg_local_group_create(int world, sbg_local_group** out) {
+    return guarded([&] {
+        if (!out || world < 1) throw std::invalid_argument("sbg_local_group_create: bad arguments");
+        *out = reinterpret_cast<sbg_local_group*>(new sbg::LocalGroup(world));
+    });
+}
+
+void sbg_local_group_destroy(sbg_local_group* g) { delete reinterpret_cast<sbg::LocalGroup*>(g); }
+
+int sbg_create_local(int norb, int nelec, int ms2, double e_core, const double* h1, const double* eri, int device,
+                     uint64_t max_det, sbg_local_group* group, int rank, sbg_ctx** out) {
+    return guarded([&] {
+        if (!out || !h1 || !eri || !group) throw std::invalid_argument("sbg_create_local: null argument");
+        auto* g = reinterpret_cast<sbg::LocalGroup*>(group);
+        auto* c = new sbg_ctx;
+        try {
+            c->c = std::make_unique<sbg::Context>(norb, nelec, ms2, e_core, h1, eri, device, max_det, rank, g->world,
+                                                  nullptr, g);
         } catch (...) {
             delete c;
             throw;

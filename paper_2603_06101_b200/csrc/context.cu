@@ -64,19 +64,99 @@ VecPool::~VecPool() {
     for (double* p : free_) cudaFree(p);
 }
 
-// ------------------------------------------------------------------ NCCL plumbing
-struct Comm {
-    ncclComm_t comm = nullptr;
-    ~Comm() {
-        if (comm) ncclCommDestroy(comm);
-    }
-};
+// ------------------------------------------------------------------ collectives (comm.hpp)
 #define SBG_NCCL(x)                                                                                     \
     do {                                                                                                \
         ncclResult_t r_ = (x);                                                                          \
         if (r_ != ncclSuccess) throw DeviceError(std::string("NCCL error ") + ncclGetErrorString(r_) + \
                                                  " in " #x);                                            \
     } while (0)
+
+namespace {
+
+class NcclComm final : public Comm {
+public:
+    NcclComm(int world, int rank, const void* id_bytes) {
+        ncclUniqueId id;
+        std::memcpy(&id, id_bytes, sizeof(id));
+        SBG_NCCL(ncclCommInitRank(&comm_, world, id, rank));
+    }
+    ~NcclComm() override {
+        if (comm_) ncclCommDestroy(comm_);
+    }
+    void all_gather(const double* send, double* recv, size_t count, cudaStream_t s) override {
+        SBG_NCCL(ncclAllGather(send, recv, count, ncclDouble, comm_, s));
+    }
+    void all_reduce_sum(double* buf, size_t count, cudaStream_t s) override {
+        SBG_NCCL(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, comm_, s));
+    }
+    void exchange(const std::vector<CommBlock>& sends, const std::vector<CommBlock>& recvs, cudaStream_t s) override {
+        SBG_NCCL(ncclGroupStart());
+        for (const auto& b : sends) SBG_NCCL(ncclSend(b.ptr, b.count, ncclDouble, b.peer, comm_, s));
+        for (const auto& b : recvs) SBG_NCCL(ncclRecv(b.ptr, b.count, ncclDouble, b.peer, comm_, s));
+        SBG_NCCL(ncclGroupEnd());
+    }
+
+private:
+    ncclComm_t comm_ = nullptr;
+};
+
+// ranks = threads of one process; every collective: finish my stream, publish, barrier, copy, barrier
+class LocalComm final : public Comm {
+public:
+    LocalComm(LocalGroup* g, int rank) : g_(g), rank_(rank) {}
+    void all_gather(const double* send, double* recv, size_t count, cudaStream_t s) override {
+        SBG_CUDA(cudaStreamSynchronize(s));
+        g_->ptr[rank_] = send;
+        g_->barrier();
+        for (int r = 0; r < g_->world; ++r)
+            if (recv + r * count != g_->ptr[r])
+                SBG_CUDA(cudaMemcpyAsync(recv + r * count, g_->ptr[r], count * 8, cudaMemcpyDeviceToDevice, s));
+        SBG_CUDA(cudaStreamSynchronize(s));
+        g_->barrier();  // nobody reads my send buffer any more
+    }
+    void all_reduce_sum(double* buf, size_t count, cudaStream_t s) override {
+        SBG_CUDA(cudaStreamSynchronize(s));
+        g_->ptr[rank_] = buf;
+        g_->barrier();
+        std::vector<double> acc(count, 0.0), part(count);
+        for (int r = 0; r < g_->world; ++r) {  // rank order: every rank forms the identical sum
+            SBG_CUDA(cudaMemcpy(part.data(), g_->ptr[r], count * 8, cudaMemcpyDeviceToHost));
+            for (size_t i = 0; i < count; ++i) acc[i] += part[i];
+        }
+        g_->barrier();  // all reads done before anyone overwrites its buffer
+        SBG_CUDA(cudaMemcpyAsync(buf, acc.data(), count * 8, cudaMemcpyHostToDevice, s));
+        SBG_CUDA(cudaStreamSynchronize(s));
+    }
+    void exchange(const std::vector<CommBlock>& sends, const std::vector<CommBlock>& recvs, cudaStream_t s) override {
+        SBG_CUDA(cudaStreamSynchronize(s));
+        g_->sends[rank_] = sends;
+        g_->barrier();
+        for (const auto& rb : recvs) {
+            const CommBlock* sb = nullptr;
+            for (const auto& b : g_->sends[rb.peer])
+                if (b.peer == rank_) sb = &b;
+            if (!sb || sb->count != rb.count) throw DeviceError("local exchange: unmatched block");
+            SBG_CUDA(cudaMemcpyAsync(rb.ptr, sb->ptr, rb.count * 8, cudaMemcpyDeviceToDevice, s));
+        }
+        SBG_CUDA(cudaStreamSynchronize(s));
+        g_->barrier();
+    }
+
+private:
+    LocalGroup* g_;
+    int rank_;
+};
+
+}  // namespace
+
+std::unique_ptr<Comm> make_nccl_comm(int world, int rank, const void* nccl_unique_id) {
+    return std::make_unique<NcclComm>(world, rank, nccl_unique_id);
+}
+std::unique_ptr<Comm> make_local_comm(LocalGroup* group, int rank) {
+    if (!group || rank < 0 || rank >= group->world) throw InvalidArgument("local group: bad rank");
+    return std::make_unique<LocalComm>(group, rank);
+}
 
 namespace {
 
@@ -106,7 +186,7 @@ void shard_range(int64_t n, int rank, int world, int64_t* lo, int64_t* hi) {
 
 // ------------------------------------------------------------------ context
 Context::Context(int norb_, int nelec_, int ms2_, double e_core_, const double* h1, const double* eri, int device_,
-                 uint64_t max_det, int rank_, int world_, const void* nccl_id)
+                 uint64_t max_det, int rank_, int world_, const void* nccl_id, LocalGroup* local_group)
     : norb(norb_), nelec(nelec_), ms2(ms2_), e_core(e_core_), rank(rank_), world(world_), device(device_) {
     if (norb < 1 || norb > kMaxOrb) throw InvalidArgument("FciProblem: norb must be in [1, 32]");
     if (nelec < 0 || nelec > 2 * norb) throw InvalidArgument("as_operator: NELEC out of range");
@@ -136,10 +216,8 @@ Context::Context(int norb_, int nelec_, int ms2_, double e_core_, const double* 
     SBG_CUDA(cudaEventCreate(&ev1_));
 
     if (world > 1) {
-        comm_ = std::make_unique<Comm>();
-        ncclUniqueId id;
-        std::memcpy(&id, nccl_id, sizeof(id));
-        SBG_NCCL(ncclCommInitRank(&comm_->comm, world, id, rank));
+        if (local_group && local_group->world != world) throw InvalidArgument("local group: world mismatch");
+        comm_ = local_group ? make_local_comm(local_group, rank) : make_nccl_comm(world, rank, nccl_id);
     }
 
     rws.grid = 16 * nsm;
@@ -319,8 +397,7 @@ void Context::gather_full(const double* x_local, cudaStream_t s) {
     if (nrows > 0)
         SBG_CUDA(cudaMemcpyAsync(xfull_.p + (int64_t)rank * per * ld, x_local, nrows * ld * 8,
                                  cudaMemcpyDeviceToDevice, s));
-    SBG_NCCL(ncclAllGather(xfull_.p + (int64_t)rank * per * ld, xfull_.p, (size_t)(per * ld), ncclDouble,
-                           comm_->comm, s));
+    comm_->all_gather(xfull_.p + (int64_t)rank * per * ld, xfull_.p, (size_t)(per * ld), s);
 }
 
 double Context::spin_squared(const double* x_local) {
@@ -351,7 +428,7 @@ double Context::spin_squared(const double* x_local) {
 }
 
 void Context::allreduce_inplace_device(double* d, int count) {
-    if (world > 1 && count > 0) SBG_NCCL(ncclAllReduce(d, d, count, ncclDouble, ncclSum, comm_->comm, st));
+    if (world > 1 && count > 0) comm_->all_reduce_sum(d, (size_t)count, st);
 }
 
 const double* Context::finish_dots(int ndot) {
@@ -449,16 +526,15 @@ void Context::sigma(const double* x_local, double* y_local, cudaStream_t s) {
                                                nr, cudaMemcpyDeviceToDevice, s));
                 off += nr * wl;
             }
-            SBG_NCCL(ncclGroupStart());
+            std::vector<CommBlock> sends, recvs;
             off = 0;
             int64_t roff = 0;
             for (int r = 0; r < world; ++r) {
                 const int64_t nr = rhi[r] - rlo[r];
                 const int64_t rw = cwh[r] - cwl[r];
                 if (r != rank) {
-                    if (nr * wl > 0) SBG_NCCL(ncclSend(a2a_send_.p + off, (size_t)(nr * wl), ncclDouble, r, comm_->comm, s));
-                    if (nrows * rw > 0)
-                        SBG_NCCL(ncclRecv(a2a_recv_.p + roff, (size_t)(nrows * rw), ncclDouble, r, comm_->comm, s));
+                    if (nr * wl > 0) sends.push_back({a2a_send_.p + off, (size_t)(nr * wl), r});
+                    if (nrows * rw > 0) recvs.push_back({a2a_recv_.p + roff, (size_t)(nrows * rw), r});
                 } else if (nrows * rw > 0) {
                     SBG_CUDA(cudaMemcpyAsync(a2a_recv_.p + roff, a2a_send_.p + off, nrows * rw * 8,
                                              cudaMemcpyDeviceToDevice, s));
@@ -466,7 +542,7 @@ void Context::sigma(const double* x_local, double* y_local, cudaStream_t s) {
                 off += nr * wl;
                 roff += nrows * rw;
             }
-            SBG_NCCL(ncclGroupEnd());
+            comm_->exchange(sends, recvs, s);
             roff = 0;
             for (int r = 0; r < world; ++r) {
                 const int64_t rw = cwh[r] - cwl[r];

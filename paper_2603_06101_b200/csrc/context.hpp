@@ -16,6 +16,7 @@
 #include <string>
 #include <vector>
 
+#include "comm.hpp"
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -55,12 +56,11 @@ private:
     void release();
 };
 
-struct Comm;  // NCCL plumbing (dist.cu); null for a single GPU
 
 class Context {
 public:
     Context(int norb, int nelec, int ms2, double e_core, const double* h1, const double* eri, int device,
-            uint64_t max_det, int rank, int world, const void* nccl_id);
+            uint64_t max_det, int rank, int world, const void* nccl_id, LocalGroup* local_group = nullptr);
     ~Context();
 
     // sector

@@ -180,11 +180,14 @@ class FciOperator:
     """Matrix-free determinant CI Hamiltonian on the GPU (drop-in for sbci::fci::FciOperator)."""
 
     def __init__(self, prob: FciProblem, max_determinants: int = K_DEFAULT_DETERMINANT_GUARD, device: int = 0,
-                 rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
+                 rank: int = 0, world: int = 1, nccl_id: bytes | None = None, local_group=None):
         L = lib()
         self.problem = prob
         h = C.c_void_p()
-        if world == 1:
+        if local_group is not None:  # ranks as threads of this process (dist.LocalRankGroup)
+            rc = L.sbg_create_local(prob.norb, prob.nelec, prob.ms2, prob.e_core, _dp(prob.h1), _dp(prob.eri), device,
+                                    int(max_determinants), local_group.handle, rank, C.byref(h))
+        elif world == 1:
             rc = L.sbg_create(prob.norb, prob.nelec, prob.ms2, prob.e_core, _dp(prob.h1), _dp(prob.eri), device,
                               int(max_determinants), C.byref(h))
         else:

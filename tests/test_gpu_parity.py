@@ -398,3 +398,48 @@ def test_reference_drivers_run_on_gpu_sigma(dev, rest, gold_dir, name, method):
     assert np.abs(r["energies"] - np.array(g[key]["energies"])).max() <= E_TOL
     if method == 1:
         assert r["iterations"].tolist() == g[key]["iterations"] and r["matvecs"] == g[key]["matvecs"]
+
+
+# ---------------------------------------------------------------- sharded path
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_sigma_and_solves_match_single_rank(dev, rest, gold_dir, world):
+    """The alpha-block sharded operator (all-gather, alpha-alpha column-window exchange, all-reduced
+    dots) on the real kernels: ranks as threads of one process (dist.LocalRankGroup), compared with
+    the single-rank operator — sigma rows, and SBCI1 / SBCI2 / Davidson energies and trajectories."""
+    from paper_2603_06101_b200.dist import LocalRankGroup
+    q = baseline_problem(1, rest)                      # (10e,10o), 252 alpha strings
+    prob = to_product(q)
+    single = P.FciOperator(prob, max_determinants=2 ** 62)
+    x = np.random.default_rng(5).uniform(-1, 1, single.dim())
+    y1 = single.apply(x)
+    g = LocalRankGroup(world)
+    ops = g.operators(prob)
+    rows = [(op.row_lo, op.row_hi) for op in ops]
+    nb = single.n_beta_strings
+    assert rows[0][0] == 0 and rows[-1][1] == single.n_alpha_strings
+    ys = g.run(lambda r, op: op.apply(x), ops)
+    for (lo, hi), y in zip(rows, ys):
+        sl = slice(lo * nb, hi * nb)
+        assert np.abs(y[sl] - y1[sl]).max() <= 1e-12 * np.abs(y1).max()
+    s2 = g.run(lambda r, op: op.spin_squared(x), ops)
+    assert max(abs(v - single.spin_squared(x)) for v in s2) <= 1e-12 * abs(s2[0])
+    gold_c1 = gold(gold_dir, "c1")
+    for solve, key in ((P.solve_n_states_sbci1, "sbci1"), (P.solve_n_states_sbci2, "sbci2"), (P.davidson_solve, "davidson")):
+        res = g.run(lambda r, op: solve(op, 4), ops)
+        e = np.array([pp.energy for pp in res[0].pairs])
+        assert all(np.array_equal(e, np.array([pp.energy for pp in rr.pairs])) for rr in res)  # identical branches
+        assert np.abs(e - np.array(gold_c1[key]["energies"])).max() <= E_TOL
+        # vectors: each rank returns its rows; assembled they are unit and orthonormal
+        V = np.zeros((4, single.dim()))
+        for (lo, hi), rr in zip(rows, res):
+            for k, pp in enumerate(rr.pairs):
+                V[k, lo * nb:hi * nb] = pp.vector[lo * nb:hi * nb]
+        assert np.abs(V @ V.T - np.eye(4)).max() <= 1e-9
+        # the same trajectory as the reference (sharding only reorders the dot-product sums)
+        assert [pp.iterations for pp in res[0].pairs] == gold_c1[key]["iterations"]
+        assert res[0].summary.matvecs == gold_c1[key]["matvecs"]
+    for op in ops:
+        op.close()
+    g.close()
+    single.close()
