@@ -141,7 +141,8 @@ int sbg_table_sizes(const sbg_ctx* ctx, int spin, int64_t* n_strings, int64_t* r
 int sbg_string_tables(sbg_ctx* ctx, int spin, uint64_t* strings, sbg_excitation* links);
 
 /* sigma = H x for nvec vectors (host buffers, each n_det). Counts nvec applications
- * (SymmetricOperator::apply, operator.hpp:25-31). x and y may not alias. */
+ * (SymmetricOperator::apply, operator.hpp:25-31). x and y may not alias. nvec > 1 pipelines the
+ * uploads and downloads of neighbouring vectors behind the sigma builds (pinned buffers overlap). */
 int sbg_sigma(sbg_ctx* ctx, const double* x, double* y, int nvec);
 /* Same on dense device buffers (n_det each) on the given cudaStream_t (NULL = library stream).
  * Inputs already resident in HBM; used by the bench's device-resident leg. */

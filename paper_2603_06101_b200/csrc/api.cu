@@ -280,12 +280,48 @@ int sbg_sigma(sbg_ctx* ctx, const double* x, double* y, int nvec) {
         require_ctx(ctx);
         if (nvec < 0 || (!x && nvec) || (!y && nvec)) throw std::invalid_argument("sbg_sigma: bad arguments");
         auto& c = *ctx->c;
-        double *dx = c.io_x(), *dy = c.io_y();
-        for (int v = 0; v < nvec; ++v) {
-            c.upload_local(x + (size_t)v * c.ndet, dx, c.st);
+        if (nvec == 1) {
+            double *dx = c.io_x(), *dy = c.io_y();
+            c.upload_local(x, dx, c.st);
             c.sigma(dx, dy, c.st);
-            c.download_local(dy, y + (size_t)v * c.ndet + c.row_lo * c.NB, c.st);
+            c.download_local(dy, y + c.row_lo * c.NB, c.st);
+            SBG_CUDA(cudaStreamSynchronize(c.st));
+            return;
         }
+        // several vectors: a two-slot pipeline, H2D of vector v+1 and D2H of vector v-1 on their own
+        // copy streams while sigma(v) runs on the compute stream
+        cudaStream_t cin = c.copy_stream(0), cout = c.copy_stream(1);
+        std::vector<cudaEvent_t> up(nvec), done(nvec), down(nvec);
+        auto mk = [](cudaEvent_t& e) { SBG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)); };
+        struct Cleanup {
+            std::vector<cudaEvent_t>* v[3];
+            ~Cleanup() {
+                for (auto* l : v)
+                    for (auto e : *l)
+                        if (e) cudaEventDestroy(e);
+            }
+        } cleanup{{&up, &done, &down}};
+        for (int v = 0; v < nvec; ++v) {
+            mk(up[v]);
+            mk(done[v]);
+            mk(down[v]);
+        }
+        for (int v = 0; v < nvec; ++v) {
+            const int slot = v & 1;
+            double *dx = c.io_x(slot), *dy = c.io_y(slot);
+            if (v >= 2) SBG_CUDA(cudaStreamWaitEvent(cin, done[v - 2], 0));  // sigma(v-2) released dx
+            c.upload_local(x + (size_t)v * c.ndet, dx, cin);
+            SBG_CUDA(cudaEventRecord(up[v], cin));
+            SBG_CUDA(cudaStreamWaitEvent(c.st, up[v], 0));
+            if (v >= 2) SBG_CUDA(cudaStreamWaitEvent(c.st, down[v - 2], 0));  // D2H(v-2) released dy
+            c.sigma(dx, dy, c.st);
+            SBG_CUDA(cudaEventRecord(done[v], c.st));
+            SBG_CUDA(cudaStreamWaitEvent(cout, done[v], 0));
+            c.download_local(dy, y + (size_t)v * c.ndet + c.row_lo * c.NB, cout);
+            SBG_CUDA(cudaEventRecord(down[v], cout));
+        }
+        SBG_CUDA(cudaStreamSynchronize(cout));
+        SBG_CUDA(cudaStreamSynchronize(cin));
         SBG_CUDA(cudaStreamSynchronize(c.st));
     });
 }

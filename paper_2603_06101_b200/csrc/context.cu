@@ -238,12 +238,19 @@ Context::~Context() {
     comm_.reset();
     for (auto& es : ev_pool_)
         for (auto& e : es.e) cudaEventDestroy(e);
+    for (auto& c : cs_)
+        if (c) cudaStreamDestroy(c);
     if (ev0_) cudaEventDestroy(ev0_);
     if (ev1_) cudaEventDestroy(ev1_);
     if (st) cudaStreamDestroy(st);
 }
 
 DBuf Context::alloc_vec() const { return DBuf(padded_len()); }
+
+cudaStream_t Context::copy_stream(int which) {
+    if (!cs_[which]) SBG_CUDA(cudaStreamCreateWithFlags(&cs_[which], cudaStreamNonBlocking));
+    return cs_[which];
+}
 
 void Context::build_tables(const double* h1, const double* eri) {
     const size_t n2 = (size_t)norb * norb, n4 = n2 * n2;

@@ -76,14 +76,16 @@ public:
     // pooled zero-initialised padded local vector; the zero fill is ordered on st (solver work)
     DBuf vec() { return DBuf(*pool_, padded_len(), st); }
     // persistent staging vectors of the host-pointer entry points (sbg_sigma, sbg_sigma_device)
-    double* io_x() {
-        if (io_x_.empty()) io_x_ = alloc_vec();
-        return io_x_.p;
+    double* io_x(int slot = 0) {
+        if (io_x_[slot].empty()) io_x_[slot] = alloc_vec();
+        return io_x_[slot].p;
     }
-    double* io_y() {
-        if (io_y_.empty()) io_y_ = alloc_vec();
-        return io_y_.p;
+    double* io_y(int slot = 0) {
+        if (io_y_[slot].empty()) io_y_[slot] = alloc_vec();
+        return io_y_[slot].p;
     }
+    // host <-> device copy streams (0: H2D, 1: D2H) of the batched host-pointer entry points
+    cudaStream_t copy_stream(int which);
 
     // y = H x on padded local vectors (counts one application)
     void sigma(const double* x_local, double* y_local, cudaStream_t s);
@@ -133,7 +135,8 @@ private:
     uint16_t* d_sc_ent_ = nullptr;
     DBuf diag_;
     // sigma workspaces
-    DBuf xfull_, xT_, sT_, saa_, a2a_send_, a2a_recv_, io_x_, io_y_;
+    DBuf xfull_, xT_, sT_, saa_, a2a_send_, a2a_recv_, io_x_[2], io_y_[2];
+    cudaStream_t cs_[2] = {nullptr, nullptr};
     AbPlan ab_{};
     SsPlan ssa_{}, ssb_{};
     bool have_ab_ = false;

@@ -343,6 +343,20 @@ def test_operator_contract(dev, gold_dir):
     op.close()
 
 
+@pytest.mark.parametrize("idx", [1, 2])
+def test_batched_host_sigma_matches_single(dev, rest, idx):
+    """sbg_sigma with nvec > 1 (two-slot H2D / sigma / D2H pipeline) equals one call per vector."""
+    q = baseline_problem(idx, rest)
+    op = P.FciOperator(to_product(q), max_determinants=2 ** 62)
+    X = np.random.default_rng(9).uniform(-1, 1, (5, op.dim()))
+    Y = op.apply(X)
+    assert op.apply_count() == 5
+    for k in range(5):
+        yk = op.apply(X[k])
+        assert np.abs(Y[k] - yk).max() <= 1e-13 * np.abs(yk).max()
+    op.close()
+
+
 def test_kernel_launch_accounting(dev, rest):
     q = baseline_problem(1, rest)
     op = P.FciOperator(to_product(q), max_determinants=2 ** 62)
