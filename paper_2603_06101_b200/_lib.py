@@ -6,7 +6,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsbg.so")
+LIB_PATH = os.environ.get("SBG_LIB_PATH", os.path.join(_HERE, "libsbg.so"))  # override: A/B builds
 
 SBG_OK, SBG_EINVAL, SBG_ENONCONV, SBG_EDEVICE, SBG_ERUNTIME = 0, 1, 2, 3, 4
 SBG_MAX_ROOTS = 64

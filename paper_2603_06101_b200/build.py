@@ -16,8 +16,10 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(ROOT, "build", "sbg")
-LIB = os.path.join(PKG, "libsbg.so")
+# developer knobs for A/B builds: SBG_NVCC_FLAGS (extra nvcc flags), SBG_LIB_OUT (library path)
+EXTRA = os.environ.get("SBG_NVCC_FLAGS", "").split()
+LIB = os.environ.get("SBG_LIB_OUT", os.path.join(PKG, "libsbg.so"))
+OBJ = os.path.join(ROOT, "build", "sbg" if not EXTRA else "sbg_" + str(abs(hash(" ".join(EXTRA)))))
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
@@ -35,7 +37,7 @@ def nvcc():
 
 def _compile(src, ptxas_verbose):
     out = os.path.join(OBJ, src.replace(".cu", ".o"))
-    cmd = [nvcc(), *ARCH, *FLAGS, *PER_FILE.get(src, []), "-dc" if False else "-c", os.path.join(CSRC, src), "-o", out]
+    cmd = [nvcc(), *ARCH, *FLAGS, *EXTRA, *PER_FILE.get(src, []), "-c", os.path.join(CSRC, src), "-o", out]
     if ptxas_verbose:
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)

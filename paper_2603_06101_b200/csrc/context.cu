@@ -232,7 +232,7 @@ Context::~Context() {
     if (st) cudaStreamSynchronize(st);
     for (void* p : {(void*)d_sa_, (void*)d_sb_, (void*)d_la_, (void*)d_lb_, (void*)d_h1_, (void*)d_eri_, (void*)d_Vp_,
                     (void*)d_Va_, (void*)d_codes_, (void*)d_sc_tgt_, (void*)d_sc_ent_,
-                    (void*)d_sc_tt_, (void*)d_sc_te_, (void*)rws.partial, (void*)rws.result})
+                    (void*)d_sc_tt_, (void*)d_sc_te_, (void*)d_red_ent_, (void*)d_red_te_, (void*)rws.partial, (void*)rws.result})
         if (p) cudaFree(p);
     if (rws.host) cudaFreeHost(rws.host);
     comm_.reset();
@@ -313,6 +313,15 @@ void Context::build_tables(const double* h1, const double* eri) {
         SBG_CUDA(cudaMemcpyAsync(d_sc_ent_, ent.data(), ent.size() * 2, cudaMemcpyHostToDevice, st));
         SBG_CUDA(cudaMemcpyAsync(d_sc_tt_, tt.data(), tt.size() * 4, cudaMemcpyHostToDevice, st));
         SBG_CUDA(cudaMemcpyAsync(d_sc_te_, te.data(), te.size() * 4, cudaMemcpyHostToDevice, st));
+        if (ab_.red) {
+            std::vector<uint32_t> e32, t32;
+            build_ab_red_list(ab_, codes, e32, t32);
+            d_red_ent_ = dmalloc<uint32_t>(e32.size());
+            d_red_te_ = dmalloc<uint32_t>(t32.size());
+            SBG_CUDA(cudaMemcpyAsync(d_red_ent_, e32.data(), e32.size() * 4, cudaMemcpyHostToDevice, st));
+            SBG_CUDA(cudaMemcpyAsync(d_red_te_, t32.data(), t32.size() * 4, cudaMemcpyHostToDevice, st));
+            SBG_CUDA(cudaStreamSynchronize(st));
+        }
         SBG_CUDA(cudaStreamSynchronize(st));
     }
     // same-spin antisymmetrized pair integrals W(pr,qs) = (pq|rs) - (ps|rq), p<r, q<s
@@ -570,7 +579,7 @@ void Context::sigma(const double* x_local, double* y_local, cudaStream_t s) {
     }
     // ---- alpha-beta (+ one-body folded, + e_core)
     if (have_ab_) {
-        launch_sigma_ab(ab_, AbScatter{d_sc_tgt_, d_sc_ent_, d_sc_tt_, d_sc_te_}, xf, y_local, d_Vp_, row_lo, row_hi,
+        launch_sigma_ab(ab_, AbScatter{d_sc_tgt_, d_sc_ent_, d_sc_tt_, d_sc_te_, d_red_ent_, d_red_te_}, xf, y_local, d_Vp_, row_lo, row_hi,
                         e_core, 1, nsm, s);
         launches += 1;
     } else {

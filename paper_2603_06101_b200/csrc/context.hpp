@@ -132,6 +132,7 @@ private:
     double *d_h1_ = nullptr, *d_eri_ = nullptr, *d_Vp_ = nullptr, *d_Va_ = nullptr, *d_Vb_ = nullptr;
     uint16_t* d_codes_ = nullptr;
     uint32_t *d_sc_tgt_ = nullptr, *d_sc_tt_ = nullptr, *d_sc_te_ = nullptr;
+    uint32_t *d_red_ent_ = nullptr, *d_red_te_ = nullptr;
     uint16_t* d_sc_ent_ = nullptr;
     DBuf diag_;
     // sigma workspaces

@@ -27,7 +27,7 @@ void launch_scatter_codes(const uint64_t* sb, int64_t nb, int64_t ld, int norb, 
 
 // ---- sigma_ab.cu: opposite-spin term (+ folded one-body, + e_core), K6 ----
 struct AbPlan {
-    int norb, na_el, nb_el, npair, npad, mb16, extra, K, KS, threads, maxT, maxE, nt;
+    int norb, na_el, nb_el, npair, npad, mb16, extra, K, KS, threads, maxT, maxE, nt, ws, red;
     int64_t NA, NB, ld;
     size_t smem;
 };
@@ -36,10 +36,14 @@ struct AbScatter {  // device pointers of the per-tile segment lists (build_ab_s
     const uint16_t* ent;
     const uint32_t* tile_tgt;
     const uint32_t* tile_ent;
+    const uint32_t* ent32;       // red mode (build_ab_red_list)
+    const uint32_t* tile_ent32;
 };
 AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int64_t ld, int nsm);
 void build_ab_scatter(const AbPlan& pl, const std::vector<uint16_t>& codes, std::vector<uint32_t>& tgt,
                       std::vector<uint16_t>& ent, std::vector<uint32_t>& tile_tgt, std::vector<uint32_t>& tile_ent);
+void build_ab_red_list(const AbPlan& pl, const std::vector<uint16_t>& codes, std::vector<uint32_t>& ent,
+                       std::vector<uint32_t>& tile_ent);
 void launch_sigma_ab(const AbPlan& pl, const AbScatter& sc, const double* x_full, double* y_local, const double* Vp,
                      int64_t row_lo, int64_t row_hi, double e_core, int accumulate, int grid, cudaStream_t st);
 

@@ -49,6 +49,9 @@ struct AbParams {
     double e_core;
     int accumulate;
     int dbg;  // profiling experiments only: 1 = skip scatter, 2 = skip MMA
+    int red;  // k_sigma_ab_ws: 1 = scatter by red.global.add into y (no sigma row in shared memory)
+    const uint32_t* ent32;      // red mode, per tile: target << 16 | negative << 15 | G offset
+    const uint32_t* tile_ent32; // [ntiles+1] offsets into ent32 (multiples of 4)
 };
 
 // Software pipeline per alpha row, one __syncthreads per tile: iteration `it` prefetches D(it+1)
@@ -262,15 +265,289 @@ __global__ void __launch_bounds__(256, 1) k_sigma_ab(const AbParams p) {
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Warp-specialized variant: 16 warps. Warps 0-7 (two warpgroups, 2 per SM sub-partition) only run
+// the DMMA GEMM; warps 8-15 load (cp.async) and scatter. setmaxnreg moves registers to the MMA
+// warpgroups (A fragments stay resident), named barriers hand tiles over:
+//   DREADY[b]  loaders -> MMA   D(it) has landed in stage b
+//   FULL[b]    MMA -> scatter   G(it) is staged in buffer b
+//   EMPTY[b]   scatter -> MMA   G buffer b may be overwritten (tile it+2)
+// so tile it's scatter overlaps tile it+1's DMMAs on other warps of the same sub-partition.
+__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+constexpr int kWsThreads = 512, kWsHalf = 256;
+// register split between the MMA and the loader/scatter warpgroups (sum 256: 256 threads each)
+#ifndef SBG_WS_MREG
+#define SBG_WS_MREG 200
+#endif
+#define SBG_WS_SREG (256 - SBG_WS_MREG)
+#define SBG_STR2(x) #x
+#define SBG_STR(x) SBG_STR2(x)
+#ifndef SBG_WSU
+#define SBG_WSU 2
+#endif
+constexpr int WSU = SBG_WSU;
+constexpr int BAR_DREADY = 1, BAR_FULL = 3, BAR_EMPTY = 5, BAR_SINT = 7, BAR_MINT = 8, BAR_KLIST = 9;
+
+template <int KS, int NT>
+__global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p) {
+    constexpr int NBT = Tile<NT>::NBT, DSTRIDE = Tile<NT>::DSTRIDE, GSTRIDE = Tile<NT>::GSTRIDE;
+    extern __shared__ __align__(16) double smem[];
+    const int KP = KS * 4;
+    const int ntiles = (int)(p.ld / NT);
+    double* srow = smem;                     // [ld], absent in red mode
+    double* Ds = srow + (p.red ? 0 : p.ld);
+    double* sAe = Ds + STAGES * KP * DSTRIDE;
+    double* Gs = sAe + KP * 8;
+    uint32_t* Lt = reinterpret_cast<uint32_t*>(Gs + STAGES * p.grows * GSTRIDE);
+    uint16_t* Le = reinterpret_cast<uint16_t*>(Lt + STAGES * p.maxT);   // red mode: u32 entries
+    uint32_t* sTT = reinterpret_cast<uint32_t*>(Le + STAGES * p.maxE);
+    uint32_t* sTE = sTT + ntiles + 1;
+    int* sJ = reinterpret_cast<int*>(sTE + ntiles + 1);
+    int* sPair = sJ + KP;
+    double* sSign = reinterpret_cast<double*>(sPair + KP);
+
+    const int tid = threadIdx.x;
+    const int w = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    const int norb = p.norb, npair = p.npair;
+    // the two roles never rejoin, so ptxas can give each its own register budget
+    if (w < 8) {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 " SBG_STR(SBG_WS_MREG) ";\n");
+        const bool main_ok = w < p.mb16;
+        const bool do_extra = p.extra && w < NBT;
+        for (int64_t ia = p.row_lo + blockIdx.x; ia < p.row_hi; ia += gridDim.x) {
+            bar_sync(0, kWsThreads);           // row start
+            bar_sync(BAR_KLIST, kWsThreads);   // K-list of row ia ready (built by the loader warps)
+            const uint64_t sa = string_unrank((uint64_t)ia, p.na_el, norb);
+            auto aval = [&](int rs, int k) -> double {
+                if (rs >= npair || k >= p.K) return 0.0;
+                const int pr = sPair[k];
+                if (pr == -1) {
+                    double s = 0.0;
+                    for (uint64_t m = sa; m; m &= m - 1) {
+                        const int q = __ffsll((long long)m) - 1;
+                        s += p.Vp[(size_t)pair_sym(q, q) * npair + rs];
+                    }
+                    return s;
+                }
+                return sSign[k] * p.Vp[(size_t)pr * npair + rs];
+            };
+            double a0[KS], a1[KS];
+            const int r0 = 16 * w + g, re = 16 * p.mb16;
+#pragma unroll
+            for (int j = 0; j < KS; ++j) {
+                const int k = 4 * j + t;
+                a0[j] = main_ok ? aval(r0, k) : 0.0;
+                a1[j] = main_ok ? aval(r0 + 8, k) : 0.0;
+            }
+            if (p.extra)
+                for (int i = tid; i < KP * 8; i += kWsHalf) sAe[i] = aval(re + (i & 7), i >> 3);
+            bar_sync(BAR_MINT, kWsHalf);
+            for (int it = 0; it < ntiles; ++it) {
+                const int b = it & 1;
+                bar_sync(BAR_DREADY + b, kWsThreads);
+                if (it >= 2) bar_sync(BAR_EMPTY + b, kWsThreads);
+                if (!(p.dbg & 2) && main_ok) {
+                    const double* D = Ds + b * KP * DSTRIDE;
+                    double* G = Gs + b * p.grows * GSTRIDE;
+                    double acc[NBT][4];
+                    double ace0[2] = {0.0, 0.0}, ace1[2] = {0.0, 0.0};
+#pragma unroll
+                    for (int nb = 0; nb < NBT; ++nb)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) acc[nb][e] = 0.0;
+                    double bf[2][NBT];
+#pragma unroll
+                    for (int nb = 0; nb < NBT; ++nb) bf[0][nb] = D[t * DSTRIDE + g + nb * 8];
+#pragma unroll
+                    for (int j = 0; j < KS; ++j) {
+                        const int cur = j & 1;
+                        if (j + 1 < KS) {
+#pragma unroll
+                            for (int nb = 0; nb < NBT; ++nb) bf[cur ^ 1][nb] = D[(4 * (j + 1) + t) * DSTRIDE + g + nb * 8];
+                        }
+#pragma unroll
+                        for (int nb = 0; nb < NBT; ++nb) dmma_16x8x4(acc[nb], a0[j], a1[j], bf[cur][nb]);
+                        if (do_extra) {
+                            const double ae = sAe[(4 * j + t) * 8 + g];
+                            const double be = D[(4 * j + t) * DSTRIDE + g + w * 8];
+                            if (cur) dmma_8x8x4(ace1, ae, be);
+                            else dmma_8x8x4(ace0, ae, be);
+                        }
+                    }
+#pragma unroll
+                    for (int nb = 0; nb < NBT; ++nb) {
+                        const int col = nb * 8 + 2 * t;
+                        G[r0 * GSTRIDE + col] = acc[nb][0];
+                        G[r0 * GSTRIDE + col + 1] = acc[nb][1];
+                        G[(r0 + 8) * GSTRIDE + col] = acc[nb][2];
+                        G[(r0 + 8) * GSTRIDE + col + 1] = acc[nb][3];
+                    }
+                    if (do_extra) {
+                        G[(re + g) * GSTRIDE + w * 8 + 2 * t] = ace0[0] + ace1[0];
+                        G[(re + g) * GSTRIDE + w * 8 + 2 * t + 1] = ace0[1] + ace1[1];
+                    }
+                }
+                bar_arrive(BAR_FULL + b, kWsThreads);
+            }
+            for (int it = ntiles - 2 < 0 ? 0 : ntiles - 2; it < ntiles; ++it) bar_sync(BAR_EMPTY + (it & 1), kWsThreads);
+        }
+    } else {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 " SBG_STR(SBG_WS_SREG) ";\n");
+        const int stid = tid - kWsHalf;
+        for (int i = stid; i <= ntiles; i += kWsHalf) {
+            sTT[i] = p.red ? 0u : p.tile_tgt[i];
+            sTE[i] = p.red ? p.tile_ent32[i] : p.tile_ent[i];
+        }
+        for (int64_t ia = p.row_lo + blockIdx.x; ia < p.row_hi; ia += gridDim.x) {
+            bar_sync(0, kWsThreads);  // row start: the MMA warps are done with the previous K-list
+            const uint64_t sa = string_unrank((uint64_t)ia, p.na_el, norb);
+            for (int k = stid; k < KP; k += kWsHalf) {  // K-list (as in k_sigma_ab)
+                int J = (int)ia, pr = -2;
+                double sg = 0.0;
+                if (k == 0) {
+                    pr = -1;
+                    sg = 1.0;
+                } else if (k < p.K) {
+                    const int nv = norb - p.na_el;
+                    const int qi = (k - 1) / nv, pi = (k - 1) % nv;
+                    uint64_t m = sa;
+                    for (int i = 0; i < qi; ++i) m &= m - 1;
+                    const int q = __ffsll((long long)m) - 1;
+                    uint64_t v = ~sa & (((uint64_t)1 << norb) - 1);
+                    for (int i = 0; i < pi; ++i) v &= v - 1;
+                    const int pp = __ffsll((long long)v) - 1;
+                    const uint64_t rem = sa ^ ((uint64_t)1 << q);
+                    J = (int)string_rank(rem | ((uint64_t)1 << pp));
+                    sg = ((pop_below(sa, q) + pop_below(rem, pp)) & 1) ? -1.0 : 1.0;
+                    pr = pair_sym(pp, q);
+                }
+                sJ[k] = J;
+                sPair[k] = pr;
+                sSign[k] = sg;
+            }
+            if (!p.red)
+                for (int64_t c = stid; c < p.ld; c += kWsHalf) srow[c] = 0.0;
+            bar_sync(BAR_SINT, kWsHalf);       // sJ visible to every loader
+            bar_arrive(BAR_KLIST, kWsThreads);
+            auto load_d = [&](int stage, int jt) {
+                double* dst = Ds + stage * KP * DSTRIDE;
+                for (int c = stid; c < KP * (NT / 2); c += kWsHalf) {
+                    const int k = c / (NT / 2), part = c % (NT / 2);
+                    cp_async16(dst + k * DSTRIDE + part * 2, p.x + (int64_t)sJ[k] * p.ld + (int64_t)jt * NT + part * 2);
+                }
+            };
+            auto load_lists = [&](int stage, int jt) {
+                if (p.red) {
+                    const uint32_t e0 = sTE[jt], ne4 = (sTE[jt + 1] - e0) / 4;
+                    uint32_t* dst = reinterpret_cast<uint32_t*>(Le + stage * p.maxE);
+                    for (uint32_t c = stid; c < ne4; c += kWsHalf) cp_async16(dst + 4 * c, p.ent32 + e0 + 4 * c);
+                    return;
+                }
+                const uint32_t t0 = sTT[jt], nt4 = (sTT[jt + 1] - t0 + 3) / 4;
+                const uint32_t e0 = sTE[jt], ne8 = (sTE[jt + 1] - e0 + 7) / 8;
+                for (uint32_t c = stid; c < nt4; c += kWsHalf) cp_async16(Lt + stage * p.maxT + 4 * c, p.tgt + t0 + 4 * c);
+                for (uint32_t c = stid; c < ne8; c += kWsHalf) cp_async16(Le + stage * p.maxE + 8 * c, p.ent + e0 + 8 * c);
+            };
+            double* yrow = p.y + (ia - p.row_lo) * p.ld;
+            // prologue: tiles 0 and 1
+            for (int jt = 0; jt < 2 && jt < ntiles; ++jt) {
+                load_d(jt, jt);
+                load_lists(jt, jt);
+            }
+            cp_async_commit();
+            cp_async_wait<0>();
+            bar_sync(BAR_SINT, kWsHalf);
+            for (int jt = 0; jt < 2 && jt < ntiles; ++jt) bar_arrive(BAR_DREADY + jt, kWsThreads);
+            // steady state: tile it's scatter runs while the MMA warps work on tile it+1; D(it+2)
+            // streams in meanwhile and is released to them as soon as the scatter is done
+            for (int it = 0; it < ntiles; ++it) {
+                const int b = it & 1;
+                bar_sync(BAR_FULL + b, kWsThreads);   // G(it) staged; D stage b free
+                if (it + 2 < ntiles) load_d(b, it + 2);
+                cp_async_commit();
+                if (p.red && !(p.dbg & 1)) {  // one reduction into y per (rs, column) entry
+                    const double* G = Gs + b * p.grows * GSTRIDE;
+                    const uint32_t* l32 = reinterpret_cast<const uint32_t*>(Le + b * p.maxE);
+                    const uint32_t n = sTE[it + 1] - sTE[it];
+                    for (uint32_t i = stid; i < n; i += kWsHalf) {
+                        const uint32_t en = l32[i];
+                        if (en == 0xFFFFFFFFu) continue;  // 16-byte padding
+                        const long long bits = __double_as_longlong(G[en & 0x7FFFu]) ^ ((long long)(en & 0x8000u) << 48);
+                        red_add_f64(yrow + (en >> 16), __longlong_as_double(bits));
+                    }
+                } else if (!(p.dbg & 1)) {
+                    const double* G = Gs + b * p.grows * GSTRIDE;
+                    const uint32_t* lt = Lt + b * p.maxT;
+                    const uint16_t* le = Le + b * p.maxE;
+                    const uint32_t nt = sTT[it + 1] - sTT[it];
+                    auto signed_g = [&](uint32_t e) {
+                        const uint16_t en = le[e];
+                        const long long bits = __double_as_longlong(G[en & 0x7FFF]);
+                        return __longlong_as_double(bits ^ ((long long)(en & 0x8000) << 48));
+                    };
+                    // WSU targets per thread in flight (independent smem chains)
+                    for (uint32_t i0 = stid; i0 < nt; i0 += WSU * kWsHalf) {
+                        uint32_t tg[WSU], beg[WSU], end[WSU];
+                        double v[WSU];
+#pragma unroll
+                        for (int u = 0; u < WSU; ++u) {
+                            const uint32_t i = i0 + u * kWsHalf;
+                            tg[u] = i < nt ? lt[i] : 0u;
+                            beg[u] = (i == 0 || i >= nt) ? 0u : (lt[i - 1] & 0xFFFFu);
+                            end[u] = tg[u] & 0xFFFFu;
+                        }
+#pragma unroll
+                        for (int u = 0; u < WSU; ++u) v[u] = end[u] > beg[u] ? signed_g(beg[u]) : 0.0;
+#pragma unroll
+                        for (int u = 0; u < WSU; ++u)
+                            for (uint32_t e = beg[u] + 1; e < end[u]; ++e) v[u] += signed_g(e);
+#pragma unroll
+                        for (int u = 0; u < WSU; ++u)  // padding segments (end <= beg) write nothing
+                            if (end[u] > beg[u]) srow[tg[u] >> 16] += v[u];
+                    }
+                }
+                bar_arrive(BAR_EMPTY + b, kWsThreads);
+                cp_async_wait<0>();                    // D(it+2) (and lists(it+1)) landed
+                bar_sync(BAR_SINT, kWsHalf);           // ... for every loader; lists stage b free
+                if (it + 2 < ntiles) {
+                    bar_arrive(BAR_DREADY + b, kWsThreads);
+                    load_lists(b, it + 2);
+                }
+                cp_async_commit();
+            }
+            cp_async_wait<0>();
+            const double* xr = p.x + ia * p.ld;
+            if (p.red) {  // y already accumulates the reductions; add e_core * x the same way
+                if (p.e_core != 0.0)
+                    for (int64_t c = stid; c < p.NB; c += kWsHalf) red_add_f64(yrow + c, p.e_core * xr[c]);
+                continue;
+            }
+            // ---- write the row: y = [y] + sigma_ab + e_core * x (srow complete after the barrier)
+            double* yr = yrow;
+            for (int64_t c = stid; c < p.ld; c += kWsHalf) {
+                double v = 0.0;
+                if (c < p.NB) {
+                    v = srow[c] + p.e_core * xr[c];
+                    if (p.accumulate) v += yr[c];
+                }
+                yr[c] = v;
+            }
+        }
+    }
+}
+
 template <int KS, int NT>
 void launch_ks(const AbPlan& pl, const AbParams& prm, int grid, cudaStream_t st) {
-    auto kern = k_sigma_ab<KS, NT>;
-    static int configured[64] = {0};
+    auto kern = pl.ws ? k_sigma_ab_ws<KS, NT> : k_sigma_ab<KS, NT>;
+    static int configured[2][64] = {{0}};
     int dev = 0;
     cudaGetDevice(&dev);
-    if (dev < 64 && !configured[dev]) {
+    if (dev < 64 && !configured[pl.ws][dev]) {
         SBG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        configured[dev] = 1;
+        configured[pl.ws][dev] = 1;
     }
     kern<<<grid, pl.threads, pl.smem, st>>>(prm);
     SBG_LAUNCH_CHECK();
@@ -310,17 +587,34 @@ AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int
         // scatter-list buffers: bounded by the tile's valid (rs, column) entries
         pl.maxT = 4 * ((nt * (1 + nb_el * (norb - nb_el)) + 3) / 4);
         pl.maxE = 8 * ((nt * (nb_el + nb_el * (norb - nb_el)) + 7) / 8);
+        if (pl.red) {  // one u32 per entry (maxE counts u16 slots), no target lists, no sigma row
+            pl.maxT = 0;
+            pl.maxE = 2 * 4 * ((nt * (nb_el + nb_el * (norb - nb_el)) + 3) / 4);
+        }
         const int64_t ntiles = ld / nt;
-        pl.smem = (size_t)ld * 8 + (size_t)STAGES * KP * (nt + 4) * 8 + (size_t)KP * 8 * 8 +
+        pl.smem = (size_t)(pl.red ? 0 : ld) * 8 + (size_t)STAGES * KP * (nt + 4) * 8 + (size_t)KP * 8 * 8 +
                   (size_t)STAGES * pl.npad * (nt + 1) * 8 + (size_t)STAGES * (pl.maxT * 4 + pl.maxE * 2) +
                   (size_t)(ntiles + 1) * 8 + (size_t)KP * 16 + 16;
     };
-    configure(32);
-    if (pl.smem > 227 * 1024) configure(16);
+    // default: k_sigma_ab_ws with reductions into y (SBG_AB_RED=0 selects the shared-memory sigma
+    // row with the target-sorted segment scatter, SBG_AB_WS then picks its warp-specialized form)
+    const char* red_env = getenv("SBG_AB_RED");
+    pl.red = red_env ? (atoi(red_env) != 0) : 1;
+    const char* nt_env = getenv("SBG_AB_NT");
+    const int nt_force = nt_env ? atoi(nt_env) : 0;
+    if (nt_force == 16 || nt_force == 32) configure(nt_force);
+    else {
+        configure(32);
+        if (pl.smem > 227 * 1024) configure(16);
+    }
     if (NB > 32767) throw InvalidArgument("sigma_ab: more than 32767 beta strings is not supported by this build");
     if ((size_t)pl.npad * (pl.nt + 1) >= 32768) throw InvalidArgument("sigma_ab: pair space too large for this build");
     if (pl.smem > 227 * 1024) throw InvalidArgument("sigma_ab: beta row does not fit in shared memory");
     if (pl.KS > 24 || pl.threads > 256) throw InvalidArgument("sigma_ab: orbital space too large for this build");
+    // warp-specialized kernel (k_sigma_ab_ws): 8 MMA warps + 8 load/scatter warps
+    const char* ws_env = getenv("SBG_AB_WS");
+    pl.ws = (ws_env ? (atoi(ws_env) != 0) : 0) || pl.red;
+    if (pl.ws) pl.threads = kWsThreads;
     return pl;
 }
 
@@ -362,6 +656,32 @@ void build_ab_scatter(const AbPlan& pl, const std::vector<uint16_t>& codes, std:
     tile_ent[ntiles] = (uint32_t)ent.size();
 }
 
+// red mode: per tile every (rs, column) entry as target << 16 | negative << 15 | G offset, in
+// target order (neighbouring lanes reduce into neighbouring y elements), padded to 4 entries
+void build_ab_red_list(const AbPlan& pl, const std::vector<uint16_t>& codes, std::vector<uint32_t>& ent,
+                       std::vector<uint32_t>& tile_ent) {
+    const int NT = pl.nt, GSTRIDE = pl.nt + 1;
+    const int64_t ntiles = pl.ld / NT;
+    ent.clear();
+    tile_ent.assign(ntiles + 1, 0);
+    std::vector<std::pair<uint32_t, uint32_t>> items;
+    for (int64_t jt = 0; jt < ntiles; ++jt) {
+        items.clear();
+        for (int rs = 0; rs < pl.npad; ++rs)
+            for (int c = 0; c < NT; ++c) {
+                const uint16_t code = codes[(size_t)(jt * NT + c) * pl.npad + rs];
+                if (code == 0xFFFF) continue;
+                items.push_back({(uint32_t)(code & 0x7FFF), (uint32_t)((rs * GSTRIDE + c) | (code & 0x8000))});
+            }
+        std::stable_sort(items.begin(), items.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+        tile_ent[jt] = (uint32_t)ent.size();
+        for (auto& it : items) ent.push_back((it.first << 16) | it.second);
+        while (ent.size() % 4) ent.push_back(0xFFFFFFFFu);
+        if ((int64_t)(ent.size() - tile_ent[jt]) * 2 > pl.maxE) throw InvalidArgument("sigma_ab: red list overflow");
+    }
+    tile_ent[ntiles] = (uint32_t)ent.size();
+}
+
 void launch_sigma_ab(const AbPlan& pl, const AbScatter& sc, const double* x_full, double* y_local, const double* Vp,
                      int64_t row_lo, int64_t row_hi, double e_core, int accumulate, int grid, cudaStream_t st) {
     ensure_binomials();
@@ -374,6 +694,10 @@ void launch_sigma_ab(const AbPlan& pl, const AbScatter& sc, const double* x_full
     prm.ent = sc.ent;
     prm.tile_tgt = sc.tile_tgt;
     prm.tile_ent = sc.tile_ent;
+    prm.red = pl.red;
+    prm.ent32 = sc.ent32;
+    prm.tile_ent32 = sc.tile_ent32;
+    if (pl.red && !accumulate) throw InvalidArgument("sigma_ab: reduction mode needs an initialised y");
     prm.norb = pl.norb;
     prm.na_el = pl.na_el;
     prm.npair = pl.npair;
