@@ -23,7 +23,7 @@ namespace {
 constexpr int NTS = 32;         // batch columns per tile (one warp-wide reduction segment)
 constexpr int XSTRIDE = NTS + 4;
 constexpr int YSTRIDE = NTS + 4;
-constexpr int TILES_PER_CTA = 8;
+constexpr int kMaxTilesPerCta = 32;  // column tiles per CTA: amortizes the per-K setup (pair list, A)
 
 struct SsParams {
     const double* x;
@@ -31,6 +31,7 @@ struct SsParams {
     const double* Va;
     int norb, nel, P, npa;
     int64_t ldx, col_lo, col_hi;
+    int tpc;  // column tiles per CTA
 };
 
 template <int KSS>
@@ -94,8 +95,8 @@ __global__ void __launch_bounds__(128, 4) k_sigma_ss(const SsParams p) {
 
     // column tiles of this CTA, X tiles double-buffered with cp.async (tile tt+1 lands while the
     // DMMAs of tile tt run); Ys is a separate staging tile for the coalesced reductions
-    const int64_t c_begin = p.col_lo + (int64_t)blockIdx.y * TILES_PER_CTA * NTS;
-    const int ntt = (int)std::min<int64_t>(TILES_PER_CTA, (p.col_hi - c_begin + NTS - 1) / NTS);
+    const int64_t c_begin = p.col_lo + (int64_t)blockIdx.y * p.tpc * NTS;
+    const int ntt = (int)std::min<int64_t>(p.tpc, (p.col_hi - c_begin + NTS - 1) / NTS);
     auto load = [&](int tt) {
         const int64_t c0 = c_begin + (int64_t)tt * NTS;
         double* dst = Xs + (tt & 1) * KPP * XSTRIDE;
@@ -229,9 +230,15 @@ void launch_sigma_ss(const SsPlan& pl, const double* x, double* y, const double*
                      int64_t col_hi, cudaStream_t st) {
     ensure_binomials();
     if (pl.P == 0 || pl.NK == 0 || col_hi <= col_lo) return;
-    SsParams prm{x, y, Va, pl.norb, pl.nel, pl.P, pl.npa, ldx, col_lo, col_hi};
-    const int64_t ncols = col_hi - col_lo;
-    const int64_t gy = (ncols + TILES_PER_CTA * NTS - 1) / (TILES_PER_CTA * NTS);
+    const int64_t ncols = col_hi - col_lo, ntiles = (ncols + NTS - 1) / NTS;
+    // as many tiles per CTA as keep >= 8 CTAs per SM in flight
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    int tpc = kMaxTilesPerCta;
+    while (tpc > 4 && pl.NK * ((ntiles + tpc - 1) / tpc) < 8LL * nsm) tpc /= 2;
+    SsParams prm{x, y, Va, pl.norb, pl.nel, pl.P, pl.npa, ldx, col_lo, col_hi, tpc};
+    const int64_t gy = (ntiles + tpc - 1) / tpc;
     dim3 grid((unsigned)pl.NK, (unsigned)gy);
     switch (pl.KSS) {
 #define SBG_KSS(n) \

@@ -263,7 +263,8 @@ def test_sbci2_one_root_routes_to_sbci1(dev, gold_dir):
     r1 = P.solve_n_states_sbci1(op, 1)
     r2 = P.solve_n_states_sbci2(op, 1)
     assert r2.summary.method == "sbci2"
-    assert r1.pairs[0].energy == r2.pairs[0].energy and r1.summary.matvecs == r2.summary.matvecs
+    # sigma reduces in L2 (red.global.add): runs agree to rounding, not bit for bit
+    assert abs(r1.pairs[0].energy - r2.pairs[0].energy) <= 1e-12 and r1.summary.matvecs == r2.summary.matvecs
     op.close()
 
 
