@@ -172,6 +172,7 @@ def time_to_energy(full=False):
         rec = {"nroots": nroots}
         energies = {}
         for m in methods:
+            solvers[m](op, nroots, want_vectors=False)    # warm-up: lazy module loading of its kernels
             t0 = time.perf_counter()
             res = solvers[m](op, nroots, want_vectors=False)
             wall = time.perf_counter() - t0
