@@ -44,6 +44,7 @@ __global__ void __launch_bounds__(128, 4) k_sigma_ss(const SsParams p) {
     int* sJ = reinterpret_cast<int*>(Ys + ysrows * YSTRIDE);
     int* sPi = sJ + KPP;
     double* sPhi = reinterpret_cast<double*>(sPi + KPP);
+    int64_t* sRow = reinterpret_cast<int64_t*>(sPhi + KPP);  // row offsets sJ[i] * ldx
 
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int w = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
@@ -80,8 +81,10 @@ __global__ void __launch_bounds__(128, 4) k_sigma_ss(const SsParams p) {
     }
     __syncthreads();
     if (sJ[0] < 0) return;  // no pairs (cannot happen for P >= 1)
-    for (int i = tid; i < KPP; i += nthr)
+    for (int i = tid; i < KPP; i += nthr) {
         if (i >= P) sJ[i] = sJ[0];  // padding rows read a valid row; their A entries are zero
+        sRow[i] = (int64_t)sJ[i] * p.ldx;
+    }
 
     double a0[KSS], a1[KSS];
     const int i0 = 16 * w + g;
@@ -137,9 +140,13 @@ __global__ void __launch_bounds__(128, 4) k_sigma_ss(const SsParams p) {
         }
         __syncthreads();
         // one warp reduces one 32-column row segment per step: coalesced 256-byte reductions
-        if (c0 + lane < p.col_hi)
-            for (int i = w; i < P; i += nthr >> 5)
-                red_add_f64(p.y + (int64_t)sJ[i] * p.ldx + c0 + lane, Ys[i * YSTRIDE + lane]);
+        if (c0 + lane < p.col_hi) {
+            double* ybase = p.y + c0 + lane;
+            const double* yl = Ys + lane;
+            const int nw = nthr >> 5;
+#pragma unroll 4
+            for (int i = w; i < P; i += nw) red_add_f64(ybase + sRow[i], yl[i * YSTRIDE]);
+        }
     }
     cp_async_wait<0>();
 }
@@ -221,7 +228,7 @@ SsPlan plan_sigma_ss(int norb, int nel) {
     pl.warps = (pl.P + 15) / 16;
     const int KPP = pl.KSS * 4;
     const int rows = std::max(KPP, 16 * pl.warps);
-    pl.smem = (size_t)(2 * KPP * XSTRIDE + rows * YSTRIDE) * 8 + (size_t)KPP * 8 + (size_t)KPP * 8 + 16;
+    pl.smem = (size_t)(2 * KPP * XSTRIDE + rows * YSTRIDE) * 8 + (size_t)KPP * 8 + (size_t)KPP * 8 + (size_t)KPP * 8 + 16;
     if (pl.KSS > 16 || pl.warps > 4) throw InvalidArgument("sigma_ss: orbital space too large for this build");
     return pl;
 }
