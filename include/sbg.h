@@ -174,6 +174,10 @@ int sbg_spin_squared(sbg_ctx* ctx, const double* x, double* out);
 int sbg_spin_squared_padded(sbg_ctx* ctx, const double* d_x_padded_local, double* out);
 int sbg_solve(sbg_ctx* ctx, int method, int nroots, const sbg_config* cfg, double* energies,
               double* vectors, sbg_stats* stats, sbg_trace_fn trace, void* trace_user);
+/* Davidson with an explicit subspace cap: DavidsonConfig::max_space (davidson.hpp:19-38; the CLI's
+ * --max-space, sbci_cli.cpp:49,125). 0 = 12*nroots; otherwise it must be >= 2*nroots. */
+int sbg_solve_davidson(sbg_ctx* ctx, int nroots, int max_space, const sbg_config* cfg, double* energies,
+                       double* vectors, sbg_stats* stats, sbg_trace_fn trace, void* trace_user);
 
 /* self test of the DMMA fragment layouts used by the sigma kernels (GPU) */
 int sbg_selftest(void);

@@ -415,8 +415,8 @@ int sbg_spin_squared_padded(sbg_ctx* ctx, const double* d_x, double* out) {
     });
 }
 
-int sbg_solve(sbg_ctx* ctx, int method, int nroots, const sbg_config* cfg, double* energies, double* vectors,
-              sbg_stats* stats, sbg_trace_fn trace, void* trace_user) {
+static int solve_impl(sbg_ctx* ctx, int method, int nroots, int max_space, const sbg_config* cfg, double* energies,
+                      double* vectors, sbg_stats* stats, sbg_trace_fn trace, void* trace_user) {
     return guarded([&] {
         require_ctx(ctx);
         if (method < 1 || method > 3)
@@ -458,7 +458,7 @@ int sbg_solve(sbg_ctx* ctx, int method, int nroots, const sbg_config* cfg, doubl
         try {
             sbg::MultiStateResult r = method == 1   ? sbg::solve_n_states_sbci1(c, nroots, to_cfg(cfg), tf)
                                       : method == 2 ? sbg::solve_n_states_sbci2(c, nroots, to_cfg(cfg), tf)
-                                                    : sbg::davidson_solve(c, nroots, to_cfg(cfg), tf);
+                                                    : sbg::davidson_solve(c, nroots, to_cfg(cfg), tf, max_space);
             std::vector<double> s2(nroots);
             for (int k = 0; k < nroots; ++k) s2[k] = c.spin_squared(r.pairs[k].vector.p);
             for (int k = 0; k < nroots; ++k) {
@@ -494,6 +494,16 @@ int sbg_solve(sbg_ctx* ctx, int method, int nroots, const sbg_config* cfg, doubl
             throw;
         }
     });
+}
+
+int sbg_solve(sbg_ctx* ctx, int method, int nroots, const sbg_config* cfg, double* energies, double* vectors,
+              sbg_stats* stats, sbg_trace_fn trace, void* trace_user) {
+    return solve_impl(ctx, method, nroots, 0, cfg, energies, vectors, stats, trace, trace_user);
+}
+
+int sbg_solve_davidson(sbg_ctx* ctx, int nroots, int max_space, const sbg_config* cfg, double* energies,
+                       double* vectors, sbg_stats* stats, sbg_trace_fn trace, void* trace_user) {
+    return solve_impl(ctx, 3, nroots, max_space, cfg, energies, vectors, stats, trace, trace_user);
 }
 
 int sbg_selftest(void) {

@@ -130,9 +130,10 @@ using namespace detail;
 
 // davidson_solve(op, nroots, cfg) (davidson.hpp:53-244)
 MultiStateResult davidson_solve(Context& c, int nroots, const SolverConfig& cfg,
-                                const std::function<void(const TraceRec&)>& trace) {
+                                const std::function<void(const TraceRec&)>& trace, int max_space_opt) {
     DavidsonConfig dcfg;
     dcfg.nroots = nroots;
+    dcfg.max_space = max_space_opt;
     dcfg.eps0 = cfg.eps0;
     dcfg.r0 = cfg.r0;
     dcfg.lindep = cfg.lindep;

@@ -32,7 +32,9 @@ namespace {
 template <int NT> struct Tile {
     static constexpr int NBT = NT / 8;         // n8 blocks per tile
     static constexpr int DSTRIDE = NT + 4;     // D row stride: bank-conflict-free B fragments (== 4 mod 16)
-    static constexpr int GSTRIDE = NT + 1;     // staged G row stride
+    // staged G row stride: == 8 mod 16 doubles, so the MMA warps' 16-byte accumulator stores are
+    // bank-conflict free (a quarter warp covers 8 distinct 16-byte bank groups)
+    static constexpr int GSTRIDE = NT + 8;
 };
 constexpr int STAGES = 2;     // D tiles, G tiles and scatter lists are double buffered
 
@@ -48,7 +50,7 @@ struct AbParams {
     int64_t NB, ld, row_lo, row_hi;
     double e_core;
     int accumulate;
-    int dbg;  // profiling experiments only: 1 = skip scatter, 2 = skip MMA
+    int dbg;  // profiling experiments only: 1 = skip scatter, 2 = skip MMA, 4 = skip gathers (ws kernel)
     int red;  // k_sigma_ab_ws: 1 = scatter by red.global.add into y (no sigma row in shared memory)
     const uint32_t* ent32;      // red mode, per tile: target << 16 | negative << 15 | G offset
     const uint32_t* tile_ent32; // [ntiles+1] offsets into ent32 (multiples of 4)
@@ -345,6 +347,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
             if (p.extra)
                 for (int i = tid; i < KP * 8; i += kWsHalf) sAe[i] = aval(re + (i & 7), i >> 3);
             bar_sync(BAR_MINT, kWsHalf);
+            // the extra m8 rows' A fragments stay in registers too (warps w < NBT)
+            double aer[KS];
+#pragma unroll
+            for (int j = 0; j < KS; ++j) aer[j] = do_extra ? sAe[(4 * j + t) * 8 + g] : 0.0;
             for (int it = 0; it < ntiles; ++it) {
                 const int b = it & 1;
                 bar_sync(BAR_DREADY + b, kWsThreads);
@@ -371,24 +377,24 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
 #pragma unroll
                         for (int nb = 0; nb < NBT; ++nb) dmma_16x8x4(acc[nb], a0[j], a1[j], bf[cur][nb]);
                         if (do_extra) {
-                            const double ae = sAe[(4 * j + t) * 8 + g];
-                            const double be = D[(4 * j + t) * DSTRIDE + g + w * 8];
-                            if (cur) dmma_8x8x4(ace1, ae, be);
-                            else dmma_8x8x4(ace0, ae, be);
+                            // warp w's extra n8 block is column block w: its B fragment is bf[cur][w]
+                            double be = bf[cur][0];
+#pragma unroll
+                            for (int nb = 1; nb < NBT; ++nb)
+                                if (w == nb) be = bf[cur][nb];
+                            if (cur) dmma_8x8x4(ace1, aer[j], be);
+                            else dmma_8x8x4(ace0, aer[j], be);
                         }
                     }
 #pragma unroll
                     for (int nb = 0; nb < NBT; ++nb) {
                         const int col = nb * 8 + 2 * t;
-                        G[r0 * GSTRIDE + col] = acc[nb][0];
-                        G[r0 * GSTRIDE + col + 1] = acc[nb][1];
-                        G[(r0 + 8) * GSTRIDE + col] = acc[nb][2];
-                        G[(r0 + 8) * GSTRIDE + col + 1] = acc[nb][3];
+                        *reinterpret_cast<double2*>(G + r0 * GSTRIDE + col) = make_double2(acc[nb][0], acc[nb][1]);
+                        *reinterpret_cast<double2*>(G + (r0 + 8) * GSTRIDE + col) = make_double2(acc[nb][2], acc[nb][3]);
                     }
-                    if (do_extra) {
-                        G[(re + g) * GSTRIDE + w * 8 + 2 * t] = ace0[0] + ace1[0];
-                        G[(re + g) * GSTRIDE + w * 8 + 2 * t + 1] = ace0[1] + ace1[1];
-                    }
+                    if (do_extra)
+                        *reinterpret_cast<double2*>(G + (re + g) * GSTRIDE + w * 8 + 2 * t) =
+                            make_double2(ace0[0] + ace1[0], ace0[1] + ace1[1]);
                 }
                 bar_arrive(BAR_FULL + b, kWsThreads);
             }
@@ -433,6 +439,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
             bar_sync(BAR_SINT, kWsHalf);       // sJ visible to every loader
             bar_arrive(BAR_KLIST, kWsThreads);
             auto load_d = [&](int stage, int jt) {
+                if (p.dbg & 4) return;  // experiment: no gathers
                 double* dst = Ds + stage * KP * DSTRIDE;
                 for (int c = stid; c < KP * (NT / 2); c += kWsHalf) {
                     const int k = c / (NT / 2), part = c % (NT / 2);
@@ -593,7 +600,7 @@ AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int
         }
         const int64_t ntiles = ld / nt;
         pl.smem = (size_t)(pl.red ? 0 : ld) * 8 + (size_t)STAGES * KP * (nt + 4) * 8 + (size_t)KP * 8 * 8 +
-                  (size_t)STAGES * pl.npad * (nt + 1) * 8 + (size_t)STAGES * (pl.maxT * 4 + pl.maxE * 2) +
+                  (size_t)STAGES * pl.npad * (nt + 8) * 8 + (size_t)STAGES * (pl.maxT * 4 + pl.maxE * 2) +
                   (size_t)(ntiles + 1) * 8 + (size_t)KP * 16 + 16;
     };
     // default: k_sigma_ab_ws with reductions into y (SBG_AB_RED=0 selects the shared-memory sigma
@@ -608,7 +615,7 @@ AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int
         if (pl.smem > 227 * 1024) configure(16);
     }
     if (NB > 32767) throw InvalidArgument("sigma_ab: more than 32767 beta strings is not supported by this build");
-    if ((size_t)pl.npad * (pl.nt + 1) >= 32768) throw InvalidArgument("sigma_ab: pair space too large for this build");
+    if ((size_t)pl.npad * (pl.nt + 8) >= 32768) throw InvalidArgument("sigma_ab: pair space too large for this build");
     if (pl.smem > 227 * 1024) throw InvalidArgument("sigma_ab: beta row does not fit in shared memory");
     if (pl.KS > 24 || pl.threads > 256) throw InvalidArgument("sigma_ab: orbital space too large for this build");
     // warp-specialized kernel (k_sigma_ab_ws): 8 MMA warps + 8 load/scatter warps
@@ -622,7 +629,7 @@ AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int
 // 0xFFFF = none). Sort key: target, then (rs, column) — a fixed summation order per target.
 void build_ab_scatter(const AbPlan& pl, const std::vector<uint16_t>& codes, std::vector<uint32_t>& tgt,
                       std::vector<uint16_t>& ent, std::vector<uint32_t>& tile_tgt, std::vector<uint32_t>& tile_ent) {
-    const int NT = pl.nt, GSTRIDE = pl.nt + 1;
+    const int NT = pl.nt, GSTRIDE = pl.nt + 8;  // Tile<NT>::GSTRIDE
     const int64_t ntiles = pl.ld / NT;
     tgt.clear();
     ent.clear();
@@ -660,7 +667,7 @@ void build_ab_scatter(const AbPlan& pl, const std::vector<uint16_t>& codes, std:
 // target order (neighbouring lanes reduce into neighbouring y elements), padded to 4 entries
 void build_ab_red_list(const AbPlan& pl, const std::vector<uint16_t>& codes, std::vector<uint32_t>& ent,
                        std::vector<uint32_t>& tile_ent) {
-    const int NT = pl.nt, GSTRIDE = pl.nt + 1;
+    const int NT = pl.nt, GSTRIDE = pl.nt + 8;  // Tile<NT>::GSTRIDE
     const int64_t ntiles = pl.ld / NT;
     ent.clear();
     tile_ent.assign(ntiles + 1, 0);

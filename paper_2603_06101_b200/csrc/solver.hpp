@@ -50,8 +50,9 @@ constexpr int detail_max_roots = 9;  // deflation sets of up to 8 states (precon
 MultiStateResult solve_n_states_sbci1(Context& ctx, int n, const SolverConfig& cfg,
                                       const std::function<void(const TraceRec&)>& trace);
 // davidson_solve(op, nroots, cfg) (davidson.hpp:53-244): block Davidson cross-check
+// max_space: DavidsonConfig::max_space (davidson.hpp:19-38), 0 = 12 * nroots
 MultiStateResult davidson_solve(Context& ctx, int nroots, const SolverConfig& cfg,
-                                const std::function<void(const TraceRec&)>& trace);
+                                const std::function<void(const TraceRec&)>& trace, int max_space = 0);
 // solve_n_states_sbci2 (sbci2.hpp:527-623): pair-sequential lowest-n driver
 MultiStateResult solve_n_states_sbci2(Context& ctx, int n, const SolverConfig& cfg,
                                       const std::function<void(const TraceRec&)>& trace);

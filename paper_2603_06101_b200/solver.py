@@ -132,7 +132,7 @@ class MultiStateResult:
     summary: RunSummary
 
 
-def _solve(op, method: int, n: int, cfg: SolverConfig | None, sink, want_vectors: bool):
+def _solve(op, method: int, n: int, cfg: SolverConfig | None, sink, want_vectors: bool, max_space: int = 0):
     cfg = cfg or SolverConfig()
     cfg.validate()
     name = METHODS[method]
@@ -153,8 +153,12 @@ def _solve(op, method: int, n: int, cfg: SolverConfig | None, sink, want_vectors
                              r.pair_partner, r.b_ab, r.b_ba, r.b_bb, r.c_ab, r.c_ba, r.c_bb, r.a_ab, r.a_ba,
                              r.energy_partner, r.x_norm_partner, r.res_norm_partner))
         cb = TRACE_FN(_cb)
-    rc = lib().sbg_solve(op.handle, method, n, C.byref(cc), e.ctypes.data_as(C.POINTER(C.c_double)),
-                         vec.ctypes.data_as(C.POINTER(C.c_double)) if vec is not None else None, C.byref(st), cb, None)
+    ep = e.ctypes.data_as(C.POINTER(C.c_double))
+    vp = vec.ctypes.data_as(C.POINTER(C.c_double)) if vec is not None else None
+    if method == 3 and max_space:
+        rc = lib().sbg_solve_davidson(op.handle, n, max_space, C.byref(cc), ep, vp, C.byref(st), cb, None)
+    else:
+        rc = lib().sbg_solve(op.handle, method, n, C.byref(cc), ep, vp, C.byref(st), cb, None)
     if rc == 2:
         raise NonConvergenceError(lib().sbg_last_error().decode(), st.failed_state, st.best_energy, st.best_residual)
     check(rc)
@@ -183,7 +187,9 @@ def solve_n_states_sbci2(op, n: int, cfg: SolverConfig | None = None, sink=None,
     return r
 
 
-def davidson_solve(op, nroots: int, cfg: SolverConfig | None = None, sink=None, want_vectors: bool = True):
-    """Block Davidson (davidson.hpp:228-244: eps0/r0/lindep from cfg, max_space 12*nroots, 400
-    iterations) on the GPU operator, with the SBCI solvers' (D - E0)^-1 preconditioner."""
-    return _solve(op, 3, nroots, cfg, sink, want_vectors)
+def davidson_solve(op, nroots: int, cfg: SolverConfig | None = None, sink=None, want_vectors: bool = True,
+                   max_space: int = 0):
+    """Block Davidson (davidson.hpp:228-244: eps0/r0/lindep from cfg, 400 iterations) on the GPU
+    operator, with the SBCI solvers' (D - E0)^-1 preconditioner. max_space = DavidsonConfig::max_space
+    (davidson.hpp:19-38): 0 = 12*nroots, else >= 2*nroots."""
+    return _solve(op, 3, nroots, cfg, sink, want_vectors, max_space)
