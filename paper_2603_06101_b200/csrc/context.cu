@@ -167,11 +167,13 @@ T* dmalloc(size_t n) {
     return p;
 }
 
+// dst += src on a column window, as fp64 reductions: it runs beside the alpha-beta kernel, which
+// reduces into the same rows of y
 __global__ void k_add_block(double* dst, int64_t ldd, const double* src, int64_t rows, int64_t cols) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= rows * cols) return;
     const int64_t r = i / cols, c = i % cols;
-    dst[r * ldd + c] += src[i];
+    red_add_f64(dst + r * ldd + c, src[i]);
 }
 
 }  // namespace
@@ -218,6 +220,9 @@ Context::Context(int norb_, int nelec_, int ms2_, double e_core_, const double* 
     if (world > 1) {
         if (local_group && local_group->world != world) throw InvalidArgument("local group: world mismatch");
         comm_ = local_group ? make_local_comm(local_group, rank) : make_nccl_comm(world, rank, nccl_id);
+        SBG_CUDA(cudaStreamCreateWithFlags(&comm_st_, cudaStreamNonBlocking));
+        for (cudaEvent_t* e : {&ev_in_, &ev_gathered_, &ev_aa_, &ev_xdone_})
+            SBG_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
 
     rws.grid = 16 * nsm;
@@ -242,6 +247,12 @@ Context::~Context() {
         if (c) cudaStreamDestroy(c);
     if (ev0_) cudaEventDestroy(ev0_);
     if (ev1_) cudaEventDestroy(ev1_);
+    for (cudaEvent_t e : {ev_in_, ev_gathered_, ev_aa_, ev_xdone_})
+        if (e) cudaEventDestroy(e);
+    if (comm_st_) {
+        cudaStreamSynchronize(comm_st_);
+        cudaStreamDestroy(comm_st_);
+    }
     if (st) cudaStreamDestroy(st);
 }
 
@@ -482,9 +493,9 @@ void Context::profile_read(double* ms, int64_t* calls) {
     for (size_t i = 0; i < ev_used_; ++i) {
         float t[4];
         const auto& e = ev_pool_[i].e;
-        SBG_CUDA(cudaEventElapsedTime(&t[0], e[3], e[4]));  // alpha-beta
-        SBG_CUDA(cudaEventElapsedTime(&t[1], e[1], e[3]));  // same-spin + transposes
-        SBG_CUDA(cudaEventElapsedTime(&t[2], e[0], e[1]));  // all-gather
+        SBG_CUDA(cudaEventElapsedTime(&t[0], e[3], e[4]));  // alpha-beta (+ the exchange it hides)
+        SBG_CUDA(cudaEventElapsedTime(&t[1], e[0], e[3]));  // same-spin + transposes (+ all-gather wait)
+        SBG_CUDA(cudaEventElapsedTime(&t[2], e[0], e[1]));  // all-gather (overlapped with beta-beta)
         SBG_CUDA(cudaEventElapsedTime(&t[3], e[0], e[4]));  // whole sigma
         for (int k = 0; k < 4; ++k) prof_ms_[k] += t[k];
         ++prof_calls_;
@@ -499,23 +510,39 @@ void Context::sigma(const double* x_local, double* y_local, cudaStream_t s) {
     if (ev) SBG_CUDA(cudaEventRecord(ev->e[0], s));
     const double* xf = x_local;
     if (world > 1) {
-        gather_full(x_local, s);
+        // (1) all-gather of x on the comm stream, beside the beta-beta term (row-local)
+        SBG_CUDA(cudaEventRecord(ev_in_, s));
+        SBG_CUDA(cudaStreamWaitEvent(comm_st_, ev_in_, 0));
         xf = xfull_.p;
+    } else if (ev) {
+        SBG_CUDA(cudaEventRecord(ev->e[1], s));
     }
-    if (ev) SBG_CUDA(cudaEventRecord(ev->e[1], s));
     bool y_written = false;
-    // ---- beta-beta via the transpose
+    // ---- beta-beta via the transpose: only this rank's alpha rows (columns of x^T) are needed
     if (ssb_.P > 0) {
-        launch_transpose(xf, NA, NB, ld, xT_.p, ldT, NB, 0, s);
-        SBG_CUDA(cudaMemsetAsync(sT_.p, 0, (size_t)NB * ldT * 8, s));
+        if (world == 1) {
+            launch_transpose(x_local, NA, NB, ld, xT_.p, ldT, NB, ldT, 0, s);
+            SBG_CUDA(cudaMemsetAsync(sT_.p, 0, (size_t)NB * ldT * 8, s));
+        } else {
+            launch_transpose(x_local, nrows, NB, ld, xT_.p + row_lo, ldT, NB, nrows, 0, s);
+            SBG_CUDA(cudaMemset2DAsync(sT_.p + row_lo, ldT * 8, 0, nrows * 8, NB, s));
+        }
         launch_sigma_ss(ssb_, xT_.p, sT_.p, d_Va_, ldT, row_lo, row_hi, s);
         // y[r][c] = sT[c][row_lo + r]
-        launch_transpose(sT_.p + row_lo, NB, nrows, ldT, y_local, ld, nrows, 0, s);
+        launch_transpose(sT_.p + row_lo, NB, nrows, ldT, y_local, ld, nrows, ld, 0, s);
         launches += 3;
         y_written = true;
     }
     if (!y_written) SBG_CUDA(cudaMemsetAsync(y_local, 0, (size_t)nrows * ld * 8, s));
+    if (world > 1) {
+        // enqueued after the beta-beta kernels: a host-synchronous comm (LocalComm) then overlaps them
+        gather_full(x_local, comm_st_);
+        if (ev) SBG_CUDA(cudaEventRecord(ev->e[1], comm_st_));
+        SBG_CUDA(cudaEventRecord(ev_gathered_, comm_st_));
+        SBG_CUDA(cudaStreamWaitEvent(s, ev_gathered_, 0));
+    }
     // ---- alpha-alpha
+    bool exchange = false;
     if (ssa_.P > 0) {
         if (world == 1) {
             launch_sigma_ss(ssa_, xf, y_local, d_Va_, ld, 0, NB, s);
@@ -523,61 +550,19 @@ void Context::sigma(const double* x_local, double* y_local, cudaStream_t s) {
         } else {
             int64_t clo, chi;
             shard_range(NB, rank, world, &clo, &chi);
-            SBG_CUDA(cudaMemsetAsync(saa_.p, 0, (size_t)NA * ld * 8, s));
+            if (chi > clo) SBG_CUDA(cudaMemset2DAsync(saa_.p + clo, ld * 8, 0, (chi - clo) * 8, NA, s));
             launch_sigma_ss(ssa_, xf, saa_.p, d_Va_, ld, clo, chi, s);
             launches += 1;
-            // all-to-all: send rows of rank r' restricted to my column window; receive my rows of
-            // every rank's window.
-            const int64_t wl = chi - clo;
-            std::vector<int64_t> rlo(world), rhi(world), cwl(world), cwh(world);
-            for (int r = 0; r < world; ++r) {
-                shard_range(NA, r, world, &rlo[r], &rhi[r]);
-                shard_range(NB, r, world, &cwl[r], &cwh[r]);
-            }
-            int64_t off = 0;
-            for (int r = 0; r < world; ++r) {
-                const int64_t nr = rhi[r] - rlo[r];
-                if (nr > 0 && wl > 0)
-                    SBG_CUDA(cudaMemcpy2DAsync(a2a_send_.p + off, wl * 8, saa_.p + rlo[r] * ld + clo, ld * 8, wl * 8,
-                                               nr, cudaMemcpyDeviceToDevice, s));
-                off += nr * wl;
-            }
-            std::vector<CommBlock> sends, recvs;
-            off = 0;
-            int64_t roff = 0;
-            for (int r = 0; r < world; ++r) {
-                const int64_t nr = rhi[r] - rlo[r];
-                const int64_t rw = cwh[r] - cwl[r];
-                if (r != rank) {
-                    if (nr * wl > 0) sends.push_back({a2a_send_.p + off, (size_t)(nr * wl), r});
-                    if (nrows * rw > 0) recvs.push_back({a2a_recv_.p + roff, (size_t)(nrows * rw), r});
-                } else if (nrows * rw > 0) {
-                    SBG_CUDA(cudaMemcpyAsync(a2a_recv_.p + roff, a2a_send_.p + off, nrows * rw * 8,
-                                             cudaMemcpyDeviceToDevice, s));
-                }
-                off += nr * wl;
-                roff += nrows * rw;
-            }
-            comm_->exchange(sends, recvs, s);
-            roff = 0;
-            for (int r = 0; r < world; ++r) {
-                const int64_t rw = cwh[r] - cwl[r];
-                if (nrows * rw > 0) {
-                    const int64_t n = nrows * rw;
-                    k_add_block<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(y_local + cwl[r], ld, a2a_recv_.p + roff,
-                                                                            nrows, rw);
-                    SBG_LAUNCH_CHECK();
-                    launches += 1;
-                }
-                roff += nrows * rw;
-            }
+            SBG_CUDA(cudaEventRecord(ev_aa_, s));
+            exchange = true;
         }
     }
     if (ev) {
         SBG_CUDA(cudaEventRecord(ev->e[2], s));
         SBG_CUDA(cudaEventRecord(ev->e[3], s));
     }
-    // ---- alpha-beta (+ one-body folded, + e_core)
+    // ---- alpha-beta (+ one-body folded, + e_core); with world > 1 it runs while the alpha-alpha
+    // blocks are exchanged on the comm stream (both reduce into y)
     if (have_ab_) {
         launch_sigma_ab(ab_, AbScatter{d_sc_tgt_, d_sc_ent_, d_sc_tt_, d_sc_te_, d_red_ent_, d_red_te_}, xf, y_local, d_Vp_, row_lo, row_hi,
                         e_core, 1, nsm, s);
@@ -589,6 +574,59 @@ void Context::sigma(const double* x_local, double* y_local, cudaStream_t s) {
         launch_onebody(xf, y_local, d_la_, (int)row_len(0), d_lb_, (int)row_len(1), d_h1_, norb, NA, NB, ld, e_core,
                        1, s);
         launches += 1;
+    }
+    if (exchange) {
+        // all-to-all of the alpha-alpha column window: send rows of rank r' restricted to my column
+        // window; receive my rows of every rank's window
+        cudaStream_t cs = comm_st_;
+        SBG_CUDA(cudaStreamWaitEvent(cs, ev_aa_, 0));
+        int64_t clo, chi;
+        shard_range(NB, rank, world, &clo, &chi);
+        const int64_t wl = chi - clo;
+        std::vector<int64_t> rlo(world), rhi(world), cwl(world), cwh(world);
+        for (int r = 0; r < world; ++r) {
+            shard_range(NA, r, world, &rlo[r], &rhi[r]);
+            shard_range(NB, r, world, &cwl[r], &cwh[r]);
+        }
+        int64_t off = 0;
+        for (int r = 0; r < world; ++r) {
+            const int64_t nr = rhi[r] - rlo[r];
+            if (nr > 0 && wl > 0)
+                SBG_CUDA(cudaMemcpy2DAsync(a2a_send_.p + off, wl * 8, saa_.p + rlo[r] * ld + clo, ld * 8, wl * 8, nr,
+                                           cudaMemcpyDeviceToDevice, cs));
+            off += nr * wl;
+        }
+        std::vector<CommBlock> sends, recvs;
+        off = 0;
+        int64_t roff = 0;
+        for (int r = 0; r < world; ++r) {
+            const int64_t nr = rhi[r] - rlo[r];
+            const int64_t rw = cwh[r] - cwl[r];
+            if (r != rank) {
+                if (nr * wl > 0) sends.push_back({a2a_send_.p + off, (size_t)(nr * wl), r});
+                if (nrows * rw > 0) recvs.push_back({a2a_recv_.p + roff, (size_t)(nrows * rw), r});
+            } else if (nrows * rw > 0) {
+                SBG_CUDA(cudaMemcpyAsync(a2a_recv_.p + roff, a2a_send_.p + off, nrows * rw * 8, cudaMemcpyDeviceToDevice,
+                                         cs));
+            }
+            off += nr * wl;
+            roff += nrows * rw;
+        }
+        comm_->exchange(sends, recvs, cs);
+        roff = 0;
+        for (int r = 0; r < world; ++r) {
+            const int64_t rw = cwh[r] - cwl[r];
+            if (nrows * rw > 0) {
+                const int64_t n = nrows * rw;
+                k_add_block<<<(unsigned)((n + 255) / 256), 256, 0, cs>>>(y_local + cwl[r], ld, a2a_recv_.p + roff, nrows,
+                                                                         rw);
+                SBG_LAUNCH_CHECK();
+                launches += 1;
+            }
+            roff += nrows * rw;
+        }
+        SBG_CUDA(cudaEventRecord(ev_xdone_, cs));
+        SBG_CUDA(cudaStreamWaitEvent(s, ev_xdone_, 0));
     }
     if (ev) SBG_CUDA(cudaEventRecord(ev->e[4], s));
     applies_.fetch_add(1, std::memory_order_relaxed);

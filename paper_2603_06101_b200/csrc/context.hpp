@@ -142,6 +142,11 @@ private:
     SsPlan ssa_{}, ssb_{};
     bool have_ab_ = false;
     cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+    // world > 1: the collectives run on their own stream, overlapped with the kernels that do not
+    // need their result (beta-beta term during the all-gather, alpha-beta during the alpha-alpha
+    // exchange)
+    cudaStream_t comm_st_ = nullptr;
+    cudaEvent_t ev_in_ = nullptr, ev_gathered_ = nullptr, ev_aa_ = nullptr, ev_xdone_ = nullptr;
     struct EvSet {
         cudaEvent_t e[5];
     };

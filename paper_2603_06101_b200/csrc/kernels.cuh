@@ -56,9 +56,10 @@ struct SsPlan {
 SsPlan plan_sigma_ss(int norb, int nel);
 void launch_sigma_ss(const SsPlan& pl, const double* x, double* y, const double* Va, int64_t ldx, int64_t col_lo,
                      int64_t col_hi, cudaStream_t st);
-// dst[c][r] = src[r][c] (+ dst if accumulate), for r < R, c < C; dst padding columns (r >= R) zeroed.
+// dst[c][r] = src[r][c] (+ dst if accumulate), for r < R, c < C; dst columns r in [R, dst_cols) zeroed,
+// columns >= dst_cols untouched (a column window of a wider destination).
 void launch_transpose(const double* src, int64_t R, int64_t C, int64_t lds, double* dst, int64_t ldd, int64_t dst_rows,
-                      int accumulate, cudaStream_t st);
+                      int64_t dst_cols, int accumulate, cudaStream_t st);
 // one-body + e_core sigma for sectors without an opposite-spin term (n_alpha == 0 or n_beta == 0)
 void launch_onebody(const double* x, double* y, const Excitation* la, int La, const Excitation* lb, int Lb,
                     const double* h1, int norb, int64_t NA, int64_t NB, int64_t ld, double e_core, int accumulate,

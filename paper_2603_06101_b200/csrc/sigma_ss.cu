@@ -97,9 +97,12 @@ __global__ void __launch_bounds__(128, 4) k_sigma_ss(const SsParams p) {
     __syncthreads();
 
     // column tiles of this CTA, X tiles double-buffered with cp.async (tile tt+1 lands while the
-    // DMMAs of tile tt run); Ys is a separate staging tile for the coalesced reductions
-    const int64_t c_begin = p.col_lo + (int64_t)blockIdx.y * p.tpc * NTS;
-    const int ntt = (int)std::min<int64_t>(p.tpc, (p.col_hi - c_begin + NTS - 1) / NTS);
+    // DMMAs of tile tt run); Ys is a separate staging tile for the coalesced reductions. Tiles sit on
+    // the NTS-aligned column grid (16-byte aligned cp.async for any window [col_lo, col_hi), e.g.
+    // odd shard boundaries); columns outside the window are computed but never reduced.
+    const int64_t c_begin = (p.col_lo / NTS + (int64_t)blockIdx.y * p.tpc) * NTS;
+    const int64_t c_end = ((p.col_hi + NTS - 1) / NTS) * NTS;
+    const int ntt = (int)std::min<int64_t>(p.tpc, (c_end - c_begin) / NTS);
     auto load = [&](int tt) {
         const int64_t c0 = c_begin + (int64_t)tt * NTS;
         double* dst = Xs + (tt & 1) * KPP * XSTRIDE;
@@ -140,7 +143,7 @@ __global__ void __launch_bounds__(128, 4) k_sigma_ss(const SsParams p) {
         }
         __syncthreads();
         // one warp reduces one 32-column row segment per step: coalesced 256-byte reductions
-        if (c0 + lane < p.col_hi) {
+        if (c0 + lane >= p.col_lo && c0 + lane < p.col_hi) {
             double* ybase = p.y + c0 + lane;
             const double* yl = Ys + lane;
             const int nw = nthr >> 5;
@@ -167,7 +170,7 @@ void launch_kss(const SsPlan& pl, const SsParams& prm, dim3 grid, cudaStream_t s
 
 // 32x32 tiled transpose of fp64 with a padded shared tile
 __global__ void k_transpose(const double* __restrict__ src, int64_t R, int64_t C, int64_t lds, double* __restrict__ dst,
-                            int64_t ldd, int64_t dst_rows, int accumulate) {
+                            int64_t ldd, int64_t dst_rows, int64_t dst_cols, int accumulate) {
     __shared__ double tile[32][33];
     const int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;  // src rows / cols
     for (int i = threadIdx.y; i < 32; i += blockDim.y) {
@@ -177,7 +180,7 @@ __global__ void k_transpose(const double* __restrict__ src, int64_t R, int64_t C
     __syncthreads();
     for (int i = threadIdx.y; i < 32; i += blockDim.y) {
         const int64_t c = c0 + i, r = r0 + threadIdx.x;  // dst row c, dst col r
-        if (c < dst_rows && r < ldd) {
+        if (c < dst_rows && r < dst_cols) {
             double v = tile[threadIdx.x][i];
             if (accumulate) v += dst[c * ldd + r];
             dst[c * ldd + r] = v;
@@ -237,7 +240,7 @@ void launch_sigma_ss(const SsPlan& pl, const double* x, double* y, const double*
                      int64_t col_hi, cudaStream_t st) {
     ensure_binomials();
     if (pl.P == 0 || pl.NK == 0 || col_hi <= col_lo) return;
-    const int64_t ncols = col_hi - col_lo, ntiles = (ncols + NTS - 1) / NTS;
+    const int64_t ntiles = (col_hi + NTS - 1) / NTS - col_lo / NTS;  // aligned tile grid (see k_sigma_ss)
     // as many tiles per CTA as keep >= 8 CTAs per SM in flight
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
@@ -258,11 +261,12 @@ void launch_sigma_ss(const SsPlan& pl, const double* x, double* y, const double*
 }
 
 void launch_transpose(const double* src, int64_t R, int64_t C, int64_t lds, double* dst, int64_t ldd, int64_t dst_rows,
-                      int accumulate, cudaStream_t st) {
-    // grid over src tiles covering rows [0, max(R, ldd)) so that dst padding columns are written
-    const int64_t rr = std::max(R, ldd), cc = std::max(C, dst_rows);
+                      int64_t dst_cols, int accumulate, cudaStream_t st) {
+    // grid over src tiles covering rows [0, max(R, dst_cols)): dst columns r in [R, dst_cols) (the
+    // padding of a full-width destination) are written as zeros
+    const int64_t rr = std::max(R, dst_cols), cc = std::max(C, dst_rows);
     dim3 grid((unsigned)((rr + 31) / 32), (unsigned)((cc + 31) / 32));
-    k_transpose<<<grid, dim3(32, 8), 0, st>>>(src, R, C, lds, dst, ldd, dst_rows, accumulate);
+    k_transpose<<<grid, dim3(32, 8), 0, st>>>(src, R, C, lds, dst, ldd, dst_rows, dst_cols, accumulate);
     SBG_LAUNCH_CHECK();
 }
 
