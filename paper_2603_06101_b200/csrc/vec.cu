@@ -14,6 +14,12 @@ namespace sbg {
 namespace {
 
 constexpr int kThreads = 256;
+// resident blocks per SM the k_lincomb passes with <= 4 dots are compiled for (register cap
+// 65536 / (256 * 3) = 85): more warps in flight to cover HBM latency (c4 commit pass, 11 vectors:
+// 3.24 -> 2.90 ms under ncu)
+#ifndef SBG_VEC_MINB
+#define SBG_VEC_MINB 3
+#endif
 
 template <int ND>
 __device__ __forceinline__ void block_reduce_store(double (&acc)[ND], int ndot, double* partial) {
@@ -41,7 +47,7 @@ __device__ __forceinline__ void block_reduce_store(double (&acc)[ND], int ndot, 
 // loads/stores: n is even and every vector base is 16-byte aligned). Slots read by dots are staged
 // in shared memory so the runtime slot indices never force the slot array into local memory.
 template <int NI, int NO, int ND>
-__global__ void __launch_bounds__(kThreads) k_lincomb(const LinArgs a, double* partial) {
+__global__ void __launch_bounds__(kThreads, ND > 4 ? 2 : SBG_VEC_MINB) k_lincomb(const LinArgs a, double* partial) {
     constexpr int NDS = ND > 0 ? ND : 1;
     __shared__ double stage[ND > 0 ? kMaxIn + kMaxOut : 1][kThreads];
     double acc[NDS];
