@@ -28,6 +28,7 @@ void launch_scatter_codes(const uint64_t* sb, int64_t nb, int64_t ld, int norb, 
 // ---- sigma_ab.cu: opposite-spin term (+ folded one-body, + e_core), K6 ----
 struct AbPlan {
     int norb, na_el, nb_el, npair, npad, mb16, extra, K, KS, threads, maxT, maxE, nt, ws, red;
+    int k0e;  // ws kernel: occupation column k = 0 as an epilogue rank-1 term (K - 1 divisible by 4)
     int64_t NA, NB, ld;
     size_t smem;
 };

@@ -293,11 +293,16 @@ constexpr int kWsThreads = 512, kWsHalf = 256;
 constexpr int WSU = SBG_WSU;
 constexpr int BAR_DREADY = 1, BAR_FULL = 3, BAR_EMPTY = 5, BAR_SINT = 7, BAR_MINT = 8, BAR_KLIST = 9;
 
-template <int KS, int NT>
+template <int KS, int NT, bool K0E>
 __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p) {
     constexpr int NBT = Tile<NT>::NBT, DSTRIDE = Tile<NT>::DSTRIDE, GSTRIDE = Tile<NT>::GSTRIDE;
     extern __shared__ __align__(16) double smem[];
-    const int KP = KS * 4;
+    // D rows: k = 0 is the row Ia itself (all occupation entries, sigma.hpp:33-35), k = 1..K-1 its
+    // single excitations. K0E (when (K-1) % 4 == 0): the DMMAs cover k = 1 .. 4*KS and k = 0 is a
+    // rank-1 term added in the epilogue (G += A(:,0) c(Ia,:)), so the K - 1 = n(norb-n) links need
+    // no padded k-step (c4: 16 instead of 17); otherwise the DMMAs cover k = 0 .. 4*KS-1.
+    constexpr int K0 = K0E ? 1 : 0;
+    const int KP = K0 + KS * 4;
     const int ntiles = (int)(p.ld / NT);
     double* srow = smem;                     // [ld], absent in red mode
     double* Ds = srow + (p.red ? 0 : p.ld);
@@ -340,17 +345,19 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
             const int r0 = 16 * w + g, re = 16 * p.mb16;
 #pragma unroll
             for (int j = 0; j < KS; ++j) {
-                const int k = 4 * j + t;
+                const int k = K0 + 4 * j + t;
                 a0[j] = main_ok ? aval(r0, k) : 0.0;
                 a1[j] = main_ok ? aval(r0 + 8, k) : 0.0;
             }
+            const double a00 = (K0E && main_ok) ? aval(r0, 0) : 0.0, a01 = (K0E && main_ok) ? aval(r0 + 8, 0) : 0.0;
             if (p.extra)
                 for (int i = tid; i < KP * 8; i += kWsHalf) sAe[i] = aval(re + (i & 7), i >> 3);
             bar_sync(BAR_MINT, kWsHalf);
             // the extra m8 rows' A fragments stay in registers too (warps w < NBT)
             double aer[KS];
 #pragma unroll
-            for (int j = 0; j < KS; ++j) aer[j] = do_extra ? sAe[(4 * j + t) * 8 + g] : 0.0;
+            for (int j = 0; j < KS; ++j) aer[j] = do_extra ? sAe[(K0 + 4 * j + t) * 8 + g] : 0.0;
+            const double ae0 = (K0E && do_extra) ? sAe[g] : 0.0;
             for (int it = 0; it < ntiles; ++it) {
                 const int b = it & 1;
                 bar_sync(BAR_DREADY + b, kWsThreads);
@@ -364,15 +371,16 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                     for (int nb = 0; nb < NBT; ++nb)
 #pragma unroll
                         for (int e = 0; e < 4; ++e) acc[nb][e] = 0.0;
+                    const double* D1 = D + K0 * DSTRIDE;  // rows of the DMMA k range
                     double bf[2][NBT];
 #pragma unroll
-                    for (int nb = 0; nb < NBT; ++nb) bf[0][nb] = D[t * DSTRIDE + g + nb * 8];
+                    for (int nb = 0; nb < NBT; ++nb) bf[0][nb] = D1[t * DSTRIDE + g + nb * 8];
 #pragma unroll
                     for (int j = 0; j < KS; ++j) {
                         const int cur = j & 1;
                         if (j + 1 < KS) {
 #pragma unroll
-                            for (int nb = 0; nb < NBT; ++nb) bf[cur ^ 1][nb] = D[(4 * (j + 1) + t) * DSTRIDE + g + nb * 8];
+                            for (int nb = 0; nb < NBT; ++nb) bf[cur ^ 1][nb] = D1[(4 * (j + 1) + t) * DSTRIDE + g + nb * 8];
                         }
 #pragma unroll
                         for (int nb = 0; nb < NBT; ++nb) dmma_16x8x4(acc[nb], a0[j], a1[j], bf[cur][nb]);
@@ -386,15 +394,22 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                             else dmma_8x8x4(ace0, aer[j], be);
                         }
                     }
+                    // epilogue: the k = 0 rank-1 term (K0E; a00 = a01 = ae0 = 0 otherwise), then
+                    // 16-byte stores of the tile
 #pragma unroll
                     for (int nb = 0; nb < NBT; ++nb) {
                         const int col = nb * 8 + 2 * t;
-                        *reinterpret_cast<double2*>(G + r0 * GSTRIDE + col) = make_double2(acc[nb][0], acc[nb][1]);
-                        *reinterpret_cast<double2*>(G + (r0 + 8) * GSTRIDE + col) = make_double2(acc[nb][2], acc[nb][3]);
+                        const double2 cv = K0E ? *reinterpret_cast<const double2*>(D + col) : make_double2(0.0, 0.0);
+                        *reinterpret_cast<double2*>(G + r0 * GSTRIDE + col) =
+                            make_double2(fma(a00, cv.x, acc[nb][0]), fma(a00, cv.y, acc[nb][1]));
+                        *reinterpret_cast<double2*>(G + (r0 + 8) * GSTRIDE + col) =
+                            make_double2(fma(a01, cv.x, acc[nb][2]), fma(a01, cv.y, acc[nb][3]));
                     }
-                    if (do_extra)
+                    if (do_extra) {
+                        const double2 cv = K0E ? *reinterpret_cast<const double2*>(D + w * 8 + 2 * t) : make_double2(0.0, 0.0);
                         *reinterpret_cast<double2*>(G + (re + g) * GSTRIDE + w * 8 + 2 * t) =
-                            make_double2(ace0[0] + ace1[0], ace0[1] + ace1[1]);
+                            make_double2(fma(ae0, cv.x, ace0[0] + ace1[0]), fma(ae0, cv.y, ace0[1] + ace1[1]));
+                    }
                 }
                 bar_arrive(BAR_FULL + b, kWsThreads);
             }
@@ -546,9 +561,9 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
     }
 }
 
-template <int KS, int NT>
+template <int KS, int NT, bool K0E>
 void launch_ks(const AbPlan& pl, const AbParams& prm, int grid, cudaStream_t st) {
-    auto kern = pl.ws ? k_sigma_ab_ws<KS, NT> : k_sigma_ab<KS, NT>;
+    auto kern = pl.ws ? k_sigma_ab_ws<KS, NT, K0E> : k_sigma_ab<KS, NT>;
     static int configured[2][64] = {{0}};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -574,8 +589,18 @@ AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int
     pl.npair = norb * (norb + 1) / 2;
     pl.K = 1 + na_el * (norb - na_el);
     pl.KS = (pl.K + 3) / 4;
-    const int KP = pl.KS * 4;
     const int full = pl.npair / 16, rem = pl.npair % 16;
+    // default: k_sigma_ab_ws with reductions into y (SBG_AB_RED=0 selects the shared-memory sigma
+    // row with the target-sorted segment scatter, SBG_AB_WS then picks its warp-specialized form)
+    const char* red_env = getenv("SBG_AB_RED");
+    pl.red = red_env ? (atoi(red_env) != 0) : 1;
+    const char* ws_env = getenv("SBG_AB_WS");
+    pl.ws = (ws_env ? (atoi(ws_env) != 0) : 0) || pl.red;
+    // k_sigma_ab_ws with K0E (the K - 1 links fill whole k-steps): KS = (K - 1) / 4 DMMA k-steps,
+    // k = 0 an epilogue rank-1 term, D tiles of 1 + 4 KS rows; otherwise KS = ceil(K / 4), 4 KS rows
+    pl.k0e = pl.ws && pl.K > 1 && (pl.K - 1) % 4 == 0;
+    if (pl.k0e) pl.KS = (pl.K - 1) / 4;
+    const int KP = pl.k0e ? 1 + 4 * pl.KS : 4 * pl.KS;
     auto configure = [&](int nt) {
         const int nbt = nt / 8;
         if (rem == 0) {
@@ -603,10 +628,6 @@ AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int
                   (size_t)STAGES * pl.npad * (nt + 8) * 8 + (size_t)STAGES * (pl.maxT * 4 + pl.maxE * 2) +
                   (size_t)(ntiles + 1) * 8 + (size_t)KP * 16 + 16;
     };
-    // default: k_sigma_ab_ws with reductions into y (SBG_AB_RED=0 selects the shared-memory sigma
-    // row with the target-sorted segment scatter, SBG_AB_WS then picks its warp-specialized form)
-    const char* red_env = getenv("SBG_AB_RED");
-    pl.red = red_env ? (atoi(red_env) != 0) : 1;
     const char* nt_env = getenv("SBG_AB_NT");
     const int nt_force = nt_env ? atoi(nt_env) : 0;
     if (nt_force == 16 || nt_force == 32) configure(nt_force);
@@ -617,10 +638,8 @@ AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int
     if (NB > 32767) throw InvalidArgument("sigma_ab: more than 32767 beta strings is not supported by this build");
     if ((size_t)pl.npad * (pl.nt + 8) >= 32768) throw InvalidArgument("sigma_ab: pair space too large for this build");
     if (pl.smem > 227 * 1024) throw InvalidArgument("sigma_ab: beta row does not fit in shared memory");
-    if (pl.KS > 24 || pl.threads > 256) throw InvalidArgument("sigma_ab: orbital space too large for this build");
+    if (pl.KS > 17 || pl.threads > 256) throw InvalidArgument("sigma_ab: orbital space too large for this build");
     // warp-specialized kernel (k_sigma_ab_ws): 8 MMA warps + 8 load/scatter warps
-    const char* ws_env = getenv("SBG_AB_WS");
-    pl.ws = (ws_env ? (atoi(ws_env) != 0) : 0) || pl.red;
     if (pl.ws) pl.threads = kWsThreads;
     return pl;
 }
@@ -711,7 +730,7 @@ void launch_sigma_ab(const AbPlan& pl, const AbScatter& sc, const double* x_full
     prm.mb16 = pl.mb16;
     prm.extra = pl.extra;
     prm.K = pl.K;
-    prm.KP = pl.KS * 4;
+    prm.KP = pl.k0e ? 1 + 4 * pl.KS : 4 * pl.KS;
     prm.grows = pl.npad;
     prm.maxT = pl.maxT;
     prm.maxE = pl.maxE;
@@ -724,11 +743,18 @@ void launch_sigma_ab(const AbPlan& pl, const AbScatter& sc, const double* x_full
     prm.dbg = getenv("SBG_AB_DEBUG") ? atoi(getenv("SBG_AB_DEBUG")) : 0;
     grid = (int)std::min<int64_t>(grid, row_hi - row_lo);
     switch (pl.KS) {
-#define SBG_KS(n) \
-    case n: if (pl.nt == 32) launch_ks<n, 32>(pl, prm, grid, st); else launch_ks<n, 16>(pl, prm, grid, st); break;
+#define SBG_KS(n)                                                                                   \
+    case n:                                                                                         \
+        if (pl.nt == 32) {                                                                          \
+            if (pl.k0e) launch_ks<n, 32, true>(pl, prm, grid, st);                                  \
+            else launch_ks<n, 32, false>(pl, prm, grid, st);                                        \
+        } else {                                                                                    \
+            if (pl.k0e) launch_ks<n, 16, true>(pl, prm, grid, st);                                  \
+            else launch_ks<n, 16, false>(pl, prm, grid, st);                                        \
+        }                                                                                           \
+        break;
         SBG_KS(1) SBG_KS(2) SBG_KS(3) SBG_KS(4) SBG_KS(5) SBG_KS(6) SBG_KS(7) SBG_KS(8) SBG_KS(9) SBG_KS(10)
-        SBG_KS(11) SBG_KS(12) SBG_KS(13) SBG_KS(14) SBG_KS(15) SBG_KS(16) SBG_KS(17) SBG_KS(18) SBG_KS(19)
-        SBG_KS(20) SBG_KS(21) SBG_KS(22) SBG_KS(23) SBG_KS(24)
+        SBG_KS(11) SBG_KS(12) SBG_KS(13) SBG_KS(14) SBG_KS(15) SBG_KS(16) SBG_KS(17)
 #undef SBG_KS
         default: throw InvalidArgument("sigma_ab: unsupported K");
     }
