@@ -291,6 +291,10 @@ constexpr int kWsThreads = 512, kWsHalf = 256;
 #define SBG_WSU 2
 #endif
 constexpr int WSU = SBG_WSU;
+#ifndef SBG_RED_UNROLL
+#define SBG_RED_UNROLL 4
+#endif
+constexpr int RED_UNROLL = SBG_RED_UNROLL;  // scatter entries per thread in flight
 constexpr int BAR_DREADY = 1, BAR_FULL = 3, BAR_EMPTY = 5, BAR_SINT = 7, BAR_MINT = 8, BAR_KLIST = 9;
 
 template <int KS, int NT, bool K0E>
@@ -494,6 +498,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                     const double* G = Gs + b * p.grows * GSTRIDE;
                     const uint32_t* l32 = reinterpret_cast<const uint32_t*>(Le + b * p.maxE);
                     const uint32_t n = sTE[it + 1] - sTE[it];
+#pragma unroll RED_UNROLL
                     for (uint32_t i = stid; i < n; i += kWsHalf) {
                         const uint32_t en = l32[i];
                         if (en == 0xFFFFFFFFu) continue;  // 16-byte padding
