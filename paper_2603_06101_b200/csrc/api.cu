@@ -280,18 +280,16 @@ int sbg_sigma(sbg_ctx* ctx, const double* x, double* y, int nvec) {
         require_ctx(ctx);
         if (nvec < 0 || (!x && nvec) || (!y && nvec)) throw std::invalid_argument("sbg_sigma: bad arguments");
         auto& c = *ctx->c;
-        if (nvec == 1) {
-            double *dx = c.io_x(), *dy = c.io_y();
-            c.upload_local(x, dx, c.st);
-            c.sigma(dx, dy, c.st);
-            c.download_local(dy, y + c.row_lo * c.NB, c.st);
-            SBG_CUDA(cudaStreamSynchronize(c.st));
-            return;
-        }
-        // several vectors: a two-slot pipeline, H2D of vector v+1 and D2H of vector v-1 on their own
-        // copy streams while sigma(v) runs on the compute stream
+        if (nvec == 0) return;
+        // Host-fed pipeline. Vectors alternate between two device slots; H2D of vector v+1 and D2H of
+        // vector v-1 run on their own copy streams while sigma(v) runs on the compute stream. On one
+        // GPU each vector also moves in row blocks (Context::sigma_rowblocks): the row-local beta-beta
+        // term of block i starts as soon as block i has landed, and block i of y is copied out as
+        // soon as its alpha-beta launch is done — so the first upload and the last download overlap
+        // the sigma they feed instead of standing alone.
+        const int nb = c.rowblocks_ok() ? 4 : 1;
         cudaStream_t cin = c.copy_stream(0), cout = c.copy_stream(1);
-        std::vector<cudaEvent_t> up(nvec), done(nvec), down(nvec);
+        std::vector<cudaEvent_t> up((size_t)nvec * nb), yd((size_t)nvec * nb), down(nvec);
         auto mk = [](cudaEvent_t& e) { SBG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)); };
         struct Cleanup {
             std::vector<cudaEvent_t>* v[3];
@@ -300,24 +298,41 @@ int sbg_sigma(sbg_ctx* ctx, const double* x, double* y, int nvec) {
                     for (auto e : *l)
                         if (e) cudaEventDestroy(e);
             }
-        } cleanup{{&up, &done, &down}};
-        for (int v = 0; v < nvec; ++v) {
-            mk(up[v]);
-            mk(done[v]);
-            mk(down[v]);
-        }
+        } cleanup{{&up, &yd, &down}};
+        for (auto& e : up) mk(e);
+        for (auto& e : yd) mk(e);
+        for (auto& e : down) mk(e);
         for (int v = 0; v < nvec; ++v) {
             const int slot = v & 1;
             double *dx = c.io_x(slot), *dy = c.io_y(slot);
-            if (v >= 2) SBG_CUDA(cudaStreamWaitEvent(cin, done[v - 2], 0));  // sigma(v-2) released dx
-            c.upload_local(x + (size_t)v * c.ndet, dx, cin);
-            SBG_CUDA(cudaEventRecord(up[v], cin));
-            SBG_CUDA(cudaStreamWaitEvent(c.st, up[v], 0));
+            cudaEvent_t* upv = &up[(size_t)v * nb];
+            cudaEvent_t* ydv = &yd[(size_t)v * nb];
+            // sigma(v-2) released dx once its last alpha-beta block is done
+            if (v >= 2) SBG_CUDA(cudaStreamWaitEvent(cin, yd[(size_t)(v - 2) * nb + nb - 1], 0));
             if (v >= 2) SBG_CUDA(cudaStreamWaitEvent(c.st, down[v - 2], 0));  // D2H(v-2) released dy
-            c.sigma(dx, dy, c.st);
-            SBG_CUDA(cudaEventRecord(done[v], c.st));
-            SBG_CUDA(cudaStreamWaitEvent(cout, done[v], 0));
-            c.download_local(dy, y + (size_t)v * c.ndet + c.row_lo * c.NB, cout);
+            if (nb == 1) {
+                c.upload_local(x + (size_t)v * c.ndet, dx, cin);
+                SBG_CUDA(cudaEventRecord(upv[0], cin));
+                SBG_CUDA(cudaStreamWaitEvent(c.st, upv[0], 0));
+                c.sigma(dx, dy, c.st);
+                SBG_CUDA(cudaEventRecord(ydv[0], c.st));
+                SBG_CUDA(cudaStreamWaitEvent(cout, ydv[0], 0));
+                c.download_local(dy, y + (size_t)v * c.ndet + c.row_lo * c.NB, cout);
+            } else {
+                for (int i = 0; i < nb; ++i) {
+                    int64_t lo, hi;
+                    c.chunk_rows(nb, i, &lo, &hi);
+                    c.upload_rows(x + (size_t)v * c.ndet, dx, lo, hi, cin);
+                    SBG_CUDA(cudaEventRecord(upv[i], cin));
+                }
+                c.sigma_rowblocks(dx, dy, c.st, nb, upv, ydv);
+                for (int i = 0; i < nb; ++i) {
+                    int64_t lo, hi;
+                    c.chunk_rows(nb, i, &lo, &hi);
+                    SBG_CUDA(cudaStreamWaitEvent(cout, ydv[i], 0));
+                    c.download_rows(dy, y + (size_t)v * c.ndet + c.row_lo * c.NB, lo, hi, cout);
+                }
+            }
             SBG_CUDA(cudaEventRecord(down[v], cout));
         }
         SBG_CUDA(cudaStreamSynchronize(cout));

@@ -407,6 +407,18 @@ void Context::download_local(const double* d_padded, double* host_dense_local, c
     if (nrows == 0) return;
     SBG_CUDA(cudaMemcpy2DAsync(host_dense_local, NB * 8, d_padded, ld * 8, NB * 8, nrows, cudaMemcpyDeviceToHost, s));
 }
+void Context::upload_rows(const double* host_dense_full, double* d_padded, int64_t lo, int64_t hi,
+                          cudaStream_t s) const {
+    if (hi <= lo) return;
+    SBG_CUDA(cudaMemcpy2DAsync(d_padded + lo * ld, ld * 8, host_dense_full + (row_lo + lo) * NB, NB * 8, NB * 8, hi - lo,
+                               cudaMemcpyHostToDevice, s));
+}
+void Context::download_rows(const double* d_padded, double* host_dense_local, int64_t lo, int64_t hi,
+                            cudaStream_t s) const {
+    if (hi <= lo) return;
+    SBG_CUDA(cudaMemcpy2DAsync(host_dense_local + lo * NB, NB * 8, d_padded + lo * ld, ld * 8, NB * 8, hi - lo,
+                               cudaMemcpyDeviceToHost, s));
+}
 void Context::pack_device(const double* d_dense_full, double* d_padded, cudaStream_t s) const {
     if (nrows == 0) return;
     SBG_CUDA(cudaMemcpy2DAsync(d_padded, ld * 8, d_dense_full + row_lo * NB, NB * 8, NB * 8, nrows,
@@ -471,6 +483,61 @@ const double* Context::finish_dots(int ndot) {
 //   3. alpha-alpha: same-spin kernel on x, fp64 reductions into y (world>1: column window +
 //      all-to-all of the blocks)
 //   4. alpha-beta + one-body + e_core: sigma_ab, accumulating into y
+// rows [lo, hi) of block i of nchunks: equal blocks on a 32-row grid
+void Context::chunk_rows(int nchunks, int i, int64_t* lo, int64_t* hi) const {
+    const int64_t per = round_up((nrows + nchunks - 1) / nchunks, 32);
+    *lo = std::min<int64_t>(nrows, (int64_t)i * per);
+    *hi = std::min<int64_t>(nrows, *lo + per);
+}
+
+void Context::sigma_rowblocks(const double* x_local, double* y_local, cudaStream_t s, int nchunks,
+                              const cudaEvent_t* x_ready, const cudaEvent_t* y_done) {
+    if (world != 1 || !have_ab_ || nchunks < 1) throw InvalidArgument("sigma_rowblocks: single-GPU two-spin sectors only");
+    EvSet* ev = next_evset();
+    if (ev) {
+        SBG_CUDA(cudaEventRecord(ev->e[0], s));
+        SBG_CUDA(cudaEventRecord(ev->e[1], s));
+    }
+    // ---- beta-beta, block by block as the rows arrive (transpose -> same-spin -> transpose back)
+    for (int i = 0; i < nchunks; ++i) {
+        int64_t lo, hi;
+        chunk_rows(nchunks, i, &lo, &hi);
+        SBG_CUDA(cudaStreamWaitEvent(s, x_ready[i], 0));
+        if (hi <= lo) continue;
+        if (ssb_.P > 0) {
+            launch_transpose(x_local + lo * ld, hi - lo, NB, ld, xT_.p + lo, ldT, NB, hi - lo, 0, s);
+            SBG_CUDA(cudaMemset2DAsync(sT_.p + lo, ldT * 8, 0, (hi - lo) * 8, NB, s));
+            launch_sigma_ss(ssb_, xT_.p, sT_.p, d_Va_, ldT, lo, hi, s);
+            launch_transpose(sT_.p + lo, NB, hi - lo, ldT, y_local + lo * ld, ld, hi - lo, ld, 0, s);
+            launches += 3;
+        } else {
+            SBG_CUDA(cudaMemsetAsync(y_local + lo * ld, 0, (size_t)(hi - lo) * ld * 8, s));
+        }
+    }
+    // ---- alpha-alpha (all rows: x complete)
+    if (ssa_.P > 0) {
+        launch_sigma_ss(ssa_, x_local, y_local, d_Va_, ld, 0, NB, s);
+        launches += 1;
+    }
+    if (ev) {
+        SBG_CUDA(cudaEventRecord(ev->e[2], s));
+        SBG_CUDA(cudaEventRecord(ev->e[3], s));
+    }
+    // ---- alpha-beta per block: rows of block i are final after its launch
+    const AbScatter sc{d_sc_tgt_, d_sc_ent_, d_sc_tt_, d_sc_te_, d_red_ent_, d_red_te_};
+    for (int i = 0; i < nchunks; ++i) {
+        int64_t lo, hi;
+        chunk_rows(nchunks, i, &lo, &hi);
+        if (hi > lo) {
+            launch_sigma_ab(ab_, sc, x_local, y_local + lo * ld, d_Vp_, lo, hi, e_core, 1, nsm, s);
+            launches += 1;
+        }
+        SBG_CUDA(cudaEventRecord(y_done[i], s));
+    }
+    if (ev) SBG_CUDA(cudaEventRecord(ev->e[4], s));
+    applies_.fetch_add(1, std::memory_order_relaxed);
+}
+
 Context::EvSet* Context::next_evset() {
     if (ev_used_ == ev_pool_.size()) {
         if (ev_pool_.size() >= 256) return nullptr;  // profile ring full: stop recording until read/reset

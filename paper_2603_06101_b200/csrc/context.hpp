@@ -89,6 +89,16 @@ public:
 
     // y = H x on padded local vectors (counts one application)
     void sigma(const double* x_local, double* y_local, cudaStream_t s);
+    // single GPU, host-fed: the same sigma with the rows in nchunks blocks so that copies overlap
+    // it. The beta-beta term of block i (row-local) waits only for x_ready[i]; the alpha-alpha and
+    // alpha-beta terms wait for every block; y_done[i] is recorded once rows of block i are final.
+    void sigma_rowblocks(const double* x_local, double* y_local, cudaStream_t s, int nchunks,
+                         const cudaEvent_t* x_ready, const cudaEvent_t* y_done);
+    void chunk_rows(int nchunks, int i, int64_t* lo, int64_t* hi) const;  // rows of block i
+    bool rowblocks_ok() const { return world == 1 && have_ab_; }
+    // host <-> padded device copies of local rows [lo, hi) (host pointers: dense full / dense local)
+    void upload_rows(const double* host_dense_full, double* d_padded, int64_t lo, int64_t hi, cudaStream_t s) const;
+    void download_rows(const double* d_padded, double* host_dense_local, int64_t lo, int64_t hi, cudaStream_t s) const;
     void sigma(const DBuf& x, DBuf& y) { sigma(x.p, y.p, st); }
     // <S^2> of a padded local vector (fci/spin.hpp:17-51); collective over ranks
     double spin_squared(const double* x_local);
