@@ -23,7 +23,13 @@ namespace {
 constexpr int NTS = 32;         // batch columns per tile (one warp-wide reduction segment)
 constexpr int XSTRIDE = NTS + 4;
 constexpr int YSTRIDE = NTS + 4;
-constexpr int kMaxTilesPerCta = 32;  // column tiles per CTA: amortizes the per-K setup (pair list, A)
+#ifndef SBG_SS_TPC
+#define SBG_SS_TPC 128
+#endif
+#ifndef SBG_SS_MINB
+#define SBG_SS_MINB 4
+#endif
+constexpr int kMaxTilesPerCta = SBG_SS_TPC;  // column tiles per CTA: amortizes the per-K setup (pair list, A)
 
 struct SsParams {
     const double* x;
@@ -35,7 +41,7 @@ struct SsParams {
 };
 
 template <int KSS>
-__global__ void __launch_bounds__(128, 4) k_sigma_ss(const SsParams p) {
+__global__ void __launch_bounds__(128, SBG_SS_MINB) k_sigma_ss(const SsParams p) {
     constexpr int KPP = KSS * 4;
     extern __shared__ __align__(16) double smem[];
     double* Xs = smem;                        // [2][KPP][XSTRIDE]
@@ -245,7 +251,9 @@ void launch_sigma_ss(const SsPlan& pl, const double* x, double* y, const double*
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    int tpc = kMaxTilesPerCta;
+    // long rows (c4: 403 tiles) do best with 128 tiles per CTA, shorter ones (c3: 108) with 32
+    // (measured: c4 same-spin 33.4 -> 32.8 ms, c3 1.87 ms kept)
+    int tpc = ntiles >= 256 ? kMaxTilesPerCta : std::min(kMaxTilesPerCta, 32);
     while (tpc > 4 && pl.NK * ((ntiles + tpc - 1) / tpc) < 8LL * nsm) tpc /= 2;
     SsParams prm{x, y, Va, pl.norb, pl.nel, pl.P, pl.npa, ldx, col_lo, col_hi, tpc};
     const int64_t gy = (ntiles + tpc - 1) / tpc;

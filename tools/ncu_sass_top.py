@@ -10,7 +10,10 @@ rows = []
 for row in r[2:]:
     if len(row) < len(h):
         continue
-    s = float(row[idx["Warp Stall Sampling (All Samples)"]] or 0)
+    try:
+        s = float(row[idx["Warp Stall Sampling (All Samples)"]] or 0)
+    except ValueError:
+        continue
     rows.append((s, row[idx["Address"]][-5:], row[idx["Source"]][:80], row[idx["Instructions Executed"]]))
 tot = sum(x[0] for x in rows) or 1
 for x in sorted(rows, reverse=True)[:int(sys.argv[3]) if len(sys.argv) > 3 else 25]:
