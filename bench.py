@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tte", action="store_true", help="skip the time-to-energy solves")
-    ap.add_argument("--tte-full", action="store_true", help="also solve c4 (3 roots, ~4 min) for time-to-energy")
+    ap.add_argument("--tte-full", action="store_true", help="also solve c4 (3 roots, SBCI1/SBCI2/Davidson, ~15 min)")
     return ap.parse_args()
 
 
@@ -159,7 +159,7 @@ def time_to_energy(full=False):
     runs = [("c1", (10, 10, 0.05), 4, ("sbci1", "sbci2", "davidson")), ("c2", (12, 12, 0.05), 1, ("sbci1",)),
             ("c3", (14, 14, 0.05), 2, ("sbci1", "davidson"))]
     if full:
-        runs.append(("c4", (16, 16, 0.08), 3, ("sbci1", "davidson")))
+        runs.append(("c4", (16, 16, 0.08), 3, ("sbci1", "sbci2", "davidson")))
     solvers = {"sbci1": P.solve_n_states_sbci1, "sbci2": P.solve_n_states_sbci2, "davidson": P.davidson_solve}
     for tag, (norb, ne, sc), nroots, methods in runs:
         ref = {}
