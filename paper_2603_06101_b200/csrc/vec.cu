@@ -117,6 +117,10 @@ __device__ __forceinline__ const double2* v2(const double* p) { return reinterpr
 
 // mode 0: overlaps o_c = xc_c . (zres / den)
 // mode 1: z = zres/den - sum_c o_c xc_c ; dots xx, xz, zz [, xy, yy, yz]
+constexpr int kPrecMaxC = 8;  // PrecArgs::xc capacity
+// MAXC: compile-time bound on the deflated states (0 for the ground state: no x_c registers, more
+// resident blocks per SM for this HBM stream)
+template <int MAXC>
 __global__ void __launch_bounds__(kThreads) k_precond(const PrecArgs a, double* partial) {
     double acc[8];
 #pragma unroll
@@ -124,16 +128,16 @@ __global__ void __launch_bounds__(kThreads) k_precond(const PrecArgs a, double* 
     const int64_t n2 = a.n >> 1, stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += stride) {
         const double2 zr = v2(a.zres)[i], D = v2(a.D)[i];
-        double2 xc[8];
+        double2 xc[MAXC > 0 ? MAXC : 1];
 #pragma unroll
-        for (int c = 0; c < 8; ++c)
+        for (int c = 0; c < MAXC; ++c)
             if (c < a.nxc) xc[c] = v2(a.xc[c])[i];
         if (a.mode == 0) {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const double v = comp(zr, h) / precond_den(comp(D, h), a.shift, a.clamp);
 #pragma unroll
-                for (int c = 0; c < 8; ++c)
+                for (int c = 0; c < MAXC; ++c)
                     if (c < a.nxc) acc[c] = fma(comp(xc[c], h), v, acc[c]);
             }
         } else {
@@ -145,7 +149,7 @@ __global__ void __launch_bounds__(kThreads) k_precond(const PrecArgs a, double* 
             for (int h = 0; h < 2; ++h) {
                 double v = comp(zr, h) / precond_den(comp(D, h), a.shift, a.clamp);
 #pragma unroll
-                for (int c = 0; c < 8; ++c)
+                for (int c = 0; c < MAXC; ++c)
                     if (c < a.nxc) v = __dadd_rn(v, __dmul_rn(-a.o[c], comp(xc[c], h)));
                 if (h) z2.y = v;
                 else z2.x = v;
@@ -475,8 +479,12 @@ void launch_lincomb(const LinArgs& args, const ReduceWs& ws, cudaStream_t st) {
 
 void launch_precond(const PrecArgs& a, const ReduceWs& ws, cudaStream_t st) {
     if (a.n & 1) throw InvalidArgument("launch_precond: odd length");
-    const int g = grid_of(reinterpret_cast<const void*>(&k_precond), ws);
-    k_precond<<<g, kThreads, 0, st>>>(a, ws.partial);
+    if (a.nxc < 0 || a.nxc > kPrecMaxC) throw InvalidArgument("launch_precond: bad deflation count");
+    const void* fn = a.nxc == 0 ? reinterpret_cast<const void*>(&k_precond<0>)
+                                : reinterpret_cast<const void*>(&k_precond<kPrecMaxC>);
+    const int g = grid_of(fn, ws);
+    if (a.nxc == 0) k_precond<0><<<g, kThreads, 0, st>>>(a, ws.partial);
+    else k_precond<kPrecMaxC><<<g, kThreads, 0, st>>>(a, ws.partial);
     SBG_LAUNCH_CHECK();
     const int nd = a.mode == 0 ? a.nxc : (a.y ? 6 : 3);
     if (nd > 0) launch_reduce_finish(ws, g, nd, st);
