@@ -138,6 +138,31 @@ def dgemm_peak_tflops(torch):
     return 2 * n ** 3 * 10 / (e0.elapsed_time(e1) * 1e-3) / 1e12
 
 
+def sigma_roofline(norb, n_el, n_det, flops, ms_step, peak_tflops, world=1):
+    """Whole-sigma roofline two ways: (1) this build's executed useful flops against the
+    measured DGEMM peak plus 16 n_det bytes against the HBM peak; (2) the SURVEY's algorithmic count
+    F_sigma = 2 n_det (norb^2 L + 2 W + L), L = n(norb-n+1), W = 1 + n(norb-n) + C(n,2) C(norb-n,2),
+    which the pair-resolved factorization here undercuts (ratio > 1 = faster than that roofline).
+    Peaks are per GPU times `world` (the whole job)."""
+    if not peak_tflops:
+        return None
+    from math import comb
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            bw = float(json.load(f)["hbm_gbs"]) * 1e9 * world
+    except Exception:
+        bw = 7.7e12 * world
+    L = n_el * (norb - n_el + 1)
+    W = 1 + n_el * (norb - n_el) + comb(n_el, 2) * comb(norb - n_el, 2)
+    f_survey = 2.0 * n_det * (norb * norb * L + 2 * W + L)
+    t_bytes = 16.0 * n_det / bw
+    t_own = flops["total"] / (peak_tflops * 1e12) + t_bytes
+    t_survey = f_survey / (peak_tflops * 1e12) + t_bytes
+    t = ms_step * 1e-3
+    return {"hbm_gbs": bw / 1e9, "fp64_tflops": peak_tflops, "executed_flops": flops["total"],
+            "frac_executed": t_own / t, "survey_F_sigma": f_survey, "frac_survey": t_survey / t}
+
+
 def profile_traffic(cfg_name):
     path = os.path.join(ROOT, "profiles", "ab_kernel_traffic.json")
     try:
@@ -345,6 +370,8 @@ def run_ours(args):
                          "traffic": profile_traffic(args.config)},
             "sigma_flops": flops,
             "sigma_tflops": flops["total"] / (ms_step * 1e-3) / 1e12,
+            "sigma_roofline": sigma_roofline(norb, ne // 2, n, flops, ms_step, peak * world if peak else None,
+                                             world),
             "clocks": clocks,
         }
         if world == 1 and not args.no_tte:
