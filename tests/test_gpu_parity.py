@@ -487,3 +487,24 @@ def test_sharded_sigma_odd_boundaries(dev, rest, cfg, world):
         op.close()
     g.close()
     single.close()
+
+
+@pytest.mark.parametrize("env", [{"SBG_AB_NT": "16"}, {"SBG_AB_RED": "0"}, {"SBG_AB_RED": "0", "SBG_AB_WS": "1"},
+                                 {}])
+@pytest.mark.parametrize("spec", [(8, 8, 0), (8, 4, 0), (10, 10, 0)])
+def test_sigma_kernel_variants_match_oracle(dev, rest, monkeypatch, env, spec):
+    """The opposite-spin kernel's selectable forms (read when the operator is planned): 16-column
+    tiles, the deterministic shared-memory sigma row (legacy and warp-specialized), on sectors whose
+    links fill whole k-steps ((8o,4e): 2*6 = 12, the epilogue occupation column) and ones that do
+    not ((8o,8e): 16 links + padding; (10o,10e): 25)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    norb, nelec, ms2 = spec
+    h1, eri = rest.synthetic(norb, 23, 0.07)
+    q = Problem(norb, nelec, ms2, 0.4, h1, eri, "variant")
+    op = P.FciOperator(to_product(q), max_determinants=2 ** 62)
+    x = seeded(op.dim(), 3)
+    y = op.apply(x)
+    ref = rest.sigma(q, x, exact=True)
+    assert np.abs(y - ref).max() <= SIGMA_RTOL * np.abs(ref).max()
+    op.close()
