@@ -329,17 +329,17 @@ def run_ours(args):
     # end to end through the public C ABI: pinned host x -> H2D -> sigma -> D2H for every step; one
     # sbg_sigma call over e2e_steps vectors, which overlaps the copies of neighbouring steps with
     # the sigma builds (the library's two-slot pipeline)
-    ne = args.e2e_steps
-    xh = torch.empty((ne, n), dtype=torch.float64, pin_memory=True)
-    yh = torch.empty((ne, n), dtype=torch.float64, pin_memory=True)
+    nvec = args.e2e_steps
+    xh = torch.empty((nvec, n), dtype=torch.float64, pin_memory=True)
+    yh = torch.empty((nvec, n), dtype=torch.float64, pin_memory=True)
     xh.uniform_(-1.0, 1.0)
     dp = C.POINTER(C.c_double)
     xp = C.cast(C.c_void_p(xh.data_ptr()), dp)
     yp = C.cast(C.c_void_p(yh.data_ptr()), dp)
-    _lib.check(L.sbg_sigma(h, xp, yp, min(ne, 2)))   # warm-up (staging buffers, copy streams)
+    _lib.check(L.sbg_sigma(h, xp, yp, min(nvec, 2)))   # warm-up (staging buffers, copy streams)
     barrier()
     t0 = time.perf_counter()
-    _lib.check(L.sbg_sigma(h, xp, yp, ne))
+    _lib.check(L.sbg_sigma(h, xp, yp, nvec))
     te = time.perf_counter() - t0
     if tdist is not None:
         t = torch.tensor([te], dtype=torch.float64, device="cuda")
