@@ -319,10 +319,11 @@ def run_ours(args):
     calls = C.c_int64()
     _lib.check(L.sbg_profile_read(h, prof, C.byref(calls)))
     ms_ab = prof[0] / max(calls.value, 1)
+    ms_ss = prof[1] / max(calls.value, 1)   # same-spin kernels + transposes (+ all-gather wait)
     if tdist is not None:
-        t = torch.tensor([ms, ms_ab], dtype=torch.float64, device="cuda")
+        t = torch.tensor([ms, ms_ab, ms_ss], dtype=torch.float64, device="cuda")
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        ms, ms_ab = t.tolist()
+        ms, ms_ab, ms_ss = t.tolist()
     ms_step = ms / args.steps
     value = 1000.0 / ms_step
 
@@ -368,6 +369,11 @@ def run_ours(args):
                          "peak_source": "cuBLAS DGEMM 4096^3 fp64 measured in this run (MEASURED_PEAKS.json has no fp64)",
                          "flops_per_launch": flops["alpha_beta"], "ms_per_launch": ms_ab,
                          "traffic": profile_traffic(args.config)},
+            "roofline_same_spin": {"kernel": "k_sigma_ss x2 + 2 transposes (alpha-alpha, beta-beta)", "bound": "tensor",
+                                   "achieved": flops["same_spin"] / (ms_ss * 1e-3) / 1e12 if ms_ss > 0 else None,
+                                   "peak": peak, "unit": "TFLOP/s",
+                                   "frac": (flops["same_spin"] / (ms_ss * 1e-3) / 1e12 / peak) if (ms_ss > 0 and peak) else None,
+                                   "ms_per_sigma": ms_ss},
             "sigma_flops": flops,
             "sigma_tflops": flops["total"] / (ms_step * 1e-3) / 1e12,
             "sigma_roofline": sigma_roofline(norb, ne // 2, n, flops, ms_step, peak * world if peak else None,
