@@ -29,6 +29,7 @@ void launch_scatter_codes(const uint64_t* sb, int64_t nb, int64_t ld, int norb, 
 struct AbPlan {
     int norb, na_el, nb_el, npair, npad, mb16, extra, K, KS, threads, maxT, maxE, nt, ws, red;
     int k0e;  // ws kernel: occupation column k = 0 as an epilogue rank-1 term (K - 1 divisible by 4)
+    int tall; // ws kernel: balanced warp assignment for 5-7 m16 blocks (warps 4-7 span the rest)
     int64_t NA, NB, ld;
     size_t smem;
 };

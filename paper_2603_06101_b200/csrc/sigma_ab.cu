@@ -297,7 +297,7 @@ constexpr int WSU = SBG_WSU;
 constexpr int RED_UNROLL = SBG_RED_UNROLL;  // scatter entries per thread in flight
 constexpr int BAR_DREADY = 1, BAR_FULL = 3, BAR_EMPTY = 5, BAR_SINT = 7, BAR_MINT = 8, BAR_KLIST = 9;
 
-template <int KS, int NT, bool K0E>
+template <int KS, int NT, bool K0E, bool TALL>
 __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p) {
     constexpr int NBT = Tile<NT>::NBT, DSTRIDE = Tile<NT>::DSTRIDE, GSTRIDE = Tile<NT>::GSTRIDE;
     extern __shared__ __align__(16) double smem[];
@@ -326,7 +326,12 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
     // the two roles never rejoin, so ptxas can give each its own register budget
     if (w < 8) {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 " SBG_STR(SBG_WS_MREG) ";\n");
-        const bool main_ok = w < p.mb16;
+        // TALL (5-7 m16 blocks, no extra rows; c2, c3): warps 0-3 own m16 blocks 0-3 with every n8
+        // block, warps 4-7 own blocks 4 .. mb16-1 for one n8 block each (w - 4), so every SM
+        // sub-partition gets mb16 units of DMMA work instead of 2x4 on some and 4 on others
+        const bool tall = TALL && w >= 4;
+        const int mbh = TALL ? p.mb16 - 4 : 0;
+        const bool main_ok = TALL ? w < 4 : w < p.mb16;
         const bool do_extra = p.extra && w < NBT;
         for (int64_t ia = p.row_lo + blockIdx.x; ia < p.row_hi; ia += gridDim.x) {
             bar_sync(0, kWsThreads);           // row start
@@ -345,6 +350,66 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                 }
                 return sSign[k] * p.Vp[(size_t)pr * npair + rs];
             };
+            if constexpr (TALL) {
+                if (tall) {
+                    constexpr int MH = 3;  // up to 3 m16 blocks per tall warp (mb16 <= 7)
+                    const int nbh = w - 4;  // this warp's n8 block
+                    double ah0[MH][KS], ah1[MH][KS], ak0[MH], ak1[MH];
+#pragma unroll
+                    for (int mb = 0; mb < MH; ++mb) {
+                        const int rh = 16 * (4 + mb) + g;
+                        const bool ok = mb < mbh && nbh < NBT;
+#pragma unroll
+                        for (int j = 0; j < KS; ++j) {
+                            ah0[mb][j] = ok ? aval(rh, K0 + 4 * j + t) : 0.0;
+                            ah1[mb][j] = ok ? aval(rh + 8, K0 + 4 * j + t) : 0.0;
+                        }
+                        ak0[mb] = (K0E && ok) ? aval(rh, 0) : 0.0;
+                        ak1[mb] = (K0E && ok) ? aval(rh + 8, 0) : 0.0;
+                    }
+                    bar_sync(BAR_MINT, kWsHalf);
+                    for (int it = 0; it < ntiles; ++it) {
+                        const int b = it & 1;
+                        bar_sync(BAR_DREADY + b, kWsThreads);
+                        if (it >= 2) bar_sync(BAR_EMPTY + b, kWsThreads);
+                        if (!(p.dbg & 2) && nbh < NBT) {
+                            const double* D = Ds + b * KP * DSTRIDE;
+                            double* G = Gs + b * p.grows * GSTRIDE;
+                            const double* D1 = D + K0 * DSTRIDE + g + nbh * 8;
+                            double acc[MH][4];
+#pragma unroll
+                            for (int mb = 0; mb < MH; ++mb)
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) acc[mb][e] = 0.0;
+                            double bq[2];
+                            bq[0] = D1[t * DSTRIDE];
+#pragma unroll
+                            for (int j = 0; j < KS; ++j) {
+                                const int cur = j & 1;
+                                if (j + 1 < KS) bq[cur ^ 1] = D1[(4 * (j + 1) + t) * DSTRIDE];
+#pragma unroll
+                                for (int mb = 0; mb < MH; ++mb)
+                                    if (mb < mbh) dmma_16x8x4(acc[mb], ah0[mb][j], ah1[mb][j], bq[cur]);
+                            }
+                            const int col = nbh * 8 + 2 * t;
+                            const double2 cv = K0E ? *reinterpret_cast<const double2*>(D + col) : make_double2(0.0, 0.0);
+#pragma unroll
+                            for (int mb = 0; mb < MH; ++mb) {
+                                if (mb >= mbh) break;
+                                const int rh = 16 * (4 + mb) + g;
+                                *reinterpret_cast<double2*>(G + rh * GSTRIDE + col) =
+                                    make_double2(fma(ak0[mb], cv.x, acc[mb][0]), fma(ak0[mb], cv.y, acc[mb][1]));
+                                *reinterpret_cast<double2*>(G + (rh + 8) * GSTRIDE + col) =
+                                    make_double2(fma(ak1[mb], cv.x, acc[mb][2]), fma(ak1[mb], cv.y, acc[mb][3]));
+                            }
+                        }
+                        bar_arrive(BAR_FULL + b, kWsThreads);
+                    }
+                    for (int it = ntiles - 2 < 0 ? 0 : ntiles - 2; it < ntiles; ++it)
+                        bar_sync(BAR_EMPTY + (it & 1), kWsThreads);
+                    continue;  // next row
+                }
+            }
             double a0[KS], a1[KS];
             const int r0 = 16 * w + g, re = 16 * p.mb16;
 #pragma unroll
@@ -566,9 +631,9 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
     }
 }
 
-template <int KS, int NT, bool K0E>
+template <int KS, int NT, bool K0E, bool TALL = false>
 void launch_ks(const AbPlan& pl, const AbParams& prm, int grid, cudaStream_t st) {
-    auto kern = pl.ws ? k_sigma_ab_ws<KS, NT, K0E> : k_sigma_ab<KS, NT>;
+    auto kern = pl.ws ? k_sigma_ab_ws<KS, NT, K0E, TALL> : k_sigma_ab<KS, NT>;
     static int configured[2][64] = {{0}};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -644,7 +709,11 @@ AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int
     if ((size_t)pl.npad * (pl.nt + 8) >= 32768) throw InvalidArgument("sigma_ab: pair space too large for this build");
     if (pl.smem > 227 * 1024) throw InvalidArgument("sigma_ab: beta row does not fit in shared memory");
     if (pl.KS > 17 || pl.threads > 256) throw InvalidArgument("sigma_ab: orbital space too large for this build");
-    // warp-specialized kernel (k_sigma_ab_ws): 8 MMA warps + 8 load/scatter warps
+    // warp-specialized kernel (k_sigma_ab_ws): 8 MMA warps + 8 load/scatter warps; 5-7 m16 blocks
+    // without extra rows use the balanced TALL warp assignment (SBG_AB_TALL=0 disables it)
+    const char* tall_env = getenv("SBG_AB_TALL");
+    pl.tall = pl.ws && pl.nt == 32 && !pl.extra && pl.mb16 >= 5 && pl.mb16 <= 7 && pl.KS <= 13 &&
+              !(tall_env && atoi(tall_env) == 0);
     if (pl.ws) pl.threads = kWsThreads;
     return pl;
 }
@@ -750,7 +819,12 @@ void launch_sigma_ab(const AbPlan& pl, const AbScatter& sc, const double* x_full
     switch (pl.KS) {
 #define SBG_KS(n)                                                                                   \
     case n:                                                                                         \
-        if (pl.nt == 32) {                                                                          \
+        if (pl.nt == 32 && pl.tall) {                                                               \
+            if constexpr (n <= 13) {                                                                \
+                if (pl.k0e) launch_ks<n, 32, true, true>(pl, prm, grid, st);                        \
+                else launch_ks<n, 32, false, true>(pl, prm, grid, st);                              \
+            }                                                                                       \
+        } else if (pl.nt == 32) {                                                                   \
             if (pl.k0e) launch_ks<n, 32, true>(pl, prm, grid, st);                                  \
             else launch_ks<n, 32, false>(pl, prm, grid, st);                                        \
         } else {                                                                                    \
