@@ -490,13 +490,14 @@ def test_sharded_sigma_odd_boundaries(dev, rest, cfg, world):
 
 
 @pytest.mark.parametrize("env", [{"SBG_AB_NT": "16"}, {"SBG_AB_RED": "0"}, {"SBG_AB_RED": "0", "SBG_AB_WS": "1"},
-                                 {}])
-@pytest.mark.parametrize("spec", [(8, 8, 0), (8, 4, 0), (10, 10, 0)])
+                                 {"SBG_AB_TALL": "0"}, {}])
+@pytest.mark.parametrize("spec", [(8, 8, 0), (8, 4, 0), (10, 10, 0), (12, 4, 0), (13, 4, 0), (14, 2, 0), (13, 5, 1)])
 def test_sigma_kernel_variants_match_oracle(dev, rest, monkeypatch, env, spec):
     """The opposite-spin kernel's selectable forms (read when the operator is planned): 16-column
-    tiles, the deterministic shared-memory sigma row (legacy and warp-specialized), on sectors whose
-    links fill whole k-steps ((8o,4e): 2*6 = 12, the epilogue occupation column) and ones that do
-    not ((8o,8e): 16 links + padding; (10o,10e): 25)."""
+    tiles, the deterministic shared-memory sigma row (legacy and warp-specialized), the balanced
+    warp assignment for 5-7 m16 blocks ((12o): 78 pairs, (13o): 91, (14o): 105) and its opt-out, on
+    sectors whose links fill whole k-steps ((8o,4e): 2*6 = 12, the epilogue occupation column) and
+    ones that do not ((8o,8e): 16 links + padding; (10o,10e): 25; (13o,5e,Ms=1/2): n_a != n_b)."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     norb, nelec, ms2 = spec
