@@ -5,19 +5,22 @@
 //
 // is the reference's spin-summed contraction (fci/sigma.hpp:86-137) restricted to its alpha-beta
 // cross terms plus both one-body terms; the same-spin two-body terms come from sigma_ss.cu.
-// One CTA owns one alpha row Ia at a time (persistent over rows) and keeps sigma(Ia,:) in shared
-// memory. Per 32-column tile of beta strings Jb:
+// One CTA owns one alpha row Ia at a time (persistent over rows). Per 32-column tile of beta
+// strings Jb:
 //   gather  D[k][Jb] = c(J_k, Jb) for the K = 1 + n_a(norb-n_a) distinct alpha strings J_k linked
 //           to Ia (k=0 is Ia itself carrying all occupation entries; sigma.hpp:33-35) — cp.async,
-//           3-stage pipeline;
+//           double-buffered;
 //   DGEMM   G[rs][Jb] = sum_k A[rs][k] D[k][Jb], A[rs][k] = sign_k V'(pair_k, rs), M = npair =
 //           norb(norb+1)/2 packed symmetric pairs, A resident in registers for the whole row —
 //           mma.sync m16n8k4 / m8n8k4 f64 (SASS DMMA.8x8x4); G staged once in shared memory;
-//   scatter sigma(Ia, Ib) += sum over the tile's (rs, Jb) with E_rs Jb = Ib of sign * G[rs][Jb].
-//           The (rs,Jb) -> Ib map depends only on the tile, so it is precomputed once as a
-//           target-sorted segment list (build_ab_scatter): every target of a tile is reduced by
-//           one thread in a fixed order — no atomics, bit-reproducible sums.
-// The row is then written once: y(Ia,:) = [y(Ia,:)] + sigma_row + e_core c(Ia,:).
+//   scatter sigma(Ia, Ib) += sign * G[rs][Jb] over the tile's (rs, Jb) with E_rs Jb = Ib; the
+//           (rs,Jb) -> Ib map depends only on the tile and is precomputed once per operator.
+// Default kernel (k_sigma_ab_ws): warp-specialized (8 DMMA warps, 8 gather/scatter warps) and the
+// scatter is one red.global.add.f64 per entry into y from a target-sorted list (build_ab_red_list);
+// e_core c(Ia,:) is added the same way. SBG_AB_RED=0 selects the deterministic form: sigma(Ia,:)
+// in shared memory, every target of a tile summed by one thread in a fixed order from a segment
+// list (build_ab_scatter), the row written once — bit-reproducible sums (k_sigma_ab, or the
+// warp-specialized kernel with SBG_AB_WS=1).
 #include <algorithm>
 #include <cstdlib>
 #include <vector>
