@@ -509,3 +509,38 @@ def test_sigma_kernel_variants_match_oracle(dev, rest, monkeypatch, env, spec):
     ref = rest.sigma(q, x, exact=True)
     assert np.abs(y - ref).max() <= SIGMA_RTOL * np.abs(ref).max()
     op.close()
+
+
+def _sweep_sectors():
+    out = []
+    for norb in range(2, 13):
+        for nelec in range(1, 2 * norb):
+            for ms2 in sorted({nelec % 2, -(nelec % 2), 2 if nelec >= 2 else nelec % 2}):
+                na, nb = (nelec + ms2) // 2, (nelec - ms2) // 2
+                if na < 0 or nb < 0 or na > norb or nb > norb or (nelec + ms2) % 2:
+                    continue
+                from math import comb
+                n = comb(norb, na) * comb(norb, nb)
+                if 2 <= n <= 6000 and comb(norb - max(na, nb) + 2, 2) <= 96:
+                    out.append((norb, nelec, ms2))
+    return out[::2]   # a spread of ~100 sectors
+
+
+@pytest.mark.timeout(900)
+def test_sigma_sector_sweep(dev, rest):
+    """sigma vs the oracle restatement on a spread of small sectors (2-12 orbitals, odd/even electron
+    counts, Ms = 0, +-1/2, 1, single-spin): every plan branch of the kernels (tile widths, extra m8
+    rows, the balanced assignment, the epilogue occupation column, one-body-only sectors)."""
+    fails = []
+    for norb, nelec, ms2 in _sweep_sectors():
+        h1, eri = rest.synthetic(norb, 100 + norb * 31 + nelec, 0.07)
+        q = Problem(norb, nelec, ms2, 0.25, h1, eri, f"{norb}o{nelec}e{ms2}")
+        op = P.FciOperator(to_product(q), max_determinants=2 ** 62)
+        x = seeded(op.dim(), norb + nelec)
+        y = op.apply(x)
+        ref = rest.sigma(q, x, exact=True)
+        err = np.abs(y - ref).max() / max(np.abs(ref).max(), 1e-300)
+        if not err <= SIGMA_RTOL:
+            fails.append((norb, nelec, ms2, err))
+        op.close()
+    assert not fails, fails
