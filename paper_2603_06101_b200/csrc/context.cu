@@ -240,6 +240,9 @@ Context::~Context() {
                     (void*)d_sc_tt_, (void*)d_sc_te_, (void*)d_red_ent_, (void*)d_red_te_, (void*)rws.partial, (void*)rws.result})
         if (p) cudaFree(p);
     if (rws.host) cudaFreeHost(rws.host);
+    for (auto& sp : csr_mem_)
+        for (void* q : sp)
+            if (q) cudaFree(q);
     comm_.reset();
     for (auto& es : ev_pool_)
         for (auto& e : es.e) cudaEventDestroy(e);
@@ -306,7 +309,16 @@ void Context::build_tables(const double* h1, const double* eri) {
                     }
         d_Vp_ = dmalloc<double>(Vp.size());
         SBG_CUDA(cudaMemcpyAsync(d_Vp_, Vp.data(), Vp.size() * 8, cudaMemcpyHostToDevice, st));
-        ab_ = plan_sigma_ab(norb, na_el, nb_el, NA, NB, ld, nsm);
+        SBG_CUDA(cudaStreamSynchronize(st));  // the host Vp buffer ends with this block
+        try {
+            ab_ = plan_sigma_ab(norb, na_el, nb_el, NA, NB, ld, nsm);
+        } catch (const InvalidArgument&) {
+            direct_ab_ = true;  // outside the tensor-core kernel's limits: link-table kernel
+        }
+    }
+    if (have_ab_ && direct_ab_) {
+        ensure_links();
+    } else if (have_ab_) {
         d_codes_ = dmalloc<uint16_t>((size_t)ld * ab_.npad);
         launch_scatter_codes(d_sb_, NB, ld, norb, ab_.npair, ab_.npad, d_codes_, st);
         launches += 1;
@@ -336,9 +348,11 @@ void Context::build_tables(const double* h1, const double* eri) {
         SBG_CUDA(cudaStreamSynchronize(st));
     }
     // same-spin antisymmetrized pair integrals W(pr,qs) = (pq|rs) - (ps|rq), p<r, q<s
+    std::vector<double> Va_host;
     if (norb >= 2) {
         const int npa = norb * (norb - 1) / 2;
-        std::vector<double> Va((size_t)npa * npa);
+        std::vector<double>& Va = Va_host;
+        Va.assign((size_t)npa * npa, 0.0);
         for (int r = 1; r < norb; ++r)
             for (int p = 0; p < r; ++p)
                 for (int s = 1; s < norb; ++s)
@@ -348,13 +362,40 @@ void Context::build_tables(const double* h1, const double* eri) {
         SBG_CUDA(cudaMemcpyAsync(d_Va_, Va.data(), Va.size() * 8, cudaMemcpyHostToDevice, st));
         SBG_CUDA(cudaStreamSynchronize(st));
     }
-    ssa_ = plan_sigma_ss(norb, na_el);
-    ssb_ = plan_sigma_ss(norb, nb_el);
+    for (int spin = 0; spin < 2; ++spin) {
+        const int nel = spin ? nb_el : na_el;
+        SsPlan& pl = spin ? ssb_ : ssa_;
+        try {
+            pl = plan_sigma_ss(norb, nel);
+        } catch (const InvalidArgument&) {
+            // more pair rows than the tensor-core kernel holds: CSR of the one-spin operator
+            pl = SsPlan{};
+            SsCsr m;
+            build_ss_csr(norb, nel, Va_host.data(), m);
+            int64_t* rp = dmalloc<int64_t>(m.rowptr.size());
+            int* cl = dmalloc<int>(m.col.size());
+            double* vl = dmalloc<double>(m.val.size());
+            SBG_CUDA(cudaMemcpy(rp, m.rowptr.data(), m.rowptr.size() * 8, cudaMemcpyHostToDevice));
+            if (!m.col.empty()) {
+                SBG_CUDA(cudaMemcpy(cl, m.col.data(), m.col.size() * 4, cudaMemcpyHostToDevice));
+                SBG_CUDA(cudaMemcpy(vl, m.val.data(), m.val.size() * 8, cudaMemcpyHostToDevice));
+            }
+            csr_mem_[spin][0] = rp;
+            csr_mem_[spin][1] = cl;
+            csr_mem_[spin][2] = vl;
+            csr_dev_[spin] = SsCsrDev{m.nstr, rp, cl, vl};
+            ss_csr_[spin] = true;
+            csr_nnz_[spin] = (double)m.col.size();
+        }
+    }
     if (!have_ab_) ensure_links();
 
     // flop accounting: useful (unpadded) multiply-adds x 2
-    flops_ab = have_ab_ ? 2.0 * ab_.npair * ab_.K * (double)ndet : 0.0;
-    flops_ss = 2.0 * ssa_.P * ssa_.P * (double)ssa_.NK * NB + 2.0 * ssb_.P * ssb_.P * (double)ssb_.NK * NA;
+    flops_ab = !have_ab_ ? 0.0
+               : direct_ab_ ? 2.0 * (double)row_len(0) * (double)row_len(1) * (double)ndet
+                            : 2.0 * ab_.npair * ab_.K * (double)ndet;
+    flops_ss = (ss_csr_[0] ? 2.0 * csr_nnz_[0] * NB : 2.0 * ssa_.P * ssa_.P * (double)ssa_.NK * NB) +
+               (ss_csr_[1] ? 2.0 * csr_nnz_[1] * NA : 2.0 * ssb_.P * ssb_.P * (double)ssb_.NK * NA);
 
     // workspaces
     if (world > 1) {
@@ -364,7 +405,7 @@ void Context::build_tables(const double* h1, const double* eri) {
         a2a_send_ = DBuf(NA * ld);
         a2a_recv_ = DBuf(nrows * ld);
     }
-    if (ssb_.P > 0) {
+    if (has_ss(1)) {
         xT_ = DBuf(NB * ldT);
         sT_ = DBuf(NB * ldT);
     }
@@ -483,6 +524,12 @@ const double* Context::finish_dots(int ndot) {
 //   3. alpha-alpha: same-spin kernel on x, fp64 reductions into y (world>1: column window +
 //      all-to-all of the blocks)
 //   4. alpha-beta + one-body + e_core: sigma_ab, accumulating into y
+void Context::run_ss(int spin, const double* x, double* y, int64_t ldx, int64_t col_lo, int64_t col_hi,
+                     cudaStream_t s) {
+    if (ss_csr_[spin]) launch_sigma_ss_csr(csr_dev_[spin], x, y, ldx, col_lo, col_hi, s);
+    else launch_sigma_ss(spin ? ssb_ : ssa_, x, y, d_Va_, ldx, col_lo, col_hi, s);
+}
+
 // rows [lo, hi) of block i of nchunks: equal blocks on a 32-row grid
 void Context::chunk_rows(int nchunks, int i, int64_t* lo, int64_t* hi) const {
     const int64_t per = round_up((nrows + nchunks - 1) / nchunks, 32);
@@ -586,7 +633,7 @@ void Context::sigma(const double* x_local, double* y_local, cudaStream_t s) {
     }
     bool y_written = false;
     // ---- beta-beta via the transpose: only this rank's alpha rows (columns of x^T) are needed
-    if (ssb_.P > 0) {
+    if (has_ss(1)) {
         if (world == 1) {
             launch_transpose(x_local, NA, NB, ld, xT_.p, ldT, NB, ldT, 0, s);
             SBG_CUDA(cudaMemsetAsync(sT_.p, 0, (size_t)NB * ldT * 8, s));
@@ -594,7 +641,7 @@ void Context::sigma(const double* x_local, double* y_local, cudaStream_t s) {
             launch_transpose(x_local, nrows, NB, ld, xT_.p + row_lo, ldT, NB, nrows, 0, s);
             SBG_CUDA(cudaMemset2DAsync(sT_.p + row_lo, ldT * 8, 0, nrows * 8, NB, s));
         }
-        launch_sigma_ss(ssb_, xT_.p, sT_.p, d_Va_, ldT, row_lo, row_hi, s);
+        run_ss(1, xT_.p, sT_.p, ldT, row_lo, row_hi, s);
         // y[r][c] = sT[c][row_lo + r]
         launch_transpose(sT_.p + row_lo, NB, nrows, ldT, y_local, ld, nrows, ld, 0, s);
         launches += 3;
@@ -610,15 +657,15 @@ void Context::sigma(const double* x_local, double* y_local, cudaStream_t s) {
     }
     // ---- alpha-alpha
     bool exchange = false;
-    if (ssa_.P > 0) {
+    if (has_ss(0)) {
         if (world == 1) {
-            launch_sigma_ss(ssa_, xf, y_local, d_Va_, ld, 0, NB, s);
+            run_ss(0, xf, y_local, ld, 0, NB, s);
             launches += 1;
         } else {
             int64_t clo, chi;
             shard_range(NB, rank, world, &clo, &chi);
             if (chi > clo) SBG_CUDA(cudaMemset2DAsync(saa_.p + clo, ld * 8, 0, (chi - clo) * 8, NA, s));
-            launch_sigma_ss(ssa_, xf, saa_.p, d_Va_, ld, clo, chi, s);
+            run_ss(0, xf, saa_.p, ld, clo, chi, s);
             launches += 1;
             SBG_CUDA(cudaEventRecord(ev_aa_, s));
             exchange = true;
@@ -630,7 +677,11 @@ void Context::sigma(const double* x_local, double* y_local, cudaStream_t s) {
     }
     // ---- alpha-beta (+ one-body folded, + e_core); with world > 1 it runs while the alpha-alpha
     // blocks are exchanged on the comm stream (both reduce into y)
-    if (have_ab_) {
+    if (have_ab_ && direct_ab_) {
+        launch_sigma_ab_direct(xf, y_local, d_Vp_, norb * (norb + 1) / 2, d_la_, (int)row_len(0), d_lb_,
+                               (int)row_len(1), row_lo, row_hi, NB, ld, e_core, s);
+        launches += 1;
+    } else if (have_ab_) {
         launch_sigma_ab(ab_, AbScatter{d_sc_tgt_, d_sc_ent_, d_sc_tt_, d_sc_te_, d_red_ent_, d_red_te_}, xf, y_local, d_Vp_, row_lo, row_hi,
                         e_core, 1, nsm, s);
         launches += 1;

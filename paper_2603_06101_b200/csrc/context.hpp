@@ -95,7 +95,7 @@ public:
     void sigma_rowblocks(const double* x_local, double* y_local, cudaStream_t s, int nchunks,
                          const cudaEvent_t* x_ready, const cudaEvent_t* y_done);
     void chunk_rows(int nchunks, int i, int64_t* lo, int64_t* hi) const;  // rows of block i
-    bool rowblocks_ok() const { return world == 1 && have_ab_; }
+    bool rowblocks_ok() const { return world == 1 && have_ab_ && !direct_ab_ && !ss_csr_[0] && !ss_csr_[1]; }
     // host <-> padded device copies of local rows [lo, hi) (host pointers: dense full / dense local)
     void upload_rows(const double* host_dense_full, double* d_padded, int64_t lo, int64_t hi, cudaStream_t s) const;
     void download_rows(const double* d_padded, double* host_dense_local, int64_t lo, int64_t hi, cudaStream_t s) const;
@@ -151,6 +151,15 @@ private:
     AbPlan ab_{};
     SsPlan ssa_{}, ssb_{};
     bool have_ab_ = false;
+    // generic fallbacks for sectors outside the tensor-core kernels' limits
+    bool direct_ab_ = false;
+    bool ss_csr_[2] = {false, false};
+    SsCsrDev csr_dev_[2];
+    void* csr_mem_[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+    double csr_nnz_[2] = {0.0, 0.0};
+    bool has_ss(int spin) const { return ss_csr_[spin] || (spin ? ssb_.P : ssa_.P) > 0; }
+    // same-spin term of one spin on a column window (x, y: rows = that spin's strings)
+    void run_ss(int spin, const double* x, double* y, int64_t ldx, int64_t col_lo, int64_t col_hi, cudaStream_t s);
     cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
     // world > 1: the collectives run on their own stream, overlapped with the kernels that do not
     // need their result (beta-beta term during the all-gather, alpha-beta during the alpha-alpha

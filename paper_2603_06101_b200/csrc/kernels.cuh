@@ -48,6 +48,10 @@ void build_ab_red_list(const AbPlan& pl, const std::vector<uint16_t>& codes, std
                        std::vector<uint32_t>& tile_ent);
 void launch_sigma_ab(const AbPlan& pl, const AbScatter& sc, const double* x_full, double* y_local, const double* Vp,
                      int64_t row_lo, int64_t row_hi, double e_core, int accumulate, int grid, cudaStream_t st);
+// generic fallback outside plan_sigma_ab's limits: y(local rows) += sigma_ab + e_core x from the link tables
+void launch_sigma_ab_direct(const double* x_full, double* y_local, const double* Vp, int npair, const Excitation* la,
+                            int La, const Excitation* lb, int Lb, int64_t row_lo, int64_t row_hi, int64_t NB, int64_t ld,
+                            double e_core, cudaStream_t st);
 
 // ---- sigma_ss.cu: same-spin term via the (n-2)-electron intermediate, K4/K5 ----
 struct SsPlan {
@@ -56,6 +60,22 @@ struct SsPlan {
     size_t smem;
 };
 SsPlan plan_sigma_ss(int norb, int nel);
+// generic fallback outside plan_sigma_ss's limits: the one-spin two-body operator as CSR
+struct SsCsr {
+    int64_t nstr = 0;
+    std::vector<int64_t> rowptr;
+    std::vector<int> col;
+    std::vector<double> val;
+};
+struct SsCsrDev {
+    int64_t nstr = 0;
+    const int64_t* rowptr = nullptr;
+    const int* col = nullptr;
+    const double* val = nullptr;
+};
+void build_ss_csr(int norb, int nel, const double* Va, SsCsr& out);
+void launch_sigma_ss_csr(const SsCsrDev& m, const double* x, double* y, int64_t ldx, int64_t col_lo, int64_t col_hi,
+                         cudaStream_t st);
 void launch_sigma_ss(const SsPlan& pl, const double* x, double* y, const double* Va, int64_t ldx, int64_t col_lo,
                      int64_t col_hi, cudaStream_t st);
 // dst[c][r] = src[r][c] (+ dst if accumulate), for r < R, c < C; dst columns r in [R, dst_cols) zeroed,

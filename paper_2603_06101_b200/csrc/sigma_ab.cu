@@ -648,7 +648,50 @@ void launch_ks(const AbPlan& pl, const AbParams& prm, int grid, cudaStream_t st)
     SBG_LAUNCH_CHECK();
 }
 
+// Generic opposite-spin term for sectors outside the tensor-core kernel's limits (more than 136
+// pair rows, more than 68 alpha links, more than 32767 beta strings): the gather form straight from
+// the reference's link tables (sigma.hpp:27-50),
+//   y(Ia, Ib) += sum_{l in links(Ia)} sum_{m in links(Ib)} s_l s_m V'(pair_l, pair_m) x(J_l, J_m)
+//                + e_core x(Ia, Ib).
+// One warp per (row, 32-column block), one lane per column; plain FP64 FMAs.
+__global__ void k_sigma_ab_direct(const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ Vp,
+                                  int npair, const Excitation* __restrict__ la, int La, const Excitation* __restrict__ lb,
+                                  int Lb, int64_t row_lo, int64_t nrows, int64_t NB, int64_t ld, double e_core) {
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t nblk = (NB + 31) / 32;
+    if (warp >= nrows * nblk) return;
+    const int64_t r = warp / nblk, Ib = (warp % nblk) * 32 + lane;
+    const int64_t Ia = row_lo + r;
+    if (Ib >= NB) return;
+    double acc = 0.0;
+    const Excitation* lbi = lb + Ib * Lb;
+    for (int l = 0; l < La; ++l) {
+        const Excitation e = la[Ia * La + l];
+        const double* vrow = Vp + (size_t)pair_sym(e.p, e.q) * npair;
+        const double* xr = x + (int64_t)e.target * ld;
+        double part = 0.0;
+        for (int m = 0; m < Lb; ++m) {
+            const Excitation f = lbi[m];
+            part = fma(f.sign * vrow[pair_sym(f.p, f.q)], xr[f.target], part);
+        }
+        acc = fma(e.sign, part, acc);
+    }
+    y[r * ld + Ib] += acc + e_core * x[Ia * ld + Ib];
+}
+
 }  // namespace
+
+void launch_sigma_ab_direct(const double* x_full, double* y_local, const double* Vp, int npair, const Excitation* la,
+                            int La, const Excitation* lb, int Lb, int64_t row_lo, int64_t row_hi, int64_t NB, int64_t ld,
+                            double e_core, cudaStream_t st) {
+    const int64_t nrows = row_hi - row_lo;
+    if (nrows <= 0) return;
+    const int64_t warps = nrows * ((NB + 31) / 32);
+    k_sigma_ab_direct<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(x_full, y_local, Vp, npair, la, La, lb, Lb,
+                                                                           row_lo, nrows, NB, ld, e_core);
+    SBG_LAUNCH_CHECK();
+}
 
 AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int64_t ld, int nsm) {
     (void)nsm;

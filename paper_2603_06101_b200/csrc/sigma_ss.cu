@@ -220,7 +220,99 @@ __global__ void k_onebody(const double* x, double* y, const Excitation* la, int 
     y[idx] = v;
 }
 
+// Generic same-spin term for sectors with more than 96 pair rows per (n-2)-string: the one-spin
+// two-body operator as a CSR matrix over strings (built on the host from the same normal-ordered
+// pair form as k_sigma_ss), applied to the other spin's contiguous batch dimension:
+//   y(I, c) += sum_J Wss(I, J) x(J, c) for columns c in [col_lo, col_hi).
+// One warp per (output string, 32-column block), one lane per column.
+__global__ void k_sigma_ss_csr(const double* __restrict__ x, double* __restrict__ y, const int64_t* __restrict__ rowptr,
+                               const int* __restrict__ col, const double* __restrict__ val, int64_t nstr, int64_t ldx,
+                               int64_t col_lo, int64_t col_hi) {
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t nblk = (col_hi - col_lo + 31) / 32;
+    if (warp >= nstr * nblk) return;
+    const int64_t I = warp / nblk, c = col_lo + (warp % nblk) * 32 + lane;
+    if (c >= col_hi) return;
+    double acc = 0.0;
+    for (int64_t e = rowptr[I]; e < rowptr[I + 1]; ++e) acc = fma(val[e], x[(int64_t)col[e] * ldx + c], acc);
+    y[I * ldx + c] += acc;
+}
+
 }  // namespace
+
+// host CSR of the one-spin two-body operator sum_{p<r,q<s} W(pr,qs) a+_p a+_r a_s a_q over the
+// n-electron strings of norb orbitals (colex order), phases as in k_sigma_ss
+void build_ss_csr(int norb, int nel, const double* Va, SsCsr& out) {
+    const int npa = norb * (norb - 1) / 2;
+    const int64_t nstr = (int64_t)binom_host_calc(norb, nel);
+    auto rank = [&](uint64_t sb) {
+        uint64_t r = 0;
+        int i = 1;
+        for (int o = 0; o < norb; ++o)
+            if (sb >> o & 1) r += binom_host_calc(o, i++);
+        return (int64_t)r;
+    };
+    auto popb = [](uint64_t sb, int o) { return __builtin_popcountll(sb & (((uint64_t)1 << o) - 1)); };
+    auto phi = [&](uint64_t full, int q, int sq) {  // <K|a_s a_q|K+{q,s}>, q < s
+        return ((popb(full, q) + popb(full ^ ((uint64_t)1 << q), sq)) & 1) ? -1.0 : 1.0;
+    };
+    std::vector<std::vector<std::pair<int, double>>> rows(nstr);
+    // enumerate J in colex order: strings with nel bits (Gosper)
+    if (nel >= 2 && nel <= norb) {
+        uint64_t J = ((uint64_t)1 << nel) - 1;
+        const uint64_t lim = (uint64_t)1 << norb;
+        while (J < lim) {
+            const int64_t jr = rank(J);
+            for (int s = 0; s < norb; ++s) {
+                if (!(J >> s & 1)) continue;
+                for (int q = 0; q < s; ++q) {
+                    if (!(J >> q & 1)) continue;
+                    const uint64_t K = J & ~((uint64_t)1 << q) & ~((uint64_t)1 << s);
+                    const double pj = phi(J, q, s);
+                    const int qs = pair_strict(q, s);
+                    for (int r = 0; r < norb; ++r) {
+                        if (K >> r & 1) continue;
+                        for (int p = 0; p < r; ++p) {
+                            if (K >> p & 1) continue;
+                            const uint64_t I = K | ((uint64_t)1 << p) | ((uint64_t)1 << r);
+                            const double v = phi(I, p, r) * Va[(size_t)pair_strict(p, r) * npa + qs] * pj;
+                            if (v != 0.0) rows[rank(I)].push_back({(int)jr, v});
+                        }
+                    }
+                }
+            }
+            const uint64_t c = J & (~J + 1), rr = J + c;  // next string with the same popcount
+            J = (((rr ^ J) >> 2) / c) | rr;
+        }
+    }
+    out.nstr = nstr;
+    out.rowptr.assign(nstr + 1, 0);
+    out.col.clear();
+    out.val.clear();
+    for (int64_t i = 0; i < nstr; ++i) {
+        auto& rw = rows[i];
+        std::sort(rw.begin(), rw.end());
+        for (size_t k = 0; k < rw.size();) {  // merge duplicate columns (diagonal / single excitations)
+            size_t e = k;
+            double v = 0.0;
+            while (e < rw.size() && rw[e].first == rw[k].first) v += rw[e++].second;
+            out.col.push_back(rw[k].first);
+            out.val.push_back(v);
+            k = e;
+        }
+        out.rowptr[i + 1] = (int64_t)out.col.size();
+    }
+}
+
+void launch_sigma_ss_csr(const SsCsrDev& m, const double* x, double* y, int64_t ldx, int64_t col_lo, int64_t col_hi,
+                         cudaStream_t st) {
+    if (m.nstr == 0 || col_hi <= col_lo) return;
+    const int64_t warps = m.nstr * ((col_hi - col_lo + 31) / 32);
+    k_sigma_ss_csr<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(x, y, m.rowptr, m.col, m.val, m.nstr, ldx,
+                                                                        col_lo, col_hi);
+    SBG_LAUNCH_CHECK();
+}
 
 SsPlan plan_sigma_ss(int norb, int nel) {
     SsPlan pl{};

@@ -544,3 +544,33 @@ def test_sigma_sector_sweep(dev, rest):
             fails.append((norb, nelec, ms2, err))
         op.close()
     assert not fails, fails
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("spec", [(17, 4, 0), (18, 3, 1), (16, 4, 0), (20, 2, 0), (20, 4, 2)])
+def test_sigma_large_orbital_fallbacks(dev, rest, spec):
+    """Sectors outside the tensor-core kernels' limits (more than 136 pair rows for the opposite-spin
+    kernel, more than 96 same-spin pair rows) run on the generic link-table / CSR kernels; sigma
+    still matches the restatement of contract_sigma."""
+    norb, nelec, ms2 = spec
+    h1, eri = rest.synthetic(norb, 40 + norb, 0.06)
+    q = Problem(norb, nelec, ms2, -0.3, h1, eri, f"{norb}o{nelec}e")
+    op = P.FciOperator(to_product(q), max_determinants=2 ** 62)
+    X = np.stack([seeded(op.dim(), s) for s in (4, 5)])
+    Y = op.apply(X)
+    for x, y in zip(X, Y):
+        ref = rest.sigma(q, x, exact=True)
+        assert np.abs(y - ref).max() <= SIGMA_RTOL * np.abs(ref).max()
+    op.close()
+
+
+def test_sbci1_large_orbital_sector_vs_dense(dev, rest):
+    """(17o,2e): both terms on the generic kernels; SBCI1 energies against the dense spectrum."""
+    h1, eri = rest.synthetic(17, 61, 0.06)
+    q = Problem(17, 2, 0, 0.1, h1, eri, "17o2e")
+    H = rest.dense_h(q)
+    ev = np.linalg.eigvalsh(0.5 * (H + H.T))
+    op = P.FciOperator(to_product(q), max_determinants=2 ** 62)
+    res = P.solve_n_states_sbci1(op, 2)
+    assert np.abs(np.array([pp.energy for pp in res.pairs]) - ev[:2]).max() <= 1e-9
+    op.close()
