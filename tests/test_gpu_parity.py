@@ -574,3 +574,29 @@ def test_sbci1_large_orbital_sector_vs_dense(dev, rest):
     res = P.solve_n_states_sbci1(op, 2)
     assert np.abs(np.array([pp.energy for pp in res.pairs]) - ev[:2]).max() <= 1e-9
     op.close()
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("spec,world", [((17, 4, 0), 3), ((16, 4, 0), 2)])
+def test_sharded_sigma_generic_kernels(dev, rest, spec, world):
+    """The generic opposite-spin / CSR same-spin kernels on the sharded path (row offsets of the
+    local rows, the alpha-alpha column window, the beta-beta local transposes)."""
+    from paper_2603_06101_b200.dist import LocalRankGroup
+    norb, nelec, ms2 = spec
+    h1, eri = rest.synthetic(norb, 7 + norb, 0.06)
+    q = Problem(norb, nelec, ms2, 0.2, h1, eri, "shard-generic")
+    prob = to_product(q)
+    single = P.FciOperator(prob, max_determinants=2 ** 62)
+    x = seeded(single.dim(), 21)
+    y1 = single.apply(x)
+    nb = single.n_beta_strings
+    g = LocalRankGroup(world)
+    ops = g.operators(prob)
+    ys = g.run(lambda r, op: op.apply(x), ops)
+    for op, y in zip(ops, ys):
+        sl = slice(op.row_lo * nb, op.row_hi * nb)
+        assert np.abs(y[sl] - y1[sl]).max() <= 1e-12 * np.abs(y1).max()
+    for op in ops:
+        op.close()
+    g.close()
+    single.close()
