@@ -802,8 +802,8 @@ void build_ab_scatter(const AbPlan& pl, const std::vector<uint16_t>& codes, std:
     tile_ent[ntiles] = (uint32_t)ent.size();
 }
 
-// red mode: per tile every (rs, column) entry as target << 16 | negative << 15 | G offset, in
-// target order (neighbouring lanes reduce into neighbouring y elements), padded to 4 entries
+// red mode: per tile every (rs, column) entry as target << 16 | negative << 15 | G offset, in G
+// order, padded to 4 entries
 void build_ab_red_list(const AbPlan& pl, const std::vector<uint16_t>& codes, std::vector<uint32_t>& ent,
                        std::vector<uint32_t>& tile_ent) {
     const int NT = pl.nt, GSTRIDE = pl.nt + 8;  // Tile<NT>::GSTRIDE
@@ -819,7 +819,9 @@ void build_ab_red_list(const AbPlan& pl, const std::vector<uint16_t>& codes, std
                 if (code == 0xFFFF) continue;
                 items.push_back({(uint32_t)(code & 0x7FFF), (uint32_t)((rs * GSTRIDE + c) | (code & 0x8000))});
             }
-        std::stable_sort(items.begin(), items.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+        // kept in G order (rs-major): a warp's shared-memory reads of G are then near-contiguous;
+        // target-sorting them instead (a warp reducing into neighbouring y elements) measured
+        // slightly slower — the row's targets are sparse within a tile either way
         tile_ent[jt] = (uint32_t)ent.size();
         for (auto& it : items) ent.push_back((it.first << 16) | it.second);
         while (ent.size() % 4) ent.push_back(0xFFFFFFFFu);
