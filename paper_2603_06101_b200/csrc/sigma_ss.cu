@@ -22,7 +22,7 @@ namespace {
 
 constexpr int NTS = 32;         // batch columns per tile (one warp-wide reduction segment)
 constexpr int XSTRIDE = NTS + 4;
-constexpr int YSTRIDE = NTS + 4;
+constexpr int YSTRIDE = NTS + 8;  // == 8 mod 16 doubles: conflict-free 16-byte accumulator stores
 #ifndef SBG_SS_TPC
 #define SBG_SS_TPC 128
 #endif
@@ -144,10 +144,8 @@ __global__ void __launch_bounds__(KSS > 16 ? 192 : 128, KSS > 16 ? 2 : SBG_SS_MI
 #pragma unroll
         for (int nb = 0; nb < NTS / 8; ++nb) {
             const int col = nb * 8 + 2 * t;
-            Ys[i0 * YSTRIDE + col] = acc[nb][0];
-            Ys[i0 * YSTRIDE + col + 1] = acc[nb][1];
-            Ys[(i0 + 8) * YSTRIDE + col] = acc[nb][2];
-            Ys[(i0 + 8) * YSTRIDE + col + 1] = acc[nb][3];
+            *reinterpret_cast<double2*>(Ys + i0 * YSTRIDE + col) = make_double2(acc[nb][0], acc[nb][1]);
+            *reinterpret_cast<double2*>(Ys + (i0 + 8) * YSTRIDE + col) = make_double2(acc[nb][2], acc[nb][3]);
         }
         __syncthreads();
         // one warp reduces one 32-column row segment per step: coalesced 256-byte reductions
