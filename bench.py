@@ -331,8 +331,16 @@ def run_ours(args):
     # sbg_sigma call over e2e_steps vectors, which overlaps the copies of neighbouring steps with
     # the sigma builds (the library's two-slot pipeline)
     nvec = args.e2e_steps
-    xh = torch.empty((nvec, n), dtype=torch.float64, pin_memory=True)
-    yh = torch.empty((nvec, n), dtype=torch.float64, pin_memory=True)
+    while True:   # 2 x nvec pinned host vectors (16 GB at c4 with 6); fewer if the host cannot pin that much
+        try:
+            xh = torch.empty((nvec, n), dtype=torch.float64, pin_memory=True)
+            yh = torch.empty((nvec, n), dtype=torch.float64, pin_memory=True)
+            break
+        except RuntimeError:
+            xh = yh = None
+            if nvec <= 2:
+                raise
+            nvec = max(2, nvec // 2)
     xh.uniform_(-1.0, 1.0)
     dp = C.POINTER(C.c_double)
     xp = C.cast(C.c_void_p(xh.data_ptr()), dp)
@@ -346,7 +354,7 @@ def run_ours(args):
         t = torch.tensor([te], dtype=torch.float64, device="cuda")
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         te = t.item()
-    e2e = args.e2e_steps / te
+    e2e = nvec / te
     local_bytes = (op.row_hi - op.row_lo) * op.n_beta_strings * 8
 
     if rank == 0:
