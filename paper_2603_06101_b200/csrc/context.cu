@@ -237,9 +237,13 @@ Context::~Context() {
     if (st) cudaStreamSynchronize(st);
     for (void* p : {(void*)d_sa_, (void*)d_sb_, (void*)d_la_, (void*)d_lb_, (void*)d_h1_, (void*)d_eri_, (void*)d_Vp_,
                     (void*)d_Va_, (void*)d_codes_, (void*)d_sc_tgt_, (void*)d_sc_ent_,
-                    (void*)d_sc_tt_, (void*)d_sc_te_, (void*)d_red_ent_, (void*)d_red_te_, (void*)rws.partial, (void*)rws.result})
+                    (void*)d_sc_tt_, (void*)d_sc_te_, (void*)rws.partial, (void*)rws.result})
         if (p) cudaFree(p);
     if (rws.host) cudaFreeHost(rws.host);
+    for (auto& pr : red_pass_) {
+        cudaFree(pr.first);
+        cudaFree(pr.second);
+    }
     for (auto& sp : csr_mem_)
         for (void* q : sp)
             if (q) cudaFree(q);
@@ -319,10 +323,10 @@ void Context::build_tables(const double* h1, const double* eri) {
     if (have_ab_ && direct_ab_) {
         ensure_links();
     } else if (have_ab_) {
-        d_codes_ = dmalloc<uint16_t>((size_t)ld * ab_.npad);
-        launch_scatter_codes(d_sb_, NB, ld, norb, ab_.npair, ab_.npad, d_codes_, st);
+        d_codes_ = dmalloc<uint16_t>((size_t)ld * ab_.code_ld);
+        launch_scatter_codes(d_sb_, NB, ld, norb, ab_.npair, ab_.code_ld, d_codes_, st);
         launches += 1;
-        std::vector<uint16_t> codes((size_t)ld * ab_.npad);
+        std::vector<uint16_t> codes((size_t)ld * ab_.code_ld);
         SBG_CUDA(cudaMemcpyAsync(codes.data(), d_codes_, codes.size() * 2, cudaMemcpyDeviceToHost, st));
         SBG_CUDA(cudaStreamSynchronize(st));  // Vp host buffer, codes
         std::vector<uint32_t> tgt, tt, te;
@@ -337,13 +341,18 @@ void Context::build_tables(const double* h1, const double* eri) {
         SBG_CUDA(cudaMemcpyAsync(d_sc_tt_, tt.data(), tt.size() * 4, cudaMemcpyHostToDevice, st));
         SBG_CUDA(cudaMemcpyAsync(d_sc_te_, te.data(), te.size() * 4, cudaMemcpyHostToDevice, st));
         if (ab_.red) {
-            std::vector<uint32_t> e32, t32;
-            build_ab_red_list(ab_, codes, e32, t32);
-            d_red_ent_ = dmalloc<uint32_t>(e32.size());
-            d_red_te_ = dmalloc<uint32_t>(t32.size());
-            SBG_CUDA(cudaMemcpyAsync(d_red_ent_, e32.data(), e32.size() * 4, cudaMemcpyHostToDevice, st));
-            SBG_CUDA(cudaMemcpyAsync(d_red_te_, t32.data(), t32.size() * 4, cudaMemcpyHostToDevice, st));
-            SBG_CUDA(cudaStreamSynchronize(st));
+            for (int pass = 0; pass < ab_.npass; ++pass) {  // one reduction list per pair-row block
+                std::vector<uint32_t> e32, t32;
+                build_ab_red_list(ab_, codes, e32, t32, pass * 128);
+                uint32_t* de = dmalloc<uint32_t>(e32.size());
+                uint32_t* dt = dmalloc<uint32_t>(t32.size());
+                SBG_CUDA(cudaMemcpyAsync(de, e32.data(), e32.size() * 4, cudaMemcpyHostToDevice, st));
+                SBG_CUDA(cudaMemcpyAsync(dt, t32.data(), t32.size() * 4, cudaMemcpyHostToDevice, st));
+                SBG_CUDA(cudaStreamSynchronize(st));
+                red_pass_.push_back({de, dt});
+            }
+            d_red_ent_ = red_pass_[0].first;
+            d_red_te_ = red_pass_[0].second;
         }
         SBG_CUDA(cudaStreamSynchronize(st));
     }
@@ -524,6 +533,17 @@ const double* Context::finish_dots(int ndot) {
 //   3. alpha-alpha: same-spin kernel on x, fp64 reductions into y (world>1: column window +
 //      all-to-all of the blocks)
 //   4. alpha-beta + one-body + e_core: sigma_ab, accumulating into y
+// the tensor-core opposite-spin kernel on rows [lo, hi), one launch per pair-row block
+void Context::run_ab(const double* x_full, double* y_rows, int64_t lo, int64_t hi, cudaStream_t s) {
+    for (int pass = 0; pass < ab_.npass; ++pass) {
+        const uint32_t* re = red_pass_.empty() ? nullptr : red_pass_[pass].first;
+        const uint32_t* rt = red_pass_.empty() ? nullptr : red_pass_[pass].second;
+        launch_sigma_ab(ab_, AbScatter{d_sc_tgt_, d_sc_ent_, d_sc_tt_, d_sc_te_, re, rt}, x_full, y_rows, d_Vp_, lo, hi,
+                        e_core, 1, nsm, s, pass);
+        launches += 1;
+    }
+}
+
 void Context::run_ss(int spin, const double* x, double* y, int64_t ldx, int64_t col_lo, int64_t col_hi,
                      cudaStream_t s) {
     if (ss_csr_[spin]) launch_sigma_ss_csr(csr_dev_[spin], x, y, ldx, col_lo, col_hi, s);
@@ -571,14 +591,10 @@ void Context::sigma_rowblocks(const double* x_local, double* y_local, cudaStream
         SBG_CUDA(cudaEventRecord(ev->e[3], s));
     }
     // ---- alpha-beta per block: rows of block i are final after its launch
-    const AbScatter sc{d_sc_tgt_, d_sc_ent_, d_sc_tt_, d_sc_te_, d_red_ent_, d_red_te_};
     for (int i = 0; i < nchunks; ++i) {
         int64_t lo, hi;
         chunk_rows(nchunks, i, &lo, &hi);
-        if (hi > lo) {
-            launch_sigma_ab(ab_, sc, x_local, y_local + lo * ld, d_Vp_, lo, hi, e_core, 1, nsm, s);
-            launches += 1;
-        }
+        if (hi > lo) run_ab(x_local, y_local + lo * ld, lo, hi, s);
         SBG_CUDA(cudaEventRecord(y_done[i], s));
     }
     if (ev) SBG_CUDA(cudaEventRecord(ev->e[4], s));
@@ -682,9 +698,7 @@ void Context::sigma(const double* x_local, double* y_local, cudaStream_t s) {
                                (int)row_len(1), row_lo, row_hi, NB, ld, e_core, s);
         launches += 1;
     } else if (have_ab_) {
-        launch_sigma_ab(ab_, AbScatter{d_sc_tgt_, d_sc_ent_, d_sc_tt_, d_sc_te_, d_red_ent_, d_red_te_}, xf, y_local, d_Vp_, row_lo, row_hi,
-                        e_core, 1, nsm, s);
-        launches += 1;
+        run_ab(xf, y_local, row_lo, row_hi, s);
     } else {
         ensure_links();
         // rows of this rank: the one-body kernel works on full-height buffers; single GPU only

@@ -160,6 +160,8 @@ private:
     bool has_ss(int spin) const { return ss_csr_[spin] || (spin ? ssb_.P : ssa_.P) > 0; }
     // same-spin term of one spin on a column window (x, y: rows = that spin's strings)
     void run_ss(int spin, const double* x, double* y, int64_t ldx, int64_t col_lo, int64_t col_hi, cudaStream_t s);
+    void run_ab(const double* x_full, double* y_rows, int64_t lo, int64_t hi, cudaStream_t s);
+    std::vector<std::pair<uint32_t*, uint32_t*>> red_pass_;  // reduction lists per pair-row block
     cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
     // world > 1: the collectives run on their own stream, overlapped with the kernels that do not
     // need their result (beta-beta term during the all-gather, alpha-beta during the alpha-alpha

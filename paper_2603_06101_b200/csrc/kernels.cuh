@@ -30,6 +30,8 @@ struct AbPlan {
     int norb, na_el, nb_el, npair, npad, mb16, extra, K, KS, threads, maxT, maxE, nt, ws, red;
     int k0e;  // ws kernel: occupation column k = 0 as an epilogue rank-1 term (K - 1 divisible by 4)
     int tall; // ws kernel: balanced warp assignment for 5-7 m16 blocks (warps 4-7 span the rest)
+    int npass = 1;    // pair-row blocks of 128 rows (npair > 136); 1 = one pass over all rows
+    int code_ld = 0;  // rows per beta string of the scatter-code table (npad, or npass * 128)
     int64_t NA, NB, ld;
     size_t smem;
 };
@@ -45,9 +47,10 @@ AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int
 void build_ab_scatter(const AbPlan& pl, const std::vector<uint16_t>& codes, std::vector<uint32_t>& tgt,
                       std::vector<uint16_t>& ent, std::vector<uint32_t>& tile_tgt, std::vector<uint32_t>& tile_ent);
 void build_ab_red_list(const AbPlan& pl, const std::vector<uint16_t>& codes, std::vector<uint32_t>& ent,
-                       std::vector<uint32_t>& tile_ent);
+                       std::vector<uint32_t>& tile_ent, int m0 = 0);
 void launch_sigma_ab(const AbPlan& pl, const AbScatter& sc, const double* x_full, double* y_local, const double* Vp,
-                     int64_t row_lo, int64_t row_hi, double e_core, int accumulate, int grid, cudaStream_t st);
+                     int64_t row_lo, int64_t row_hi, double e_core, int accumulate, int grid, cudaStream_t st,
+                     int pass = 0);
 // generic fallback outside plan_sigma_ab's limits: y(local rows) += sigma_ab + e_core x from the link tables
 void launch_sigma_ab_direct(const double* x_full, double* y_local, const double* Vp, int npair, const Excitation* la,
                             int La, const Excitation* lb, int Lb, int64_t row_lo, int64_t row_hi, int64_t NB, int64_t ld,

@@ -57,6 +57,8 @@ struct AbParams {
     int red;  // k_sigma_ab_ws: 1 = scatter by red.global.add into y (no sigma row in shared memory)
     const uint32_t* ent32;      // red mode, per tile: target << 16 | negative << 15 | G offset
     const uint32_t* tile_ent32; // [ntiles+1] offsets into ent32 (multiples of 4)
+    int m0;                     // first pair row of this pass (pair-row blocks when npair > 136)
+    int add_ecore;              // this pass adds e_core * x
 };
 
 // Software pipeline per alpha row, one __syncthreads per tile: iteration `it` prefetches D(it+1)
@@ -341,6 +343,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
             bar_sync(BAR_KLIST, kWsThreads);   // K-list of row ia ready (built by the loader warps)
             const uint64_t sa = string_unrank((uint64_t)ia, p.na_el, norb);
             auto aval = [&](int rs, int k) -> double {
+                rs += p.m0;  // pair-row block of this pass
                 if (rs >= npair || k >= p.K) return 0.0;
                 const int pr = sPair[k];
                 if (pr == -1) {
@@ -616,7 +619,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
             cp_async_wait<0>();
             const double* xr = p.x + ia * p.ld;
             if (p.red) {  // y already accumulates the reductions; add e_core * x the same way
-                if (p.e_core != 0.0)
+                if (p.e_core != 0.0 && p.add_ecore)
                     for (int64_t c = stid; c < p.NB; c += kWsHalf) red_add_f64(yrow + c, p.e_core * xr[c]);
                 continue;
             }
@@ -705,7 +708,16 @@ AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int
     pl.npair = norb * (norb + 1) / 2;
     pl.K = 1 + na_el * (norb - na_el);
     pl.KS = (pl.K + 3) / 4;
-    const int full = pl.npair / 16, rem = pl.npair % 16;
+    // more pair rows than eight MMA warps + one m8 block hold (norb > 16): passes over blocks of
+    // 128 pair rows (warp-specialized reduction kernel only)
+    const int red_default = !(getenv("SBG_AB_RED") && atoi(getenv("SBG_AB_RED")) == 0);
+    pl.npass = 1;
+    int mrows = pl.npair;
+    if (pl.npair > 136 && red_default) {
+        pl.npass = (pl.npair + 127) / 128;
+        mrows = 128;
+    }
+    const int full = mrows / 16, rem = mrows % 16;
     // default: k_sigma_ab_ws with reductions into y (SBG_AB_RED=0 selects the shared-memory sigma
     // row with the target-sorted segment scatter, SBG_AB_WS then picks its warp-specialized form)
     const char* red_env = getenv("SBG_AB_RED");
@@ -730,6 +742,7 @@ AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int
             pl.extra = 0;
         }
         pl.npad = pl.extra ? 16 * pl.mb16 + 8 : 16 * pl.mb16;
+        pl.code_ld = pl.npass > 1 ? pl.npass * 128 : pl.npad;  // rows of the scatter-code table
         pl.threads = 32 * pl.mb16;
         pl.nt = nt;
         // scatter-list buffers: bounded by the tile's valid (rs, column) entries
@@ -779,7 +792,7 @@ void build_ab_scatter(const AbPlan& pl, const std::vector<uint16_t>& codes, std:
         items.clear();
         for (int rs = 0; rs < pl.npad; ++rs)
             for (int c = 0; c < NT; ++c) {
-                const uint16_t code = codes[(size_t)(jt * NT + c) * pl.npad + rs];
+                const uint16_t code = codes[(size_t)(jt * NT + c) * pl.code_ld + rs];
                 if (code == 0xFFFF) continue;
                 items.push_back({(uint32_t)(code & 0x7FFF), (uint16_t)((rs * GSTRIDE + c) | (code & 0x8000))});
             }
@@ -805,7 +818,7 @@ void build_ab_scatter(const AbPlan& pl, const std::vector<uint16_t>& codes, std:
 // red mode: per tile every (rs, column) entry as target << 16 | negative << 15 | G offset, in G
 // order, padded to 4 entries
 void build_ab_red_list(const AbPlan& pl, const std::vector<uint16_t>& codes, std::vector<uint32_t>& ent,
-                       std::vector<uint32_t>& tile_ent) {
+                       std::vector<uint32_t>& tile_ent, int m0) {
     const int NT = pl.nt, GSTRIDE = pl.nt + 8;  // Tile<NT>::GSTRIDE
     const int64_t ntiles = pl.ld / NT;
     ent.clear();
@@ -815,7 +828,8 @@ void build_ab_red_list(const AbPlan& pl, const std::vector<uint16_t>& codes, std
         items.clear();
         for (int rs = 0; rs < pl.npad; ++rs)
             for (int c = 0; c < NT; ++c) {
-                const uint16_t code = codes[(size_t)(jt * NT + c) * pl.npad + rs];
+                if (rs + m0 >= pl.npair) continue;
+                const uint16_t code = codes[(size_t)(jt * NT + c) * pl.code_ld + rs + m0];
                 if (code == 0xFFFF) continue;
                 items.push_back({(uint32_t)(code & 0x7FFF), (uint32_t)((rs * GSTRIDE + c) | (code & 0x8000))});
             }
@@ -831,7 +845,7 @@ void build_ab_red_list(const AbPlan& pl, const std::vector<uint16_t>& codes, std
 }
 
 void launch_sigma_ab(const AbPlan& pl, const AbScatter& sc, const double* x_full, double* y_local, const double* Vp,
-                     int64_t row_lo, int64_t row_hi, double e_core, int accumulate, int grid, cudaStream_t st) {
+                     int64_t row_lo, int64_t row_hi, double e_core, int accumulate, int grid, cudaStream_t st, int pass) {
     ensure_binomials();
     if (row_hi <= row_lo) return;
     AbParams prm{};
@@ -845,6 +859,9 @@ void launch_sigma_ab(const AbPlan& pl, const AbScatter& sc, const double* x_full
     prm.red = pl.red;
     prm.ent32 = sc.ent32;
     prm.tile_ent32 = sc.tile_ent32;
+    prm.m0 = pass * 128;
+    prm.add_ecore = pass == 0;
+    if (pass > 0 && !(pl.red && pl.ws)) throw InvalidArgument("sigma_ab: pair-row passes need the reduction kernel");
     if (pl.red && !accumulate) throw InvalidArgument("sigma_ab: reduction mode needs an initialised y");
     prm.norb = pl.norb;
     prm.na_el = pl.na_el;

@@ -547,11 +547,15 @@ def test_sigma_sector_sweep(dev, rest):
 
 
 @pytest.mark.timeout(900)
+@pytest.mark.parametrize("direct", [False, True])
 @pytest.mark.parametrize("spec", [(17, 4, 0), (18, 3, 1), (16, 4, 0), (20, 2, 0), (20, 4, 2)])
-def test_sigma_large_orbital_fallbacks(dev, rest, spec):
-    """Sectors outside the tensor-core kernels' limits (more than 136 pair rows for the opposite-spin
-    kernel, more than 96 same-spin pair rows) run on the generic link-table / CSR kernels; sigma
-    still matches the restatement of contract_sigma."""
+def test_sigma_large_orbital_fallbacks(dev, rest, monkeypatch, spec, direct):
+    """Sectors beyond one pass of the tensor-core kernels: more than 136 pair rows (the opposite-spin
+    kernel runs in 128-row pair blocks, or — deterministic mode, SBG_AB_RED=0 — on the generic
+    link-table kernel) and more than 96 same-spin pair rows (CSR kernel); sigma still matches the
+    restatement of contract_sigma."""
+    if direct:
+        monkeypatch.setenv("SBG_AB_RED", "0")
     norb, nelec, ms2 = spec
     h1, eri = rest.synthetic(norb, 40 + norb, 0.06)
     q = Problem(norb, nelec, ms2, -0.3, h1, eri, f"{norb}o{nelec}e")
