@@ -42,8 +42,10 @@ struct SsParams {
 
 template <int KSS>
 // up to 4 MMA warps (P <= 64 pairs, KSS <= 16: the BASELINE sectors) with the register cap of 4
-// resident CTAs; 5-6 warps (P <= 96: few electrons in many orbitals) with a looser cap
-__global__ void __launch_bounds__(KSS > 16 ? 192 : 128, KSS > 16 ? 2 : SBG_SS_MINB) k_sigma_ss(const SsParams p) {
+// resident CTAs; 5-6 warps (P <= 96) and 7-8 warps (P <= 128: few electrons in many orbitals) with
+// looser caps
+__global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS > 24 ? 1 : (KSS > 16 ? 2 : SBG_SS_MINB))
+    k_sigma_ss(const SsParams p) {
     constexpr int KPP = KSS * 4;
     extern __shared__ __align__(16) double smem[];
     double* Xs = smem;                        // [2][KPP][XSTRIDE]
@@ -330,7 +332,7 @@ SsPlan plan_sigma_ss(int norb, int nel) {
     const int KPP = pl.KSS * 4;
     const int rows = std::max(KPP, 16 * pl.warps);
     pl.smem = (size_t)(2 * KPP * XSTRIDE + rows * YSTRIDE) * 8 + (size_t)KPP * 8 + (size_t)KPP * 8 + (size_t)KPP * 8 + 16;
-    if (pl.KSS > 24 || pl.warps > 6) throw InvalidArgument("sigma_ss: orbital space too large for this build");
+    if (pl.KSS > 32 || pl.warps > 8) throw InvalidArgument("sigma_ss: orbital space too large for this build");
     return pl;
 }
 
@@ -355,7 +357,8 @@ void launch_sigma_ss(const SsPlan& pl, const double* x, double* y, const double*
     case n: launch_kss<n>(pl, prm, grid, st); break;
         SBG_KSS(1) SBG_KSS(2) SBG_KSS(3) SBG_KSS(4) SBG_KSS(5) SBG_KSS(6) SBG_KSS(7) SBG_KSS(8) SBG_KSS(9)
         SBG_KSS(10) SBG_KSS(11) SBG_KSS(12) SBG_KSS(13) SBG_KSS(14) SBG_KSS(15) SBG_KSS(16) SBG_KSS(17)
-        SBG_KSS(18) SBG_KSS(19) SBG_KSS(20) SBG_KSS(21) SBG_KSS(22) SBG_KSS(23) SBG_KSS(24)
+        SBG_KSS(18) SBG_KSS(19) SBG_KSS(20) SBG_KSS(21) SBG_KSS(22) SBG_KSS(23) SBG_KSS(24) SBG_KSS(25)
+        SBG_KSS(26) SBG_KSS(27) SBG_KSS(28) SBG_KSS(29) SBG_KSS(30) SBG_KSS(31) SBG_KSS(32)
 #undef SBG_KSS
         default: throw InvalidArgument("sigma_ss: unsupported pair count");
     }
