@@ -447,15 +447,24 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
 #pragma unroll
                         for (int e = 0; e < 4; ++e) acc[nb][e] = 0.0;
                     const double* D1 = D + K0 * DSTRIDE;  // rows of the DMMA k range
-                    double bf[2][NBT];
+#ifndef SBG_BF_DEPTH
+#define SBG_BF_DEPTH 2
+#endif
+                    constexpr int BFD = SBG_BF_DEPTH;  // B-fragment register ring (loads BFD-1 k-steps ahead)
+                    double bf[BFD][NBT];
 #pragma unroll
-                    for (int nb = 0; nb < NBT; ++nb) bf[0][nb] = D1[t * DSTRIDE + g + nb * 8];
+                    for (int jj = 0; jj < BFD - 1; ++jj)
+                        if (jj < KS) {
+#pragma unroll
+                            for (int nb = 0; nb < NBT; ++nb) bf[jj][nb] = D1[(4 * jj + t) * DSTRIDE + g + nb * 8];
+                        }
 #pragma unroll
                     for (int j = 0; j < KS; ++j) {
-                        const int cur = j & 1;
-                        if (j + 1 < KS) {
+                        const int cur = j % BFD;
+                        if (j + BFD - 1 < KS) {
 #pragma unroll
-                            for (int nb = 0; nb < NBT; ++nb) bf[cur ^ 1][nb] = D1[(4 * (j + 1) + t) * DSTRIDE + g + nb * 8];
+                            for (int nb = 0; nb < NBT; ++nb)
+                                bf[(j + BFD - 1) % BFD][nb] = D1[(4 * (j + BFD - 1) + t) * DSTRIDE + g + nb * 8];
                         }
 #pragma unroll
                         for (int nb = 0; nb < NBT; ++nb) dmma_16x8x4(acc[nb], a0[j], a1[j], bf[cur][nb]);
