@@ -174,25 +174,21 @@ public:
             b = 1.0;
             c = -k * vz * gs.C_z;
         }
-        // cancellation guard (sbci1.hpp:259-262): norms of y' and x' before committing
-        {
-            Lin L;
-            const int sx = L.in(st.x.p), sy = L.in(st.y.p), sz = L.in(z_.p);
-            const int yn = use_three ? L.out(nullptr, {{sy, 1.0}, {sz, -c}}) : L.out(nullptr, {{sz, -c}});
-            const int xn = L.out(nullptr, {{sx, 1.0}, {yn, b}});
-            L.dot(yn, yn);
-            L.dot(xn, xn);
-            const auto r = L.run(c_);
-            if (std::sqrt(nxx) + std::abs(b) * std::sqrt(r[0]) > 1e6 * std::max(std::sqrt(r[1]), 1e-300)) {
-                out.outcome = StepOutcome::restart(RestartReason::StallSmallB);
-                return out;
-            }
-        }
-        // commit (sbci1.hpp:263-267): y' = y - c z, Hy' = Hy - c Hz, x' = x + b y', Hx' = Hx + b Hy',
-        // z' = (1/k) Hx' - (E'/k) x'; reductions |z'|^2, |x'|^2 and the deflation overlaps x_c . z'
+        // guard + commit in one pass (sbci1.hpp:259-267): y' = y - c z, Hy' = Hy - c Hz,
+        // x' = x + b y', Hx' = Hx + b Hy', z' = (1/k) Hx' - (E'/k) x' are written into spare
+        // buffers with |z'|^2, |x'|^2, |y'|^2 and the deflation overlaps x_c . z'; the cancellation
+        // guard is then evaluated from those norms and the spares are swapped in only if it passes
+        // (a rejected step leaves the state untouched, as in the reference)
         double zz2, xx2;
         std::vector<double> ovl;
         {
+            if (sp_y_.empty()) {
+                sp_y_ = c_.vec();
+                sp_hy_ = c_.vec();
+                sp_x_ = c_.vec();
+                sp_hx_ = c_.vec();
+                sp_z_ = c_.vec();
+            }
             Lin L;
             const int sx = L.in(st.x.p), sy = L.in(st.y.p), sz = L.in(z_.p), shx = L.in(st.hx.p),
                       shy = L.in(st.hy.p), shz = L.in(hz_.p);
@@ -200,18 +196,28 @@ public:
             const bool fused_ovl = L.fits((int)defl.size());
             if (fused_ovl)
                 for (auto& mm : defl.m) sxc.push_back(L.in(mm.x.p));
-            const int yn = use_three ? L.out(st.y.p, {{sy, 1.0}, {sz, -c}}) : L.out(st.y.p, {{sz, -c}});
-            const int hyn = use_three ? L.out(st.hy.p, {{shy, 1.0}, {shz, -c}}) : L.out(st.hy.p, {{shz, -c}});
-            const int xn = L.out(st.x.p, {{sx, 1.0}, {yn, b}});
-            const int hxn = L.out(st.hx.p, {{shx, 1.0}, {hyn, b}});
-            const int zn = L.out(st.zres.p, {{hxn, 1.0 / k}, {xn, -e_new / k}});
+            const int yn = use_three ? L.out(sp_y_.p, {{sy, 1.0}, {sz, -c}}) : L.out(sp_y_.p, {{sz, -c}});
+            const int hyn = use_three ? L.out(sp_hy_.p, {{shy, 1.0}, {shz, -c}}) : L.out(sp_hy_.p, {{shz, -c}});
+            const int xn = L.out(sp_x_.p, {{sx, 1.0}, {yn, b}});
+            const int hxn = L.out(sp_hx_.p, {{shx, 1.0}, {hyn, b}});
+            const int zn = L.out(sp_z_.p, {{hxn, 1.0 / k}, {xn, -e_new / k}});
             L.dot(zn, zn);
             L.dot(xn, xn);
+            L.dot(yn, yn);
             for (int s : sxc) L.dot(s, zn);
             const auto r = L.run(c_);
             zz2 = r[0];
             xx2 = r[1];
-            ovl.assign(r.begin() + 2, r.end());
+            if (std::sqrt(nxx) + std::abs(b) * std::sqrt(r[2]) > 1e6 * std::max(std::sqrt(xx2), 1e-300)) {
+                out.outcome = StepOutcome::restart(RestartReason::StallSmallB);
+                return out;
+            }
+            std::swap(st.y, sp_y_);
+            std::swap(st.hy, sp_hy_);
+            std::swap(st.x, sp_x_);
+            std::swap(st.hx, sp_hx_);
+            std::swap(st.zres, sp_z_);
+            ovl.assign(r.begin() + 3, r.end());
             if (!fused_ovl) ovl = deflation_overlaps(c_, defl, st.zres);
         }
         g_ph[4] += ms_since(tp);
@@ -287,6 +293,7 @@ public:
     SolverConfig cfg_;
     const std::function<void(const TraceRec&)>& trace_;
     DBuf z_, hz_;
+    DBuf sp_y_, sp_hy_, sp_x_, sp_hx_, sp_z_;  // candidate state of the merged guard + commit pass
 };
 
 
