@@ -263,19 +263,24 @@ public:
 
         // y'_a = y_a - c_aa z_a - c_ab z_b + a_ab x_b ; y'_b = y_b - c_ba z_a - c_bb z_b + a_ba x_a ;
         // x'_a = x_a + b_aa y'_a + b_ab y'_b ; x'_b = x_b + b_ba y'_a + b_bb y'_b   (sbci2.hpp:265-297)
-        auto build = [&](Lin& L, bool write) {
+        // guard + commit in one pass: y', x' of both states go into spare buffers with the six norms
+        // the cancellation guard (sbci2.hpp:299-306) needs; the spares are swapped in only if it
+        // passes, so a rejected step leaves the state untouched as in the reference
+        {
+            if (sp_ya_.empty()) {
+                sp_ya_ = c_.vec();
+                sp_yb_ = c_.vec();
+                sp_xa_ = c_.vec();
+                sp_xb_ = c_.vec();
+            }
+            Lin L;
             const int sya = L.in(st.ya.p), syb = L.in(st.yb.p), sza = L.in(za_.p), szb = L.in(zb_.p),
                       sxa = L.in(st.xa.p), sxb = L.in(st.xb.p);
-            const int ya = L.out(write ? st.ya.p : nullptr, {{sya, 1.0}, {sza, -co.c_aa}, {szb, -co.c_ab}, {sxb, co.a_ab}});
-            const int yb = L.out(write ? st.yb.p : nullptr, {{syb, 1.0}, {sza, -co.c_ba}, {szb, -co.c_bb}, {sxa, co.a_ba}});
-            const int xa = L.out(write ? st.xa.p : nullptr, {{sxa, 1.0}, {ya, co.b_aa}, {yb, co.b_ab}});
-            const int xb = L.out(write ? st.xb.p : nullptr, {{sxb, 1.0}, {ya, co.b_ba}, {yb, co.b_bb}});
-            return std::array<int, 6>{ya, yb, xa, xb, sxa, sxb};
-        };
-        {  // cancellation guard (sbci2.hpp:299-306) before anything is written
-            Lin L;
-            const auto s = build(L, false);
-            for (int k = 0; k < 6; ++k) L.dot(s[k], s[k]);
+            const int ya = L.out(sp_ya_.p, {{sya, 1.0}, {sza, -co.c_aa}, {szb, -co.c_ab}, {sxb, co.a_ab}});
+            const int yb = L.out(sp_yb_.p, {{syb, 1.0}, {sza, -co.c_ba}, {szb, -co.c_bb}, {sxa, co.a_ba}});
+            const int xa = L.out(sp_xa_.p, {{sxa, 1.0}, {ya, co.b_aa}, {yb, co.b_ab}});
+            const int xb = L.out(sp_xb_.p, {{sxb, 1.0}, {ya, co.b_ba}, {yb, co.b_bb}});
+            for (int k : {ya, yb, xa, xb, sxa, sxb}) L.dot(k, k);
             const auto r = L.run(c_);
             const double ya_nm = std::sqrt(r[0]), yb_nm = std::sqrt(r[1]);
             const double ingredients_a = std::sqrt(r[4]) + std::abs(co.b_aa) * ya_nm + std::abs(co.b_ab) * yb_nm;
@@ -285,15 +290,12 @@ public:
                 out.outcome = StepOutcome::restart(RestartReason::StallSmallB);
                 return out;
             }
-        }
-        {  // commit y', x' in place (the elementwise update reads each element before writing it)
-            Lin L;
-            const auto s = build(L, true);
-            L.dot(s[2], s[2]);
-            L.dot(s[3], s[3]);
-            const auto r = L.run(c_);
-            out.xa_norm = std::sqrt(r[0]);
-            out.xb_norm = std::sqrt(r[1]);
+            std::swap(st.ya, sp_ya_);
+            std::swap(st.yb, sp_yb_);
+            std::swap(st.xa, sp_xa_);
+            std::swap(st.xb, sp_xb_);
+            out.xa_norm = std::sqrt(r[2]);
+            out.xb_norm = std::sqrt(r[3]);
         }
         double zz;
         std::vector<double> ovl;
@@ -360,6 +362,7 @@ public:
     Ops o_;
     SolverConfig cfg_;
     DBuf za_, zb_, hza_, hzb_, zrb_next_;
+    DBuf sp_ya_, sp_yb_, sp_xa_, sp_xb_;  // candidate y', x' of the merged guard + commit pass
 };
 
 struct Sbci2PairResult {
