@@ -23,6 +23,7 @@ from __future__ import annotations
 import argparse
 import ctypes as C
 import json
+import math
 import os
 import subprocess
 import sys
@@ -245,11 +246,15 @@ def run_reference(args):
     rates = sorted(s["value"] for s in samples)
     value = rates[len(rates) // 2]
     info = samples[len(samples) // 2]
+    norb, ne = CONFIGS[args.config][0], CONFIGS[args.config][1]
+    n_det = math.comb(norb, ne // 2) ** 2
     out = {"metric": METRIC, "value": value, "unit": "sigma/s", "impl": "reference", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True,
-           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": f"{args.config} sigma build", "norb": CONFIGS[args.config][0],
-                      "nelec": CONFIGS[args.config][1], "ms2": 0, "seed": SEED},
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (pinned BASELINE generator, seed 2603)",
+           "config": {"workload": f"{args.config} sigma build (BASELINE configs[{ {'c2': 2, 'c3': 3, 'c4': 4}[args.config]}])",
+                      "norb": norb, "nelec": ne, "ms2": 0, "n_det": n_det, "vector_bytes": n_det * 8,
+                      "parallelism": f"host cores ({info['cores']} threads)"},
            "cpu_baseline": {k: info[k] for k in ("value", "unit", "cores", "kind", "sample")},
            "e2e": {"value": value, "unit": "sigma/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
