@@ -182,6 +182,10 @@ int sbg_solve_davidson(sbg_ctx* ctx, int nroots, int max_space, const sbg_config
 /* self test of the DMMA fragment layouts used by the sigma kernels (GPU) */
 int sbg_selftest(void);
 
+/* self test of the NCCL collectives used by the sharded path (all-gather, all-reduce, grouped
+ * send/recv) on a one-rank communicator (GPU) */
+int sbg_selftest_nccl(void);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

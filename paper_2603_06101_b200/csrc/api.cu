@@ -535,4 +535,18 @@ int sbg_selftest(void) {
     return SBG_OK;
 }
 
+int sbg_selftest_nccl(void) {
+    int bad = -1;
+    const int rc = guarded([&] {
+        SBG_CUDA(cudaSetDevice(0));
+        bad = sbg::run_nccl_selftest();
+    });
+    if (rc != SBG_OK) return rc;
+    if (bad != 0) {
+        g_err = "NCCL collective self test: " + std::to_string(bad) + " wrong entries";
+        return SBG_EDEVICE;
+    }
+    return SBG_OK;
+}
+
 }  // extern "C"

@@ -184,5 +184,6 @@ void launch_spin_raise(const double* x_full, int64_t ld, int na, int nb, int nor
 
 // ---- selftest.cu ----
 int run_mma_selftest();
+int run_nccl_selftest();
 
 }  // namespace sbg

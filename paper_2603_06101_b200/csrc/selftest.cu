@@ -2,6 +2,9 @@
 // sigma_ss.cu (common.cuh), against a host product. Returns 0 when both shapes match exactly.
 #include <cmath>
 #include <vector>
+#include <nccl.h>
+
+#include "comm.hpp"
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -50,6 +53,40 @@ int run_mma_selftest() {
             if (C16[i * 8 + j] != s) ++bad;
             if (i < 8 && C8[i * 8 + j] != s) ++bad;
         }
+    return bad;
+}
+
+// The production collectives (NcclComm, comm.hpp) on a one-rank NCCL communicator: all-gather into
+// a larger buffer, in-place all-reduce, and a grouped send/recv to self. Multi-rank NCCL needs one
+// GPU per rank; this pins the link against libnccl and the call sequence on the box that has one.
+// Returns the number of wrong entries.
+int run_nccl_selftest() {
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) throw DeviceError("ncclGetUniqueId failed");
+    auto comm = make_nccl_comm(1, 0, &id);
+    const size_t n = 4099;
+    std::vector<double> h(n), out(n);
+    for (size_t i = 0; i < n; ++i) h[i] = 0.5 * (double)i - 17.25;
+    cudaStream_t st;
+    SBG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    double *a, *b, *c;
+    SBG_CUDA(cudaMalloc(&a, n * 8));
+    SBG_CUDA(cudaMalloc(&b, n * 8));
+    SBG_CUDA(cudaMalloc(&c, n * 8));
+    SBG_CUDA(cudaMemcpy(a, h.data(), n * 8, cudaMemcpyHostToDevice));
+    SBG_CUDA(cudaMemset(b, 0, n * 8));
+    SBG_CUDA(cudaMemset(c, 0, n * 8));
+    int bad = 0;
+    comm->all_gather(a, b, n, st);
+    comm->all_reduce_sum(b, n, st);
+    comm->exchange({CommBlock{b, n, 0}}, {CommBlock{c, n, 0}}, st);
+    SBG_CUDA(cudaStreamSynchronize(st));
+    SBG_CUDA(cudaMemcpy(out.data(), c, n * 8, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < n; ++i) bad += out[i] != h[i];
+    cudaFree(a);
+    cudaFree(b);
+    cudaFree(c);
+    cudaStreamDestroy(st);
     return bad;
 }
 

@@ -55,6 +55,11 @@ def test_dmma_fragment_selftest(dev):
     _lib.check(_lib.lib().sbg_selftest())
 
 
+def test_nccl_collectives_selftest(dev):
+    # the production NcclComm (all-gather, all-reduce, grouped send/recv) on a one-rank communicator
+    _lib.check(_lib.lib().sbg_selftest_nccl())
+
+
 def _check_tables_diag(rest, q):
     op = P.FciOperator(to_product(q), max_determinants=2 ** 62)
     try:
