@@ -3,6 +3,8 @@
 
     python oracle/make_golden.py fast      # fixtures, c0, c1 (minutes)
     python oracle/make_golden.py c2solve   # (12e,12o) SBCI1 ground state (~30-60 min, serial reference)
+    python oracle/make_golden.py c34       # (14e,14o) / (16e,16o): tables + diagonal digests from the
+                                           # reference, complete sigma rows from the exact restatement
 
 Outputs: tests/golden/golden_<tag>.json (scalars) and tests/golden/<tag>_*.npy (small arrays).
 Seeded vectors: numpy default_rng(seed).uniform(-1, 1, n_det), normalised (see seeded_vector).
@@ -117,6 +119,61 @@ def c2(solve):
     print("c2", sc, flush=True)
 
 
+def digest(*arrays):
+    import hashlib
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+# complete alpha rows per config for the full-size sigma parity (c3: 12, c4: 6 rows)
+C34_ROWS = {3: 12, 4: 6}
+
+
+def c34_rows(na, idx):
+    k = C34_ROWS[idx]
+    rows = np.random.default_rng(13).choice(na, k - 2, replace=False).tolist()
+    rows += [0, na - 1]          # the first and last alpha strings (edge tiles of the schedule)
+    return np.array(sorted(set(rows)), np.int64)
+
+
+def c34():
+    """(14e,14o) and (16e,16o), where the reference cannot build a full sigma:
+    * strings, link tables and the exact diagonal computed by the REFERENCE ITSELF, stored as
+      SHA-256 digests (bit-exact pins; the arrays are 0.1-1.3 GB), plus the 8 lowest diagonal
+      entries in the reference's stable order (the seed determinants, sbci1.hpp:50-53);
+    * complete sigma rows (every beta string) of a few alpha strings from the restatement's
+      or_sigma_alpha_rows, which reproduces contract_sigma's accumulation order (bit-identical to
+      the reference wherever the reference runs; pinned by tests/test_oracle_pins.py)."""
+    F = Reference()
+    R = Restatement()
+    for idx in (3, 4):
+        c = CONFIGS[idx]
+        P = baseline_problem(idx, R)
+        n = R.ndet(P)
+        na = R.binomial(P.norb, P.n_alpha)
+        t = time.time()
+        strings = F.strings(P.norb, P.n_alpha)
+        p, q, tt, s = F.links(P.norb, P.n_alpha)
+        D = F.diag(P)
+        t_tab = time.time() - t
+        order = np.lexsort((np.arange(n), D))
+        sc = dict(norb=P.norb, nelec=P.nelec, n_strings=na, n_det=n, h1_sum=float(P.h1.sum()), eri_sum=float(P.eri.sum()),
+                  strings_sha256=digest(strings), links_sha256=digest(p, q, tt, s), diag_sha256=digest(D),
+                  diag_min=float(D.min()), diag_lowest=order[:8].tolist(),
+                  diag_lowest_values=D[order[:8]].tolist(), reference_tables_seconds=t_tab)
+        del D, order
+        x = seeded_vector(n)
+        rows = c34_rows(na, idx)
+        t = time.time()
+        vals = R.sigma_alpha_rows(P, x, rows)
+        sc["sigma_alpha_rows_seconds"] = time.time() - t
+        sc["sigma_rows_vector"] = "numpy default_rng(7).uniform(-1, 1, n_det), normalised"
+        save(c["name"], sc, dict(sigma_alpha_rows=rows, sigma_alpha_vals=vals))
+        print(c["name"], {k: v for k, v in sc.items() if "sha" not in k}, flush=True)
+
+
 def methods():
     """Adds the reference's SBCI2 and Davidson records for c0/c1 to their golden JSON files."""
     F = Reference()
@@ -144,3 +201,5 @@ if __name__ == "__main__":
         c2(True)
     elif what == "methods":
         methods()
+    elif what == "c34":
+        c34()

@@ -104,10 +104,21 @@ class Restatement:
                                            C.c_int64(0), C.c_int64(na)))
         return y
 
-    def sigma_sample(self, P, x, nthreads, rows_per_thread, block_rows=4):
+    def bench(self, P, nthreads):
+        """CPU-baseline timing context (or_bench_*): tables and per-thread outputs built once."""
+        return SampleBench(self, P, nthreads)
+
+    def sigma_alpha_rows(self, P, x, alpha_rows, block_rows=8, nthreads=None):
+        """Complete sigma rows (all beta strings) of the given alpha strings, bit-identical to the
+        reference's contract_sigma rows (or_sigma_alpha_rows). Returns len(alpha_rows) x n_beta."""
         x = np.ascontiguousarray(x, np.float64)
-        self._ck(self.lib.or_sigma_sample(*P.args(), _dp(x), int(nthreads), C.c_int64(rows_per_thread),
-                                          int(block_rows)))
+        rows = np.ascontiguousarray(alpha_rows, np.int64)
+        nb = self.binomial(P.norb, P.n_beta)
+        out = np.zeros((len(rows), nb))
+        self._ck(self.lib.or_sigma_alpha_rows(*P.args(), _dp(x), rows.ctypes.data_as(C.c_void_p),
+                                              C.c_int64(len(rows)), int(block_rows), int(nthreads or os.cpu_count() or 1),
+                                              _dp(out)))
+        return out
 
     def dense_h(self, P):
         n = self.ndet(P)
@@ -126,6 +137,37 @@ class Restatement:
         h1 = np.zeros(norb * norb); eri = np.zeros(norb ** 4)
         self._ck(self.lib.or_synthetic(norb, C.c_uint64(seed), C.c_double(offdiag_scale), _dp(h1), _dp(eri)))
         return h1, eri
+
+
+class SampleBench:
+    """Bounded samples of the blocked contract_sigma restatement on host threads (bench.py's CPU
+    legs). Setup (strings, links, absorbed h2e, one n_det output per thread) happens here, outside
+    the timed run()."""
+
+    def __init__(self, rest, P, nthreads):
+        L = rest.lib
+        L.or_bench_create.restype = C.c_void_p
+        L.or_bench_destroy.argtypes = [C.c_void_p]
+        self.rest, self.nthreads = rest, int(nthreads)
+        self.h = L.or_bench_create(*P.args(), self.nthreads)
+        if not self.h:
+            raise RuntimeError(L.or_last_error().decode())
+        self.n_alpha = rest.binomial(P.norb, P.n_alpha)
+
+    def run(self, x, nthreads, rows_per_thread, block_rows=4, row0=0):
+        """Wall seconds of nthreads workers x rows_per_thread intermediate alpha rows each."""
+        sec = C.c_double()
+        self.rest._ck(self.rest.lib.or_bench_run(C.c_void_p(self.h), _dp(x), int(nthreads), C.c_int64(rows_per_thread),
+                                                 int(block_rows), C.c_int64(row0), C.byref(sec)))
+        return sec.value
+
+    def close(self):
+        if self.h:
+            self.rest.lib.or_bench_destroy(C.c_void_p(self.h))
+            self.h = None
+
+    def __del__(self):
+        self.close()
 
 
 class Reference:

@@ -22,6 +22,7 @@
 //   or_synthetic          BASELINE.json integral generator (not in the reference; pinned here)
 #include <algorithm>
 #include <bit>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -259,33 +260,41 @@ int or_diag(int norb, int nelec, int ms2, double e_core, const double* h1, const
     });
 }
 
-// contract_sigma (sigma.hpp:86-137) processed in blocks of `block_rows` alpha rows of the
-// t1/g1 intermediate, so the 2*norb^2*n_det workspace shrinks to 2*norb^2*block_rows*nb.
-// exact=1 runs the blocks twice (alpha scatter of every block, then beta scatter of every
-// block), which reproduces the reference's accumulation order exactly.
-// row_lo/row_hi restrict which intermediate alpha rows are processed (a bounded sample for
-// the CPU baseline timing); pass 0 / n_alpha_strings for the full sigma.
-int or_sigma_blocked(int norb, int nelec, int ms2, double e_core, const double* h1, const double* eri,
-                     const double* x, double* y, int block_rows, int exact, int64_t row_lo, int64_t row_hi) {
-    return guarded([&] {
-        Prob P{norb, nelec, ms2, e_core, h1, eri};
-        auto sa = strings_of(norb, P.na()), sb = strings_of(norb, P.nb());
-        const auto La = links_of(sa, norb), Lb = links_of(sb, norb);
-        const size_t na = sa.size(), nb = sb.size(), ndet = na * nb;
-        const size_t no2 = (size_t)norb * norb;
-        const auto h2e = absorb(P, P.na() + P.nb());
-        // reverse alpha links: for intermediate row K, the (source ia, link) pairs targeting K, in
-        // the reference's scatter order (ia ascending, link order).
-        std::vector<std::vector<std::pair<uint32_t, int>>> rev(na);
+// Tables of one sector for the blocked restatement (built once, reused by every call).
+struct Blocked {
+    Prob P;
+    std::vector<u64> sa, sb;
+    std::vector<std::vector<Link>> La, Lb;
+    std::vector<double> h2e;
+    // reverse alpha links: for intermediate row K, the (source ia, link) pairs targeting K, in the
+    // reference's scatter order (ia ascending, link order)
+    std::vector<std::vector<std::pair<uint32_t, int>>> rev;
+    size_t na = 0, nb = 0, ndet = 0, no2 = 0;
+    explicit Blocked(const Prob& p) : P(p) {
+        sa = strings_of(P.norb, P.na());
+        sb = strings_of(P.norb, P.nb());
+        La = links_of(sa, P.norb);
+        Lb = links_of(sb, P.norb);
+        na = sa.size();
+        nb = sb.size();
+        ndet = na * nb;
+        no2 = (size_t)P.norb * P.norb;
+        h2e = absorb(P, P.na() + P.nb());
+        rev.resize(na);
         for (size_t ia = 0; ia < na; ++ia)
             for (size_t l = 0; l < La[ia].size(); ++l) rev[La[ia][l].target].push_back({(uint32_t)ia, (int)l});
-        std::fill(y, y + ndet, 0.0);
-        const size_t B = (size_t)std::max(1, block_rows);
-        std::vector<double> t1, g1;
+    }
+    // contract_sigma (sigma.hpp:86-137) on intermediate alpha rows [row_lo, row_hi) in blocks of
+    // block_rows, accumulating into y (not cleared here). exact=1 runs the blocks twice (alpha scatter
+    // of every block, then beta scatter of every block): the reference's accumulation order exactly.
+    void run(const double* x, double* y, size_t B, int exact, size_t row_lo, size_t row_hi, std::vector<double>& t1,
+             std::vector<double>& g1) const {
+        const int norb = P.norb;
+        B = std::max<size_t>(1, B);
         const int passes = exact ? 2 : 1;
         for (int pass = 0; pass < passes; ++pass) {
-            for (size_t k0 = (size_t)row_lo; k0 < (size_t)row_hi; k0 += B) {
-                const size_t k1 = std::min((size_t)row_hi, k0 + B), nk = k1 - k0, bd = nk * nb;
+            for (size_t k0 = row_lo; k0 < row_hi; k0 += B) {
+                const size_t k1 = std::min(row_hi, k0 + B), nk = k1 - k0, bd = nk * nb;
                 t1.assign(no2 * bd, 0.0);
                 // phase A restricted to targets in [k0,k1): t1[pq][K,ib] += sign*x[ia,ib]
                 for (size_t K = k0; K < k1; ++K)
@@ -330,29 +339,177 @@ int or_sigma_blocked(int norb, int nelec, int ms2, double e_core, const double* 
                 }
             }
         }
-        if (row_lo == 0 && (size_t)row_hi == na)
-            for (size_t i = 0; i < ndet; ++i) y[i] += P.e_core * x[i];
+    }
+};
+
+// contract_sigma processed in blocks of `block_rows` alpha rows of the t1/g1 intermediate, so the
+// 2*norb^2*n_det workspace shrinks to 2*norb^2*block_rows*nb. row_lo/row_hi restrict which
+// intermediate alpha rows are processed; pass 0 / n_alpha_strings for the full sigma (then
+// e_core * x is added last, as sigma.hpp:135 does).
+int or_sigma_blocked(int norb, int nelec, int ms2, double e_core, const double* h1, const double* eri,
+                     const double* x, double* y, int block_rows, int exact, int64_t row_lo, int64_t row_hi) {
+    return guarded([&] {
+        Blocked T(Prob{norb, nelec, ms2, e_core, h1, eri});
+        std::fill(y, y + T.ndet, 0.0);
+        std::vector<double> t1, g1;
+        T.run(x, y, (size_t)block_rows, exact, (size_t)row_lo, (size_t)row_hi, t1, g1);
+        if (row_lo == 0 && (size_t)row_hi == T.na)
+            for (size_t i = 0; i < T.ndet; ++i) y[i] += e_core * x[i];
     });
 }
 
-// Multithreaded bounded sample of the single-pass blocked restatement: `nthreads` workers each
-// process `rows_per_thread` intermediate alpha rows (disjoint ranges, private outputs). Used only
-// as bench.py's CPU baseline where the verbatim reference cannot run (c3/c4 workspace).
-int or_sigma_sample(int norb, int nelec, int ms2, double e_core, const double* h1, const double* eri,
-                    const double* x, int nthreads, int64_t rows_per_thread, int block_rows) {
+// Complete sigma rows of selected alpha strings, in contract_sigma's exact accumulation order
+// (sigma.hpp:86-137): only intermediate rows K that scatter into a selected row are formed — the
+// row itself (its occupation entries and the phase-E beta scatter) and its single excitations (the
+// link table is symmetric: K -> Ia iff Ia -> K). Phase D contributions reach y[Ia] in ascending K
+// and link order and phase E (K = Ia) comes after all of them, exactly as in the full reference
+// sweep, so each returned row is bit-identical to the reference's sigma row (the same restatement
+// that is pinned bit-for-bit by tests/test_oracle_pins.py). Size-independent: a (16e,16o) row needs
+// ~65 intermediate rows. Phase C (the h2e . t1 product) runs on `nthreads` threads over pq.
+// out: n_rows x n_beta_strings, row-major.
+int or_sigma_alpha_rows(int norb, int nelec, int ms2, double e_core, const double* h1, const double* eri,
+                        const double* x, const int64_t* rows, int64_t n_rows, int block_rows, int nthreads,
+                        double* out) {
     return guarded([&] {
-        const int na = (int)binom(norb, (nelec + ms2) / 2), nb = (int)binom(norb, (nelec - ms2) / 2);
+        Prob P{norb, nelec, ms2, e_core, h1, eri};
+        auto sa = strings_of(norb, P.na()), sb = strings_of(norb, P.nb());
+        const auto La = links_of(sa, norb), Lb = links_of(sb, norb);
+        const size_t na = sa.size(), nb = sb.size();
+        const size_t no2 = (size_t)norb * norb;
+        const auto h2e = absorb(P, P.na() + P.nb());
+        std::vector<int64_t> slot(na, -1);  // alpha row -> output row
+        for (int64_t r = 0; r < n_rows; ++r) {
+            if (rows[r] < 0 || (size_t)rows[r] >= na) throw std::invalid_argument("alpha row out of range");
+            slot[rows[r]] = r;
+        }
+        std::vector<uint32_t> ks;
+        for (int64_t r = 0; r < n_rows; ++r)
+            for (const auto& e : La[rows[r]]) ks.push_back(e.target);
+        std::sort(ks.begin(), ks.end());
+        ks.erase(std::unique(ks.begin(), ks.end()), ks.end());
+        std::vector<std::vector<std::pair<uint32_t, int>>> rev(na);
+        {
+            std::vector<char> need(na, 0);
+            for (auto K : ks) need[K] = 1;
+            for (size_t ia = 0; ia < na; ++ia)
+                for (size_t l = 0; l < La[ia].size(); ++l)
+                    if (need[La[ia][l].target]) rev[La[ia][l].target].push_back({(uint32_t)ia, (int)l});
+        }
+        std::fill(out, out + (size_t)n_rows * nb, 0.0);
+        std::vector<std::vector<double>> g_self(n_rows);  // g1[pq][Ia, :] for phase E
+        const size_t B = (size_t)std::max(1, block_rows);
+        const int nt = std::max(1, nthreads);
+        std::vector<double> t1, g1;
+        for (size_t b0 = 0; b0 < ks.size(); b0 += B) {
+            const size_t nk = std::min(B, ks.size() - b0), bd = nk * nb;
+            t1.assign(no2 * bd, 0.0);
+            for (size_t i = 0; i < nk; ++i) {  // phase A
+                const uint32_t K = ks[b0 + i];
+                for (auto [ia, l] : rev[K]) {
+                    const auto& e = La[ia][l];
+                    double* dst = t1.data() + (size_t)(e.p * norb + e.q) * bd + i * nb;
+                    const double* src = x + (size_t)ia * nb;
+                    for (size_t ib = 0; ib < nb; ++ib) dst[ib] += e.sign * src[ib];
+                }
+            }
+            for (size_t ib = 0; ib < nb; ++ib)  // phase B
+                for (const auto& e : Lb[ib]) {
+                    double* dst = t1.data() + (size_t)(e.p * norb + e.q) * bd;
+                    for (size_t i = 0; i < nk; ++i) dst[i * nb + e.target] += e.sign * x[(size_t)ks[b0 + i] * nb + ib];
+                }
+            g1.assign(no2 * bd, 0.0);  // phase C, pq rows split over threads
+            {
+                std::vector<std::thread> th;
+                for (int t = 0; t < nt; ++t)
+                    th.emplace_back([&, t] {
+                        for (size_t pq = t; pq < no2; pq += nt) {
+                            double* o = g1.data() + pq * bd;
+                            const double* hrow = h2e.data() + pq * no2;
+                            for (size_t rs = 0; rs < no2; ++rs) {
+                                const double c = hrow[rs];
+                                if (c == 0.0) continue;
+                                const double* src = t1.data() + rs * bd;
+                                for (size_t d = 0; d < bd; ++d) o[d] += c * src[d];
+                            }
+                        }
+                    });
+                for (auto& t : th) t.join();
+            }
+            for (size_t i = 0; i < nk; ++i) {  // phase D into the selected rows only
+                const uint32_t K = ks[b0 + i];
+                for (const auto& e : La[K]) {
+                    const int64_t r = slot[e.target];
+                    if (r < 0) continue;
+                    const double* src = g1.data() + (size_t)(e.p * norb + e.q) * bd + i * nb;
+                    double* dst = out + (size_t)r * nb;
+                    for (size_t ib = 0; ib < nb; ++ib) dst[ib] += e.sign * src[ib];
+                }
+                if (slot[K] >= 0) {  // keep g1[.][K, :] for its phase E
+                    auto& gs = g_self[slot[K]];
+                    gs.resize(no2 * nb);
+                    for (size_t pq = 0; pq < no2; ++pq)
+                        std::memcpy(gs.data() + pq * nb, g1.data() + pq * bd + i * nb, nb * 8);
+                }
+            }
+        }
+        for (int64_t r = 0; r < n_rows; ++r) {  // phase E, then e_core * x (sigma.hpp:133-136)
+            const auto& gs = g_self[r];
+            double* dst = out + (size_t)r * nb;
+            for (size_t ib = 0; ib < nb; ++ib)
+                for (const auto& e : Lb[ib]) dst[e.target] += e.sign * gs[(size_t)(e.p * norb + e.q) * nb + ib];
+            const double* xr = x + (size_t)rows[r] * nb;
+            for (size_t ib = 0; ib < nb; ++ib) dst[ib] += P.e_core * xr[ib];
+        }
+    });
+}
+
+// CPU-baseline timing context (bench.py cpu_baseline / --impl reference): the sector tables and
+// one full-length output vector per worker thread are built ONCE here, outside any timed region.
+struct SampleBench {
+    Blocked T;
+    std::vector<std::vector<double>> y;   // per-thread private sigma accumulators (n_det each)
+    std::vector<std::vector<double>> t1, g1;
+    SampleBench(const Prob& p, int nthreads) : T(p), y(nthreads), t1(nthreads), g1(nthreads) {
+        for (auto& v : y) v.assign(T.ndet, 0.0);
+    }
+};
+
+void* or_bench_create(int norb, int nelec, int ms2, double e_core, const double* h1, const double* eri, int nthreads) {
+    try {
+        return new SampleBench(Prob{norb, nelec, ms2, e_core, h1, eri}, std::max(1, nthreads));
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+void or_bench_destroy(void* b) { delete static_cast<SampleBench*>(b); }
+
+// Timed bounded sample of the single-pass blocked restatement: each worker thread processes
+// `rows_per_thread` intermediate alpha rows (disjoint ranges starting at `row0`, wrapping) into its
+// private y. *seconds = wall time from the release of the workers to the last join (steady clock).
+int or_bench_run(void* handle, const double* x, int nthreads, int64_t rows_per_thread, int block_rows, int64_t row0,
+                 double* seconds) {
+    return guarded([&] {
+        auto* b = static_cast<SampleBench*>(handle);
+        if (!b || nthreads < 1 || nthreads > (int)b->y.size()) throw std::invalid_argument("or_bench_run: bad thread count");
+        const int64_t na = (int64_t)b->T.na;
         std::vector<std::thread> th;
         std::vector<int> rc(nthreads, 0);
+        const auto t0 = std::chrono::steady_clock::now();
         for (int t = 0; t < nthreads; ++t)
             th.emplace_back([&, t] {
-                std::vector<double> y((size_t)na * nb);
-                const int64_t lo = (t * rows_per_thread) % na;
-                const int64_t hi = std::min<int64_t>(na, lo + rows_per_thread);
-                rc[t] = or_sigma_blocked(norb, nelec, ms2, e_core, h1, eri, x, y.data(), block_rows, 0, lo, hi);
+                try {
+                    const int64_t lo = (row0 + t * rows_per_thread) % na;
+                    const int64_t hi = std::min<int64_t>(na, lo + rows_per_thread);
+                    b->T.run(x, b->y[t].data(), (size_t)block_rows, 0, (size_t)lo, (size_t)hi, b->t1[t], b->g1[t]);
+                } catch (...) {
+                    rc[t] = 1;
+                }
             });
         for (auto& t : th) t.join();
-        for (int r : rc) if (r) throw std::runtime_error("sample worker failed");
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        for (int r : rc)
+            if (r) throw std::runtime_error("sample worker failed");
     });
 }
 

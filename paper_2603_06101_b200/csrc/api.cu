@@ -4,6 +4,7 @@
 
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <numeric>
 #include <random>
 #include <string>
@@ -12,8 +13,14 @@
 #include "context.hpp"
 #include "solver.hpp"
 
+// One operator handle. The reference's apply is const and callable from several threads at once
+// (operator.hpp:14-18, 47; test_operator.cpp:49-64): every entry point that touches the context's
+// streams, staging slots, scratch or profile ring holds `mu`, and Context chains its sigma builds on
+// the device (ev_order_), so concurrent callers are serialised host-side and device-side while
+// apply_count stays an atomic counter.
 struct sbg_ctx {
     std::unique_ptr<sbg::Context> c;
+    std::mutex mu;
 };
 
 namespace {
@@ -74,6 +81,13 @@ sbg::SolverConfig to_cfg(const sbg_config* c) {
 void require_ctx(const sbg_ctx* ctx) {
     if (!ctx || !ctx->c) throw std::invalid_argument("null sbg_ctx");
     SBG_CUDA(cudaSetDevice(ctx->c->device));
+}
+// the same, holding the context's lock for the rest of the call
+[[nodiscard]] std::unique_lock<std::mutex> lock_ctx(sbg_ctx* ctx) {
+    if (!ctx || !ctx->c) throw std::invalid_argument("null sbg_ctx");
+    std::unique_lock<std::mutex> lk(ctx->mu);
+    SBG_CUDA(cudaSetDevice(ctx->c->device));
+    return lk;
 }
 }  // namespace
 
@@ -251,7 +265,7 @@ int sbg_local_rows(const sbg_ctx* ctx, int64_t* lo, int64_t* hi) {
 
 int sbg_diagonal(sbg_ctx* ctx, double* out) {
     return guarded([&] {
-        require_ctx(ctx);
+        auto lk = lock_ctx(ctx);
         auto& c = *ctx->c;
         c.download_local(c.diagonal().p, out + c.row_lo * c.NB, c.st);
         SBG_CUDA(cudaStreamSynchronize(c.st));
@@ -269,7 +283,7 @@ int sbg_table_sizes(const sbg_ctx* ctx, int spin, int64_t* n_strings, int64_t* r
 
 int sbg_string_tables(sbg_ctx* ctx, int spin, uint64_t* strings, sbg_excitation* links) {
     return guarded([&] {
-        require_ctx(ctx);
+        auto lk = lock_ctx(ctx);
         if (spin != 0 && spin != 1) throw std::invalid_argument("spin must be 0 or 1");
         ctx->c->string_tables(spin, strings, reinterpret_cast<sbg::Excitation*>(links));
     });
@@ -277,7 +291,7 @@ int sbg_string_tables(sbg_ctx* ctx, int spin, uint64_t* strings, sbg_excitation*
 
 int sbg_sigma(sbg_ctx* ctx, const double* x, double* y, int nvec) {
     return guarded([&] {
-        require_ctx(ctx);
+        auto lk = lock_ctx(ctx);
         if (nvec < 0 || (!x && nvec) || (!y && nvec)) throw std::invalid_argument("sbg_sigma: bad arguments");
         auto& c = *ctx->c;
         if (nvec == 0) return;
@@ -345,7 +359,7 @@ int64_t sbg_padded_len(const sbg_ctx* ctx) { return ctx && ctx->c ? ctx->c->padd
 
 int sbg_pack(sbg_ctx* ctx, const double* d_dense_full, double* d_padded_local, void* stream) {
     return guarded([&] {
-        require_ctx(ctx);
+        auto lk = lock_ctx(ctx);
         auto& c = *ctx->c;
         cudaStream_t s = stream ? (cudaStream_t)stream : c.st;
         SBG_CUDA(cudaMemsetAsync(d_padded_local, 0, c.padded_len() * 8, s));
@@ -355,7 +369,7 @@ int sbg_pack(sbg_ctx* ctx, const double* d_dense_full, double* d_padded_local, v
 
 int sbg_unpack(sbg_ctx* ctx, const double* d_padded_local, double* d_dense_local, void* stream) {
     return guarded([&] {
-        require_ctx(ctx);
+        auto lk = lock_ctx(ctx);
         auto& c = *ctx->c;
         c.unpack_device(d_padded_local, d_dense_local, stream ? (cudaStream_t)stream : c.st);
     });
@@ -363,7 +377,7 @@ int sbg_unpack(sbg_ctx* ctx, const double* d_padded_local, double* d_dense_local
 
 int sbg_sigma_padded(sbg_ctx* ctx, const double* dx, double* dy, void* stream) {
     return guarded([&] {
-        require_ctx(ctx);
+        auto lk = lock_ctx(ctx);
         auto& c = *ctx->c;
         c.sigma(dx, dy, stream ? (cudaStream_t)stream : c.st);
     });
@@ -371,7 +385,7 @@ int sbg_sigma_padded(sbg_ctx* ctx, const double* dx, double* dy, void* stream) {
 
 int sbg_sigma_device(sbg_ctx* ctx, const double* d_x, double* d_y, void* stream) {
     return guarded([&] {
-        require_ctx(ctx);
+        auto lk = lock_ctx(ctx);
         auto& c = *ctx->c;
         cudaStream_t s = stream ? (cudaStream_t)stream : c.st;
         double *px = c.io_x(), *py = c.io_y();
@@ -386,18 +400,18 @@ uint64_t sbg_apply_count(const sbg_ctx* ctx) { return ctx && ctx->c ? ctx->c->ap
 void sbg_reset_apply_count(sbg_ctx* ctx) {
     if (ctx && ctx->c) ctx->c->applies().store(0);
 }
-uint64_t sbg_kernel_launches(const sbg_ctx* ctx) { return ctx && ctx->c ? ctx->c->launches : 0; }
+uint64_t sbg_kernel_launches(const sbg_ctx* ctx) { return ctx && ctx->c ? ctx->c->launches.load() : 0; }
 
 int sbg_profile_reset(sbg_ctx* ctx) {
     return guarded([&] {
-        require_ctx(ctx);
+        auto lk = lock_ctx(ctx);
         ctx->c->profile_reset();
     });
 }
 
 int sbg_profile_read(sbg_ctx* ctx, double* ms, int64_t* calls) {
     return guarded([&] {
-        require_ctx(ctx);
+        auto lk = lock_ctx(ctx);
         ctx->c->profile_read(ms, calls);
     });
 }
@@ -413,7 +427,7 @@ int sbg_sigma_flops(const sbg_ctx* ctx, double* ab, double* ss, double* total) {
 
 int sbg_spin_squared(sbg_ctx* ctx, const double* x, double* out) {
     return guarded([&] {
-        require_ctx(ctx);
+        auto lk = lock_ctx(ctx);
         if (!x || !out) throw std::invalid_argument("sbg_spin_squared: null argument");
         auto& c = *ctx->c;
         double* dx = c.io_x();
@@ -424,7 +438,7 @@ int sbg_spin_squared(sbg_ctx* ctx, const double* x, double* out) {
 
 int sbg_spin_squared_padded(sbg_ctx* ctx, const double* d_x, double* out) {
     return guarded([&] {
-        require_ctx(ctx);
+        auto lk = lock_ctx(ctx);
         if (!d_x || !out) throw std::invalid_argument("sbg_spin_squared_padded: null argument");
         *out = ctx->c->spin_squared(d_x);
     });
@@ -433,7 +447,7 @@ int sbg_spin_squared_padded(sbg_ctx* ctx, const double* d_x, double* out) {
 static int solve_impl(sbg_ctx* ctx, int method, int nroots, int max_space, const sbg_config* cfg, double* energies,
                       double* vectors, sbg_stats* stats, sbg_trace_fn trace, void* trace_user) {
     return guarded([&] {
-        require_ctx(ctx);
+        auto lk = lock_ctx(ctx);
         if (method < 1 || method > 3)
             throw std::invalid_argument("sbg_solve: method must be 1 (sbci1), 2 (sbci2) or 3 (davidson)");
         if (nroots < 1 || nroots > sbg::detail_max_roots)
@@ -538,8 +552,7 @@ int sbg_selftest(void) {
 int sbg_selftest_nccl(void) {
     int bad = -1;
     const int rc = guarded([&] {
-        SBG_CUDA(cudaSetDevice(0));
-        bad = sbg::run_nccl_selftest();
+        bad = sbg::run_nccl_selftest();  // on the calling thread's current device
     });
     if (rc != SBG_OK) return rc;
     if (bad != 0) {

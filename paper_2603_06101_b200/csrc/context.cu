@@ -91,10 +91,23 @@ public:
         SBG_NCCL(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, comm_, s));
     }
     void exchange(const std::vector<CommBlock>& sends, const std::vector<CommBlock>& recvs, cudaStream_t s) override {
+        // the group is always closed, even when a send/recv fails inside it (an open group would
+        // make the next collective hang); the first failure is reported after ncclGroupEnd
         SBG_NCCL(ncclGroupStart());
-        for (const auto& b : sends) SBG_NCCL(ncclSend(b.ptr, b.count, ncclDouble, b.peer, comm_, s));
-        for (const auto& b : recvs) SBG_NCCL(ncclRecv(b.ptr, b.count, ncclDouble, b.peer, comm_, s));
-        SBG_NCCL(ncclGroupEnd());
+        ncclResult_t first = ncclSuccess;
+        const char* what = "";
+        for (const auto& b : sends) {
+            const ncclResult_t r = ncclSend(b.ptr, b.count, ncclDouble, b.peer, comm_, s);
+            if (r != ncclSuccess && first == ncclSuccess) first = r, what = "ncclSend";
+        }
+        for (const auto& b : recvs) {
+            const ncclResult_t r = ncclRecv(b.ptr, b.count, ncclDouble, b.peer, comm_, s);
+            if (r != ncclSuccess && first == ncclSuccess) first = r, what = "ncclRecv";
+        }
+        const ncclResult_t end = ncclGroupEnd();
+        if (first != ncclSuccess)
+            throw DeviceError(std::string("NCCL error ") + ncclGetErrorString(first) + " in " + what);
+        if (end != ncclSuccess) throw DeviceError(std::string("NCCL error ") + ncclGetErrorString(end) + " in ncclGroupEnd");
     }
 
 private:
@@ -207,21 +220,22 @@ Context::Context(int norb_, int nelec_, int ms2_, double e_core_, const double* 
                                  " (pass a larger bound to override)");
     if (world < 1 || rank < 0 || rank >= world) throw InvalidArgument("sbg_create_dist: bad rank/world");
     ld = round_up(NB, 32);
-    ldT = round_up(NA, 32);
     shard_range(NA, rank, world, &row_lo, &row_hi);
     nrows = row_hi - row_lo;
+    ldT = round_up(std::max<int64_t>(nrows, 1), 32);  // beta-beta: only this rank's alpha rows are transposed
 
     SBG_CUDA(cudaSetDevice(device));
     SBG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
     SBG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     SBG_CUDA(cudaEventCreate(&ev0_));
     SBG_CUDA(cudaEventCreate(&ev1_));
+    SBG_CUDA(cudaEventCreateWithFlags(&ev_order_, cudaEventDisableTiming));
 
     if (world > 1) {
         if (local_group && local_group->world != world) throw InvalidArgument("local group: world mismatch");
         comm_ = local_group ? make_local_comm(local_group, rank) : make_nccl_comm(world, rank, nccl_id);
         SBG_CUDA(cudaStreamCreateWithFlags(&comm_st_, cudaStreamNonBlocking));
-        for (cudaEvent_t* e : {&ev_in_, &ev_gathered_, &ev_aa_, &ev_xdone_})
+        for (cudaEvent_t* e : {&ev_in_, &ev_gathered_, &ev_aa_, &ev_xdone_, &ev_ab_})
             SBG_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
 
@@ -254,7 +268,8 @@ Context::~Context() {
         if (c) cudaStreamDestroy(c);
     if (ev0_) cudaEventDestroy(ev0_);
     if (ev1_) cudaEventDestroy(ev1_);
-    for (cudaEvent_t e : {ev_in_, ev_gathered_, ev_aa_, ev_xdone_})
+    if (ev_order_) cudaEventDestroy(ev_order_);
+    for (cudaEvent_t e : {ev_in_, ev_gathered_, ev_aa_, ev_xdone_, ev_ab_})
         if (e) cudaEventDestroy(e);
     if (comm_st_) {
         cudaStreamSynchronize(comm_st_);
@@ -407,11 +422,17 @@ void Context::build_tables(const double* h1, const double* eri) {
                (ss_csr_[1] ? 2.0 * csr_nnz_[1] * NA : 2.0 * ssb_.P * ssb_.P * (double)ssb_.NK * NA);
 
     // workspaces
+    // workspaces beyond the shards: the gathered x is full size by construction; the
+    // alpha-alpha window (all rows x this rank's beta-column window) and its send buffer are
+    // NA x window, the transposed beta-beta operands nrows wide
     if (world > 1) {
         const int64_t per = (NA + world - 1) / world;
         xfull_ = DBuf(per * world * ld);
-        saa_ = DBuf(NA * ld);
-        a2a_send_ = DBuf(NA * ld);
+        shard_range(NB, rank, world, &aa_lo_, &aa_hi_);
+        aa_c0_ = aa_lo_ / 32 * 32;
+        ldw_ = round_up(std::max<int64_t>(aa_hi_ - aa_c0_, 1), 32);
+        saa_ = DBuf(NA * ldw_);
+        a2a_send_ = DBuf(NA * std::max<int64_t>(aa_hi_ - aa_lo_, 1));
         a2a_recv_ = DBuf(nrows * ld);
     }
     if (has_ss(1)) {
@@ -545,9 +566,9 @@ void Context::run_ab(const double* x_full, double* y_rows, int64_t lo, int64_t h
 }
 
 void Context::run_ss(int spin, const double* x, double* y, int64_t ldx, int64_t col_lo, int64_t col_hi,
-                     cudaStream_t s) {
-    if (ss_csr_[spin]) launch_sigma_ss_csr(csr_dev_[spin], x, y, ldx, col_lo, col_hi, s);
-    else launch_sigma_ss(spin ? ssb_ : ssa_, x, y, d_Va_, ldx, col_lo, col_hi, s);
+                     cudaStream_t s, int64_t ldy, int64_t ycol0) {
+    if (ss_csr_[spin]) launch_sigma_ss_csr(csr_dev_[spin], x, y, ldx, col_lo, col_hi, s, ldy, ycol0);
+    else launch_sigma_ss(spin ? ssb_ : ssa_, x, y, d_Va_, ldx, col_lo, col_hi, s, ldy, ycol0);
 }
 
 // rows [lo, hi) of block i of nchunks: equal blocks on a 32-row grid
@@ -560,6 +581,7 @@ void Context::chunk_rows(int nchunks, int i, int64_t* lo, int64_t* hi) const {
 void Context::sigma_rowblocks(const double* x_local, double* y_local, cudaStream_t s, int nchunks,
                               const cudaEvent_t* x_ready, const cudaEvent_t* y_done) {
     if (world != 1 || !have_ab_ || nchunks < 1) throw InvalidArgument("sigma_rowblocks: single-GPU two-spin sectors only");
+    order_begin(s);
     EvSet* ev = next_evset();
     if (ev) {
         SBG_CUDA(cudaEventRecord(ev->e[0], s));
@@ -598,7 +620,16 @@ void Context::sigma_rowblocks(const double* x_local, double* y_local, cudaStream
         SBG_CUDA(cudaEventRecord(y_done[i], s));
     }
     if (ev) SBG_CUDA(cudaEventRecord(ev->e[4], s));
+    order_end(s);
     applies_.fetch_add(1, std::memory_order_relaxed);
+}
+
+void Context::order_begin(cudaStream_t s) {
+    if (order_recorded_) SBG_CUDA(cudaStreamWaitEvent(s, ev_order_, 0));
+}
+void Context::order_end(cudaStream_t s) {
+    SBG_CUDA(cudaEventRecord(ev_order_, s));
+    order_recorded_ = true;
 }
 
 Context::EvSet* Context::next_evset() {
@@ -636,6 +667,7 @@ void Context::profile_read(double* ms, int64_t* calls) {
 }
 
 void Context::sigma(const double* x_local, double* y_local, cudaStream_t s) {
+    order_begin(s);
     EvSet* ev = next_evset();
     if (ev) SBG_CUDA(cudaEventRecord(ev->e[0], s));
     const double* xf = x_local;
@@ -650,16 +682,12 @@ void Context::sigma(const double* x_local, double* y_local, cudaStream_t s) {
     bool y_written = false;
     // ---- beta-beta via the transpose: only this rank's alpha rows (columns of x^T) are needed
     if (has_ss(1)) {
-        if (world == 1) {
-            launch_transpose(x_local, NA, NB, ld, xT_.p, ldT, NB, ldT, 0, s);
-            SBG_CUDA(cudaMemsetAsync(sT_.p, 0, (size_t)NB * ldT * 8, s));
-        } else {
-            launch_transpose(x_local, nrows, NB, ld, xT_.p + row_lo, ldT, NB, nrows, 0, s);
-            SBG_CUDA(cudaMemset2DAsync(sT_.p + row_lo, ldT * 8, 0, nrows * 8, NB, s));
-        }
-        run_ss(1, xT_.p, sT_.p, ldT, row_lo, row_hi, s);
-        // y[r][c] = sT[c][row_lo + r]
-        launch_transpose(sT_.p + row_lo, NB, nrows, ldT, y_local, ld, nrows, ld, 0, s);
+        // x^T of the local rows: [NB][ldT], column r = local alpha row r
+        launch_transpose(x_local, nrows, NB, ld, xT_.p, ldT, NB, ldT, 0, s);
+        SBG_CUDA(cudaMemsetAsync(sT_.p, 0, (size_t)NB * ldT * 8, s));
+        run_ss(1, xT_.p, sT_.p, ldT, 0, nrows, s);
+        // y[r][c] = sT[c][r]
+        launch_transpose(sT_.p, NB, nrows, ldT, y_local, ld, nrows, ld, 0, s);
         launches += 3;
         y_written = true;
     }
@@ -678,10 +706,9 @@ void Context::sigma(const double* x_local, double* y_local, cudaStream_t s) {
             run_ss(0, xf, y_local, ld, 0, NB, s);
             launches += 1;
         } else {
-            int64_t clo, chi;
-            shard_range(NB, rank, world, &clo, &chi);
-            if (chi > clo) SBG_CUDA(cudaMemset2DAsync(saa_.p + clo, ld * 8, 0, (chi - clo) * 8, NA, s));
-            run_ss(0, xf, saa_.p, ld, clo, chi, s);
+            const int64_t clo = aa_lo_, chi = aa_hi_;
+            if (chi > clo) SBG_CUDA(cudaMemset2DAsync(saa_.p + (clo - aa_c0_), ldw_ * 8, 0, (chi - clo) * 8, NA, s));
+            run_ss(0, xf, saa_.p, ld, clo, chi, s, ldw_, aa_c0_);
             launches += 1;
             SBG_CUDA(cudaEventRecord(ev_aa_, s));
             exchange = true;
@@ -707,13 +734,13 @@ void Context::sigma(const double* x_local, double* y_local, cudaStream_t s) {
                        1, s);
         launches += 1;
     }
+    if (exchange) SBG_CUDA(cudaEventRecord(ev_ab_, s));
     if (exchange) {
         // all-to-all of the alpha-alpha column window: send rows of rank r' restricted to my column
         // window; receive my rows of every rank's window
         cudaStream_t cs = comm_st_;
         SBG_CUDA(cudaStreamWaitEvent(cs, ev_aa_, 0));
-        int64_t clo, chi;
-        shard_range(NB, rank, world, &clo, &chi);
+        const int64_t clo = aa_lo_, chi = aa_hi_;
         const int64_t wl = chi - clo;
         std::vector<int64_t> rlo(world), rhi(world), cwl(world), cwh(world);
         for (int r = 0; r < world; ++r) {
@@ -724,7 +751,7 @@ void Context::sigma(const double* x_local, double* y_local, cudaStream_t s) {
         for (int r = 0; r < world; ++r) {
             const int64_t nr = rhi[r] - rlo[r];
             if (nr > 0 && wl > 0)
-                SBG_CUDA(cudaMemcpy2DAsync(a2a_send_.p + off, wl * 8, saa_.p + rlo[r] * ld + clo, ld * 8, wl * 8, nr,
+                SBG_CUDA(cudaMemcpy2DAsync(a2a_send_.p + off, wl * 8, saa_.p + rlo[r] * ldw_ + (clo - aa_c0_), ldw_ * 8, wl * 8, nr,
                                            cudaMemcpyDeviceToDevice, cs));
             off += nr * wl;
         }
@@ -745,6 +772,9 @@ void Context::sigma(const double* x_local, double* y_local, cudaStream_t s) {
             roff += nrows * rw;
         }
         comm_->exchange(sends, recvs, cs);
+        // the blocks travel beside the alpha-beta kernel; adding them into y may too only when that
+        // kernel reduces atomically — otherwise after it (its plain row updates would lose ours)
+        if (!ab_reduces()) SBG_CUDA(cudaStreamWaitEvent(cs, ev_ab_, 0));
         roff = 0;
         for (int r = 0; r < world; ++r) {
             const int64_t rw = cwh[r] - cwl[r];
@@ -761,6 +791,7 @@ void Context::sigma(const double* x_local, double* y_local, cudaStream_t s) {
         SBG_CUDA(cudaStreamWaitEvent(s, ev_xdone_, 0));
     }
     if (ev) SBG_CUDA(cudaEventRecord(ev->e[4], s));
+    order_end(s);
     applies_.fetch_add(1, std::memory_order_relaxed);
 }
 

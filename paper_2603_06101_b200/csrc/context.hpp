@@ -66,7 +66,7 @@ public:
     // sector
     int norb, nelec, ms2, na_el, nb_el;
     double e_core;
-    int64_t NA, NB, ndet, ld, ldT;
+    int64_t NA, NB, ndet, ld, ldT;  // ldT: leading dimension of the transposed local rows [NB][ldT]
     int64_t row_lo, row_hi, nrows;  // alpha rows owned by this rank
     int rank, world, device, nsm;
     cudaStream_t st = nullptr;
@@ -124,7 +124,7 @@ public:
     void profile_read(double* ms, int64_t* calls);
 
     std::atomic<uint64_t>& applies() { return applies_; }
-    uint64_t launches = 0;
+    std::atomic<uint64_t> launches{0};
     double sigma_ms = 0.0;  // accumulated device time of sigma calls (events)
     double flops_ab = 0, flops_ss = 0;
 
@@ -159,15 +159,28 @@ private:
     double csr_nnz_[2] = {0.0, 0.0};
     bool has_ss(int spin) const { return ss_csr_[spin] || (spin ? ssb_.P : ssa_.P) > 0; }
     // same-spin term of one spin on a column window (x, y: rows = that spin's strings)
-    void run_ss(int spin, const double* x, double* y, int64_t ldx, int64_t col_lo, int64_t col_hi, cudaStream_t s);
+    void run_ss(int spin, const double* x, double* y, int64_t ldx, int64_t col_lo, int64_t col_hi, cudaStream_t s,
+                int64_t ldy = 0, int64_t ycol0 = 0);
+    // world > 1: the alpha-alpha term's beta-column window [aa_lo_, aa_hi_) lives in saa_ as
+    // [NA][ldw_] starting at the aligned column aa_c0_
+    int64_t aa_lo_ = 0, aa_hi_ = 0, aa_c0_ = 0, ldw_ = 0;
     void run_ab(const double* x_full, double* y_rows, int64_t lo, int64_t hi, cudaStream_t s);
     std::vector<std::pair<uint32_t*, uint32_t*>> red_pass_;  // reduction lists per pair-row block
     cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+    // device-side order of sigma builds issued on different streams (they share xT_, sT_, xfull_, the
+    // alpha-alpha buffers): every build waits for the previous one's completion event
+    cudaEvent_t ev_order_ = nullptr;
+    bool order_recorded_ = false;
+    void order_begin(cudaStream_t s);
+    void order_end(cudaStream_t s);
     // world > 1: the collectives run on their own stream, overlapped with the kernels that do not
     // need their result (beta-beta term during the all-gather, alpha-beta during the alpha-alpha
     // exchange)
     cudaStream_t comm_st_ = nullptr;
-    cudaEvent_t ev_in_ = nullptr, ev_gathered_ = nullptr, ev_aa_ = nullptr, ev_xdone_ = nullptr;
+    cudaEvent_t ev_in_ = nullptr, ev_gathered_ = nullptr, ev_aa_ = nullptr, ev_xdone_ = nullptr, ev_ab_ = nullptr;
+    // the alpha-beta kernel reduces into y with red.global.add (so the exchanged alpha-alpha blocks
+    // may be added beside it); the direct and deterministic forms read-modify-write y rows instead
+    bool ab_reduces() const { return have_ab_ && !direct_ab_ && ab_.red; }
     struct EvSet {
         cudaEvent_t e[5];
     };

@@ -77,10 +77,11 @@ struct SsCsrDev {
     const double* val = nullptr;
 };
 void build_ss_csr(int norb, int nel, const double* Va, SsCsr& out);
+// y may be a column window of the output: column c of row I at y[I * ldy + c - ycol0] (ldy 0 = ldx)
 void launch_sigma_ss_csr(const SsCsrDev& m, const double* x, double* y, int64_t ldx, int64_t col_lo, int64_t col_hi,
-                         cudaStream_t st);
+                         cudaStream_t st, int64_t ldy = 0, int64_t ycol0 = 0);
 void launch_sigma_ss(const SsPlan& pl, const double* x, double* y, const double* Va, int64_t ldx, int64_t col_lo,
-                     int64_t col_hi, cudaStream_t st);
+                     int64_t col_hi, cudaStream_t st, int64_t ldy = 0, int64_t ycol0 = 0);
 // dst[c][r] = src[r][c] (+ dst if accumulate), for r < R, c < C; dst columns r in [R, dst_cols) zeroed,
 // columns >= dst_cols untouched (a column window of a wider destination).
 void launch_transpose(const double* src, int64_t R, int64_t C, int64_t lds, double* dst, int64_t ldd, int64_t dst_rows,

@@ -57,36 +57,44 @@ int run_mma_selftest() {
 }
 
 // The production collectives (NcclComm, comm.hpp) on a one-rank NCCL communicator: all-gather into
-// a larger buffer, in-place all-reduce, and a grouped send/recv to self. Multi-rank NCCL needs one
+// a larger buffer, in-place all-reduce, and a grouped send/recv to self, on the caller's current device. Multi-rank NCCL needs one
 // GPU per rank; this pins the link against libnccl and the call sequence on the box that has one.
 // Returns the number of wrong entries.
 int run_nccl_selftest() {
+    // RAII: buffers and the stream are released even when an NCCL call throws
+    struct DevBuf {
+        double* p = nullptr;
+        explicit DevBuf(size_t n) { SBG_CUDA(cudaMalloc(&p, n * 8)); }
+        ~DevBuf() { cudaFree(p); }
+    };
+    struct Stream {
+        cudaStream_t s = nullptr;
+        Stream() { SBG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+        ~Stream() {
+            if (s) {
+                cudaStreamSynchronize(s);
+                cudaStreamDestroy(s);
+            }
+        }
+    };
     ncclUniqueId id;
     if (ncclGetUniqueId(&id) != ncclSuccess) throw DeviceError("ncclGetUniqueId failed");
-    auto comm = make_nccl_comm(1, 0, &id);
     const size_t n = 4099;
     std::vector<double> h(n), out(n);
     for (size_t i = 0; i < n; ++i) h[i] = 0.5 * (double)i - 17.25;
-    cudaStream_t st;
-    SBG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    double *a, *b, *c;
-    SBG_CUDA(cudaMalloc(&a, n * 8));
-    SBG_CUDA(cudaMalloc(&b, n * 8));
-    SBG_CUDA(cudaMalloc(&c, n * 8));
-    SBG_CUDA(cudaMemcpy(a, h.data(), n * 8, cudaMemcpyHostToDevice));
-    SBG_CUDA(cudaMemset(b, 0, n * 8));
-    SBG_CUDA(cudaMemset(c, 0, n * 8));
+    Stream st;
+    DevBuf a(n), b(n), c(n);
+    auto comm = make_nccl_comm(1, 0, &id);
+    SBG_CUDA(cudaMemcpy(a.p, h.data(), n * 8, cudaMemcpyHostToDevice));
+    SBG_CUDA(cudaMemset(b.p, 0, n * 8));
+    SBG_CUDA(cudaMemset(c.p, 0, n * 8));
     int bad = 0;
-    comm->all_gather(a, b, n, st);
-    comm->all_reduce_sum(b, n, st);
-    comm->exchange({CommBlock{b, n, 0}}, {CommBlock{c, n, 0}}, st);
-    SBG_CUDA(cudaStreamSynchronize(st));
-    SBG_CUDA(cudaMemcpy(out.data(), c, n * 8, cudaMemcpyDeviceToHost));
+    comm->all_gather(a.p, b.p, n, st.s);
+    comm->all_reduce_sum(b.p, n, st.s);
+    comm->exchange({CommBlock{b.p, n, 0}}, {CommBlock{c.p, n, 0}}, st.s);
+    SBG_CUDA(cudaStreamSynchronize(st.s));
+    SBG_CUDA(cudaMemcpy(out.data(), c.p, n * 8, cudaMemcpyDeviceToHost));
     for (size_t i = 0; i < n; ++i) bad += out[i] != h[i];
-    cudaFree(a);
-    cudaFree(b);
-    cudaFree(c);
-    cudaStreamDestroy(st);
     return bad;
 }
 

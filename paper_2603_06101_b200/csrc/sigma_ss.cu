@@ -33,11 +33,12 @@ constexpr int kMaxTilesPerCta = SBG_SS_TPC;  // column tiles per CTA: amortizes 
 
 struct SsParams {
     const double* x;
-    double* y;
+    double* y;  // column c of row I lives at y[I * ldy + c - ycol0] (a column window of the output)
     const double* Va;
     int norb, nel, P, npa;
     int64_t ldx, col_lo, col_hi;
     int tpc;  // column tiles per CTA
+    int64_t ldy, ycol0;
 };
 
 template <int KSS>
@@ -55,6 +56,7 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
     int* sPi = sJ + KPP;
     double* sPhi = reinterpret_cast<double*>(sPi + KPP);
     int64_t* sRow = reinterpret_cast<int64_t*>(sPhi + KPP);  // row offsets sJ[i] * ldx
+    int64_t* sRowY = sRow + KPP;                             // row offsets sJ[i] * ldy
 
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int w = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
@@ -94,6 +96,7 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
     for (int i = tid; i < KPP; i += nthr) {
         if (i >= P) sJ[i] = sJ[0];  // padding rows read a valid row; their A entries are zero
         sRow[i] = (int64_t)sJ[i] * p.ldx;
+        sRowY[i] = (int64_t)sJ[i] * p.ldy;
     }
 
     double a0[KSS], a1[KSS];
@@ -152,11 +155,11 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
         __syncthreads();
         // one warp reduces one 32-column row segment per step: coalesced 256-byte reductions
         if (c0 + lane >= p.col_lo && c0 + lane < p.col_hi) {
-            double* ybase = p.y + c0 + lane;
+            double* ybase = p.y + (c0 + lane - p.ycol0);
             const double* yl = Ys + lane;
             const int nw = nthr >> 5;
 #pragma unroll 4
-            for (int i = w; i < P; i += nw) red_add_f64(ybase + sRow[i], yl[i * YSTRIDE]);
+            for (int i = w; i < P; i += nw) red_add_f64(ybase + sRowY[i], yl[i * YSTRIDE]);
         }
     }
     cp_async_wait<0>();
@@ -227,7 +230,7 @@ __global__ void k_onebody(const double* x, double* y, const Excitation* la, int 
 // One warp per (output string, 32-column block), one lane per column.
 __global__ void k_sigma_ss_csr(const double* __restrict__ x, double* __restrict__ y, const int64_t* __restrict__ rowptr,
                                const int* __restrict__ col, const double* __restrict__ val, int64_t nstr, int64_t ldx,
-                               int64_t col_lo, int64_t col_hi) {
+                               int64_t col_lo, int64_t col_hi, int64_t ldy, int64_t ycol0) {
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int64_t nblk = (col_hi - col_lo + 31) / 32;
@@ -236,7 +239,7 @@ __global__ void k_sigma_ss_csr(const double* __restrict__ x, double* __restrict_
     if (c >= col_hi) return;
     double acc = 0.0;
     for (int64_t e = rowptr[I]; e < rowptr[I + 1]; ++e) acc = fma(val[e], x[(int64_t)col[e] * ldx + c], acc);
-    y[I * ldx + c] += acc;
+    y[I * ldy + c - ycol0] += acc;
 }
 
 }  // namespace
@@ -306,11 +309,12 @@ void build_ss_csr(int norb, int nel, const double* Va, SsCsr& out) {
 }
 
 void launch_sigma_ss_csr(const SsCsrDev& m, const double* x, double* y, int64_t ldx, int64_t col_lo, int64_t col_hi,
-                         cudaStream_t st) {
+                         cudaStream_t st, int64_t ldy, int64_t ycol0) {
+    if (ldy == 0) ldy = ldx;
     if (m.nstr == 0 || col_hi <= col_lo) return;
     const int64_t warps = m.nstr * ((col_hi - col_lo + 31) / 32);
     k_sigma_ss_csr<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(x, y, m.rowptr, m.col, m.val, m.nstr, ldx,
-                                                                        col_lo, col_hi);
+                                                                        col_lo, col_hi, ldy, ycol0);
     SBG_LAUNCH_CHECK();
 }
 
@@ -331,13 +335,14 @@ SsPlan plan_sigma_ss(int norb, int nel) {
     pl.warps = (pl.P + 15) / 16;
     const int KPP = pl.KSS * 4;
     const int rows = std::max(KPP, 16 * pl.warps);
-    pl.smem = (size_t)(2 * KPP * XSTRIDE + rows * YSTRIDE) * 8 + (size_t)KPP * 8 + (size_t)KPP * 8 + (size_t)KPP * 8 + 16;
+    pl.smem = (size_t)(2 * KPP * XSTRIDE + rows * YSTRIDE) * 8 + (size_t)KPP * 8 * 5 + 16;
     if (pl.KSS > 32 || pl.warps > 8) throw InvalidArgument("sigma_ss: orbital space too large for this build");
     return pl;
 }
 
 void launch_sigma_ss(const SsPlan& pl, const double* x, double* y, const double* Va, int64_t ldx, int64_t col_lo,
-                     int64_t col_hi, cudaStream_t st) {
+                     int64_t col_hi, cudaStream_t st, int64_t ldy, int64_t ycol0) {
+    if (ldy == 0) ldy = ldx;
     ensure_binomials();
     if (pl.P == 0 || pl.NK == 0 || col_hi <= col_lo) return;
     const int64_t ntiles = (col_hi + NTS - 1) / NTS - col_lo / NTS;  // aligned tile grid (see k_sigma_ss)
@@ -349,7 +354,7 @@ void launch_sigma_ss(const SsPlan& pl, const double* x, double* y, const double*
     // (measured: c4 same-spin 33.4 -> 32.8 ms, c3 1.87 ms kept)
     int tpc = ntiles >= 256 ? kMaxTilesPerCta : std::min(kMaxTilesPerCta, 32);
     while (tpc > 4 && pl.NK * ((ntiles + tpc - 1) / tpc) < 8LL * nsm) tpc /= 2;
-    SsParams prm{x, y, Va, pl.norb, pl.nel, pl.P, pl.npa, ldx, col_lo, col_hi, tpc};
+    SsParams prm{x, y, Va, pl.norb, pl.nel, pl.P, pl.npa, ldx, col_lo, col_hi, tpc, ldy, ycol0};
     const int64_t gy = (ntiles + tpc - 1) / tpc;
     dim3 grid((unsigned)pl.NK, (unsigned)gy);
     switch (pl.KSS) {

@@ -165,6 +165,107 @@ def test_sigma_full_size_properties(dev, rest, idx):
     op.close()
 
 
+# ---------------------------------------------------------------- (14e,14o) / (16e,16o): full size
+def _digest(*arrays):
+    import hashlib
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("idx", [3, 4])
+def test_tables_and_diagonal_bit_exact_c34(dev, rest, gold_dir, idx):
+    """Strings, alpha/beta link tables and the exact diagonal at (14e,14o)/(16e,16o) bit-identical to
+    the reference's own (SHA-256 digests written by the reference, oracle/make_golden.py c34) and to
+    the restatement; the 8 lowest diagonal entries in the reference's stable order — the seed
+    determinants, where (16e,16o) has near-ties (fci_operator.hpp:16-57, sbci1.hpp:50-53)."""
+    q = baseline_problem(idx, rest)
+    g = gold(gold_dir, q.name)
+    op = P.FciOperator(to_product(q), max_determinants=2 ** 62)
+    try:
+        for spin in (0, 1):
+            s, l = op.string_tables(spin)
+            assert _digest(s) == g["strings_sha256"]
+            assert _digest(l["p"], l["q"], l["target"], l["sign"]) == g["links_sha256"]
+        d = op.diagonal()
+        assert _digest(d) == g["diag_sha256"]
+        order = np.lexsort((np.arange(len(d)), d))[:8]
+        assert order.tolist() == g["diag_lowest"]
+        assert d[order].tolist() == g["diag_lowest_values"]
+        s, l = op.string_tables(0)
+        assert np.array_equal(s, rest.strings(q.norb, q.n_alpha))
+        rp, rq, rt, rs = rest.links(q.norb, q.n_alpha)
+        assert np.array_equal(l["target"], rt) and np.array_equal(l["sign"], rs)
+        assert np.array_equal(l["p"], rp) and np.array_equal(l["q"], rq)
+        if idx == 3:   # the restatement's diagonal too (c4: 13 s serial, the reference digest covers it)
+            assert np.array_equal(d, rest.diag(q))
+    finally:
+        op.close()
+
+
+def sigma_via_padded(op, x):
+    """The bench's entry point: dense device x -> sbg_pack -> sbg_sigma_padded -> sbg_unpack."""
+    import ctypes as C
+    import torch
+    L = _lib.lib()
+    h = op.handle
+    dx = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    torch.cuda.synchronize()
+    pl = L.sbg_padded_len(h)
+    px = torch.empty(pl, dtype=torch.float64, device="cuda")
+    py = torch.empty_like(px)
+    dy = torch.zeros_like(dx)
+    s = torch.cuda.Stream()
+    sp = C.c_void_p(s.cuda_stream)
+    ptr = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    _lib.check(L.sbg_pack(h, ptr(dx), ptr(px), sp))
+    _lib.check(L.sbg_sigma_padded(h, ptr(px), ptr(py), sp))
+    _lib.check(L.sbg_unpack(h, ptr(py), ptr(dy), sp))
+    s.synchronize()
+    out = dy.cpu().numpy()
+    del dx, px, py, dy
+    torch.cuda.empty_cache()
+    return out
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("idx", [3, 4])
+def test_sigma_complete_rows_c34(dev, rest, gold_dir, idx):
+    """Complete sigma rows (every beta string of selected alpha strings) at (14e,14o)/(16e,16o)
+    against the restatement of contract_sigma in the reference's own accumulation order
+    (tests/golden/c{3,4}_sigma_alpha_*), through BOTH the bench path (sbg_sigma_padded: one
+    opposite-spin launch over all rows) and the host path (sbg_sigma: four row blocks)."""
+    q = baseline_problem(idx, rest)
+    rows = np.load(os.path.join(gold_dir, f"{q.name}_sigma_alpha_rows.npy"))
+    vals = np.load(os.path.join(gold_dir, f"{q.name}_sigma_alpha_vals.npy"))
+    op = P.FciOperator(to_product(q), max_determinants=2 ** 62)
+    nb = op.n_beta_strings
+    x = seeded(op.dim())
+    scale = np.abs(vals).max()
+    for y in (sigma_via_padded(op, x), op.apply(x)):
+        got = np.stack([y[r * nb:(r + 1) * nb] for r in rows])
+        assert np.abs(got - vals).max() <= SIGMA_RTOL * scale
+    op.close()
+
+
+@pytest.mark.timeout(1800)
+def test_sbci1_vs_davidson_c4(dev, rest):
+    """(16e,16o), 3 roots (BASELINE configs[4]): GPU SBCI1 energies within 1e-8 Eh of GPU block
+    Davidson (no serial reference energies exist at this size), with <S^2> integral."""
+    q = baseline_problem(4, rest)
+    op = P.FciOperator(to_product(q), max_determinants=2 ** 62)
+    r1 = P.solve_n_states_sbci1(op, 3, want_vectors=False)
+    rd = P.davidson_solve(op, 3, want_vectors=False)
+    e1 = np.array([pp.energy for pp in r1.pairs])
+    ed = np.array([pp.energy for pp in rd.pairs])
+    assert np.abs(e1 - ed).max() <= E_TOL
+    s2 = [st.s_squared for st in r1.summary.states]
+    assert all(abs(v - round(v)) <= 1e-6 for v in s2), s2
+    op.close()
+
+
 @pytest.mark.parametrize("name", ["h4_2e", "h6_4e"])
 def test_sbci1_fixtures_match_reference(dev, gold_dir, name):
     p, _ = fixture(gold_dir, name)
