@@ -8,15 +8,18 @@ and the one the north star's roofline target is quoted on. A "step" is one full 
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c4] [--impl ours|reference]
 
-N > 1 is launched by torchrun: one rank per GPU, the CI vector sharded by alpha-string blocks,
-NCCL all-gather of x + all-reduce + alpha-alpha block exchange inside libsbg ("scaling": strong —
-the total work per step is fixed). The timed region is bracketed by a barrier + device sync on
-both sides and the max over ranks is reported.
+--gpus N > 1 without torchrun re-launches itself under torch.distributed.run (one rank per GPU,
+127.0.0.1 rendezvous) and fails if fewer than N GPUs are visible. Each rank owns a block of alpha
+strings; libsbg all-gathers x, all-reduces the dot buffers and exchanges the alpha-alpha blocks over
+NCCL ("scaling": strong — the total work per step is fixed). The timed region is bracketed by a
+barrier + device sync on both sides and the max over ranks is reported.
 
 --impl reference times the reference's CPU algorithm on the host cores: the reference library
-itself cannot build a (16e,16o) sigma (678 GB workspace), so the blocked restatement
-of contract_sigma (oracle/sbci_oracle.cpp, bit-exact with the reference at <= (10e,10o)) runs a
-bounded sample of intermediate alpha rows on all host threads and the sigma rate is extrapolated.
+itself cannot build a (16e,16o) sigma (678 GB workspace), so the blocked restatement of
+contract_sigma (oracle/sbci_oracle.cpp, bit-identical to the reference's sigma wherever the
+reference runs) processes a bounded sample of intermediate alpha rows on all host threads per step;
+the sigma rate is that sample's rate times the explicit `extrapolation` factor. Nothing of libsbg is
+loaded on that path (integrals from the oracle's copy of the pinned generator).
 """
 from __future__ import annotations
 
@@ -34,11 +37,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {"c2": (12, 12, 0.05), "c3": (14, 14, 0.05), "c4": (16, 16, 0.08)}
+CONFIG_INDEX = {"c2": 2, "c3": 3, "c4": 4}
 SEED = 2603
 METRIC = "sigma_builds_per_s"
+DATA = "synthetic (pinned BASELINE generator, seed 2603)"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -49,9 +54,55 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tte", action="store_true", help="skip the time-to-energy solves")
     ap.add_argument("--tte-full", action="store_true", help="also solve c4 (3 roots, SBCI1/SBCI2/Davidson, ~15 min)")
-    return ap.parse_args()
+    ap.add_argument("--tte-reference", action="store_true",
+                    help="also run the compiled reference's c1 (SBCI1/SBCI2/Davidson) and c2 (SBCI1) solves on the host "
+                         "(~40 min serial)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher check without a GPU: ranks rendezvous over gloo, time a host step, max over ranks")
+    return ap.parse_args(argv)
 
 
+def config_dict(cfg_name, world):
+    """The workload, identical for both arms (the driver compares the two lines' config dicts)."""
+    norb, ne, _ = CONFIGS[cfg_name]
+    n_det = math.comb(norb, ne // 2) ** 2
+    return {"workload": f"{cfg_name} sigma build (BASELINE configs[{CONFIG_INDEX[cfg_name]}])",
+            "norb": norb, "nelec": ne, "ms2": 0, "n_det": n_det, "vector_bytes": n_det * 8,
+            "parallelism": f"alpha-row shards x{world}" if world > 1 else "single GPU",
+            "l2": "inputs larger than L2 (no flush needed)"}
+
+
+# ------------------------------------------------------------------------------------ launcher
+def maybe_spawn(args):
+    """--gpus N > 1 outside torchrun: re-launch under torch.distributed.run, one rank per GPU."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    if not args.dry_run:
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} requested but {have} GPU(s) visible"}),
+                  flush=True)
+            return 3
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    # NCCL's communicator set-up (rings, NVLS, P2P transport) on stderr, the JSON line alone on stdout
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd, env=env).returncode
+
+
+def env_rank_world():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+# ------------------------------------------------------------------------------------ clocks
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -97,32 +148,171 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.samples)}
 
 
-def cpu_baseline(cfg_name, threads=None, rows_per_thread=None):
-    """Reference algorithm (blocked contract_sigma restatement) on the host cores: bounded sample."""
+# ------------------------------------------------------------------------------------ CPU legs
+def host_info():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count() or 1
+    try:
+        mem = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_AVPHYS_PAGES")
+    except (ValueError, OSError):
+        mem = 0
+    return {"cpu_model": model, "nproc": os.cpu_count() or 1, "usable_cores": usable, "free_ram_bytes": mem}
+
+
+class CpuReference:
+    """The reference's sigma algorithm on the host: the blocked contract_sigma restatement
+    (oracle/sbci_oracle.cpp, TEST INFRASTRUCTURE — only this CPU leg of bench.py executes it). All
+    set-up (integrals, tables, one n_det output per worker thread) is done here, before any timing."""
+
+    def __init__(self, cfg_name, threads=None):
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import numpy as np
+        from oracle import CONFIGS as OC, Problem, Restatement
+        norb, ne, sc = CONFIGS[cfg_name]
+        idx = CONFIG_INDEX[cfg_name]
+        assert OC[idx]["norb"] == norb and OC[idx]["offdiag"] == sc
+        self.rest = Restatement()
+        h1, eri = self.rest.synthetic(norb, SEED, sc)          # the oracle's copy of the pinned generator
+        self.P = Problem(norb, ne, 0, 0.0, h1, eri)
+        self.na = self.rest.binomial(norb, ne // 2)
+        self.n_det = self.na * self.na
+        info = host_info()
+        self.info = info
+        want = threads or info["usable_cores"]
+        # one private n_det output per worker (the scatter targets span the whole vector): cap by RAM
+        if info["free_ram_bytes"]:
+            want = max(1, min(want, int(0.6 * info["free_ram_bytes"] // (self.n_det * 8)) - 1))
+        self.threads = want
+        self.x = np.random.default_rng(7).uniform(-1, 1, self.n_det)
+        self.bench = self.rest.bench(self.P, self.threads)
+        self.row0 = 0
+
+    def sample(self, nthreads, rows_per_thread):
+        """One bounded sample; returns (seconds, rows processed)."""
+        t = self.bench.run(self.x, nthreads, rows_per_thread, block_rows=min(rows_per_thread, 4), row0=self.row0)
+        self.row0 = (self.row0 + nthreads * rows_per_thread) % self.na
+        return t, nthreads * rows_per_thread
+
+    def calibrate(self, nthreads, target_s):
+        """rows per thread so that one sample takes about target_s (one probe row per thread)."""
+        t, _ = self.sample(nthreads, 1)
+        rpt = max(1, int(round(target_s / max(t, 1e-3))))
+        return max(1, min(rpt, self.na // nthreads)), t     # never more than one full sigma per sample
+
+    def close(self):
+        self.bench.close()
+
+
+def cpu_leg(cfg_name, target_s=12.0, serial_s=6.0, steps=1):
+    """Bounded CPU samples on all usable threads (`steps` of them) plus the serial 1-core rate."""
+    cr = CpuReference(cfg_name)
+    rpt, _ = cr.calibrate(cr.threads, target_s)
+    times = [cr.sample(cr.threads, rpt)[0] for _ in range(steps)]
+    t = sorted(times)[len(times) // 2]
+    rows = cr.threads * rpt
+    extrap = cr.na / rows
+    value = 1.0 / (t * extrap)
+    r1, _ = cr.calibrate(1, serial_s)
+    t1, _ = cr.sample(1, r1)
+    serial_sigma_s = t1 * cr.na / r1
+    out = {"value": value, "unit": "sigma/s", "cores": cr.threads, "kind": "port",
+           "sample": (f"{rows} of {cr.na} intermediate alpha rows of the blocked contract_sigma restatement "
+                      f"(oracle/sbci_oracle.cpp:or_bench_run; tables and per-thread outputs allocated before timing), "
+                      f"{cr.threads} threads x {rpt} rows, {t:.2f} s per sample (median of {steps}); "
+                      f"one full sigma = {extrap:.1f} samples = {t * extrap:.0f} s on {cr.threads} threads"),
+           "extrapolation": extrap, "sample_seconds": t, "sample_seconds_all": times,
+           "serial_1core": {"value": 1.0 / serial_sigma_s, "unit": "sigma/s", "sigma_seconds": serial_sigma_s,
+                            "sample": f"{r1} intermediate alpha rows on 1 thread, {t1:.2f} s; x{cr.na / r1:.0f}",
+                            "note": "the reference is serial (SURVEY §0): this is its own core count"},
+           **{k: cr.info[k] for k in ("cpu_model", "nproc", "usable_cores")}}
+    cr.close()
+    return out
+
+
+def reference_solves_on_host(full):
+    """The compiled reference (oracle/_ref/libsbci_ref.so, built from /root/reference) on this host:
+    one sigma at c1 and c2 always (median of 3 / 1), and with `full` its c1 SBCI1/SBCI2/Davidson and
+    c2 SBCI1 solves (serial, tens of minutes)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import numpy as np
-    from oracle import Problem, Restatement
-    import paper_2603_06101_b200 as P
-    norb, ne, sc = CONFIGS[cfg_name]
-    p = P.synthetic_problem(norb, ne, SEED, sc)
-    q = Problem(p.norb, p.nelec, p.ms2, p.e_core, p.h1, p.eri)
-    rest = Restatement()
-    na = rest.binomial(norb, ne // 2)
-    threads = threads or os.cpu_count() or 1
-    rpt = rows_per_thread or {"c2": 58, "c3": 64, "c4": 12}[cfg_name]
-    x = np.random.default_rng(7).uniform(-1, 1, na * na)
-    t0 = time.perf_counter()
-    rest.sigma_sample(q, x, threads, rpt, block_rows=min(rpt, 4))
-    t = time.perf_counter() - t0
-    rows = threads * rpt
-    sigma_s = t * na / rows          # rows run concurrently on `threads` cores
-    return {"value": 1.0 / sigma_s, "unit": "sigma/s", "cores": threads, "kind": "port",
-            "sample": f"{rows} of {na} intermediate alpha rows of the blocked contract_sigma restatement "
-                      f"(oracle/sbci_oracle.cpp:or_sigma_sample), {threads} threads x {rpt} rows, {t:.1f} s; "
-                      f"extrapolated to one full sigma ({sigma_s:.0f} s)",
-            "seconds": t}
+    from oracle import Reference, Restatement, baseline_problem
+    if not Reference.available():
+        return {"unavailable": "oracle/_ref/libsbci_ref.so not built"}
+    F, R = Reference(), Restatement()
+    out = {"host": host_info()}
+    for idx, reps in ((1, 3), (2, 1)):
+        P = baseline_problem(idx, R)
+        x = np.random.default_rng(7).uniform(-1, 1, R.ndet(P))
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            F.sigma(P, x)
+            ts.append(time.perf_counter() - t0)
+        out[f"c{idx}_sigma_seconds_1core"] = sorted(ts)[len(ts) // 2]
+    if full:
+        for idx, nroots, methods in ((1, 4, (1, 2, 3)), (2, 1, (1,))):
+            P = baseline_problem(idx, R)
+            for m in methods:
+                t0 = time.perf_counter()
+                r = F.solve(P, nroots, method=m)
+                out[f"c{idx}_{('sbci1', 'sbci2', 'davidson')[m - 1]}"] = {
+                    "seconds_1core": time.perf_counter() - t0, "matvecs": r["matvecs"],
+                    "energies": r["energies"].tolist()}
+    return out
 
 
+def run_reference(args):
+    """--impl reference: the CPU arm. Each step = one bounded sample of the reference algorithm on
+    all usable host threads; ms_per_step is that measured sample time and `extrapolation` turns it
+    into one full sigma (value = 1 / (sample_seconds * extrapolation))."""
+    rank, world, _ = env_rank_world()
+    if rank != 0:
+        return 0
+    per_step = max(2.0, min(10.0, 150.0 / max(1, args.steps + args.warmup)))
+    cr = CpuReference(args.config)
+    rpt, _ = cr.calibrate(cr.threads, per_step)
+    for _ in range(args.warmup):
+        cr.sample(cr.threads, rpt)
+    times = [cr.sample(cr.threads, rpt)[0] for _ in range(args.steps)]
+    t = sorted(times)[len(times) // 2]
+    rows = cr.threads * rpt
+    extrap = cr.na / rows
+    value = 1.0 / (t * extrap)
+    r1, _ = cr.calibrate(1, 4.0)
+    t1, _ = cr.sample(1, r1)
+    serial_sigma_s = t1 * cr.na / r1
+    cb = {"value": value, "unit": "sigma/s", "cores": cr.threads, "kind": "port",
+          "sample": (f"per step {rows} of {cr.na} intermediate alpha rows ({cr.threads} threads x {rpt} rows) of the "
+                     f"blocked contract_sigma restatement (oracle/sbci_oracle.cpp:or_bench_run), median {t:.2f} s; "
+                     f"one full sigma = {extrap:.1f} steps")}
+    out = {"metric": METRIC, "value": value, "unit": "sigma/s", "impl": "reference", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1000.0,
+           "ms_per_step_meaning": "measured wall time of one bounded sample (the timed unit of this arm)",
+           "extrapolation": extrap, "sigma_seconds": t * extrap,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": DATA,
+           "config": config_dict(args.config, world),
+           "cpu_baseline": cb,
+           "serial_1core": {"value": 1.0 / serial_sigma_s, "unit": "sigma/s", "sigma_seconds": serial_sigma_s,
+                            "sample": f"{r1} rows on 1 thread in {t1:.2f} s"},
+           "host": cr.info,
+           "e2e": {"value": value, "unit": "sigma/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    cr.close()
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------ GPU arm
 def dgemm_peak_tflops(torch):
     n = 4096
     a = torch.randn(n, n, dtype=torch.float64, device="cuda")
@@ -177,8 +367,8 @@ def time_to_energy(full=False):
     """Second half of the BASELINE metric: solves on the GPU through the public API (reference
     SolverConfig defaults), wall time of the solver call with the operator built. c1/c2: energies vs
     the reference's own converged energies (tests/golden, produced by the compiled reference on the
-    same pinned integrals) and the reference's single-core wall time. c3 (and c4 with --tte-full),
-    where the serial reference has no energies: SBCI1 vs GPU block Davidson."""
+    same pinned integrals). c3 (and c4 with --tte-full), where the serial reference has no energies:
+    SBCI1 vs GPU block Davidson."""
     import numpy as np
     import paper_2603_06101_b200 as P
     out = {}
@@ -208,12 +398,12 @@ def time_to_energy(full=False):
                  "energies": e.tolist(), "s_squared": [s.s_squared for s in res.summary.states]}
             if m in ref:
                 r["max_abs_dE_vs_reference_Eh"] = float(np.abs(e - np.array(ref[m]["energies"])).max())
-                r["reference_seconds_1core"] = ref[m]["wall_s"]
                 r["reference_sigma_builds"] = ref[m]["matvecs"]
+                r["reference_seconds_1core_builder_host"] = ref[m]["wall_s"]   # when the golden was made
             rec[m] = r
         # time until every requested state is within 1e-8 Eh of its target: the
         # reference's converged energies where it ran (c1, c2), else the GPU Davidson energies;
-        # measured in a second, traced run (the trace callback adds one small pass per iteration)
+        # measured in a second, traced run (the trace callback costs a host call per iteration)
         target = np.array(ref["sbci1"]["energies"]) if "sbci1" in ref else energies.get("davidson")
         if target is not None:
             for m in methods:
@@ -236,39 +426,49 @@ def time_to_energy(full=False):
     return out
 
 
-def run_reference(args):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
-    # warm-up: one sample (page-in, thread start-up); each timed step is one bounded sample
-    cpu_baseline(args.config)
-    samples = [cpu_baseline(args.config) for _ in range(args.steps)]
-    rates = sorted(s["value"] for s in samples)
-    value = rates[len(rates) // 2]
-    info = samples[len(samples) // 2]
-    norb, ne = CONFIGS[args.config][0], CONFIGS[args.config][1]
-    n_det = math.comb(norb, ne // 2) ** 2
-    out = {"metric": METRIC, "value": value, "unit": "sigma/s", "impl": "reference", "n_gpus": args.gpus,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True,
-           "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic (pinned BASELINE generator, seed 2603)",
-           "config": {"workload": f"{args.config} sigma build (BASELINE configs[{ {'c2': 2, 'c3': 3, 'c4': 4}[args.config]}])",
-                      "norb": norb, "nelec": ne, "ms2": 0, "n_det": n_det, "vector_bytes": n_det * 8,
-                      "parallelism": f"host cores ({info['cores']} threads)"},
-           "cpu_baseline": {k: info[k] for k in ("value", "unit", "cores", "kind", "sample")},
-           "e2e": {"value": value, "unit": "sigma/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+def run_dry(args):
+    """Launcher check (CPU): every rank rendezvous over gloo, times a fixed host step, max over ranks."""
+    import numpy as np
+    import torch.distributed as tdist
+    rank, world, _ = env_rank_world()
+    if world > 1:
+        tdist.init_process_group("gloo")
+    a = np.random.default_rng(rank).standard_normal((256, 256))
+    for _ in range(args.warmup):
+        a @ a
+    if world > 1:
+        tdist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        a = (a @ a) / 256.0
+    t = time.perf_counter() - t0
+    if world > 1:
+        import torch
+        tt = torch.tensor([t], dtype=torch.float64)
+        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
+        t = tt.item()
+        ranks = [None] * world
+        tdist.all_gather_object(ranks, rank)
+    else:
+        ranks = [0]
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "dry_run": True, "n_gpus": world, "ranks": ranks, "steps": args.steps,
+                          "ms_per_step": 1000.0 * t / max(args.steps, 1), "config": config_dict(args.config, world)}),
+              flush=True)
+    if world > 1:
+        tdist.barrier()
+        tdist.destroy_process_group()
+    return 0
 
 
 def run_ours(args):
-    import numpy as np
     import torch
     import paper_2603_06101_b200 as P
     from paper_2603_06101_b200 import _lib, dist as pdist
 
-    rank, world, local = pdist.env_rank_world()
+    rank, world, local = env_rank_world()
     if world != args.gpus:
-        world = max(world, 1)
+        raise SystemExit(f"bench: WORLD_SIZE={world} but --gpus {args.gpus}")
     torch.cuda.set_device(local)
     tdist = None
     if world > 1:
@@ -361,6 +561,7 @@ def run_ours(args):
         te = t.item()
     e2e = nvec / te
     local_bytes = (op.row_hi - op.row_lo) * op.n_beta_strings * 8
+    del xh, yh
 
     if rank == 0:
         clocks = clk.summary()
@@ -368,11 +569,8 @@ def run_ours(args):
         out = {
             "metric": METRIC, "value": value, "unit": "sigma/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (pinned BASELINE generator, seed 2603)",
-            "config": {"workload": f"{args.config} sigma build (BASELINE configs[{ {'c2': 2, 'c3': 3, 'c4': 4}[args.config]}])",
-                       "norb": norb, "nelec": ne, "ms2": 0, "n_det": n, "vector_bytes": n * 8,
-                       "parallelism": f"alpha-row shards x{world}" if world > 1 else "single GPU",
-                       "l2": "inputs larger than L2 (no flush needed)"},
+            "vs_baseline": None, "dtype": "f64", "data": DATA,
+            "config": config_dict(args.config, world),
             "e2e": {"value": e2e, "unit": "sigma/s", "h2d_bytes_per_step": local_bytes * world,
                     "d2h_bytes_per_step": local_bytes * world},
             "gpu_launches": launches,
@@ -395,23 +593,28 @@ def run_ours(args):
         }
         if world == 1 and not args.no_tte:
             out["time_to_energy"] = time_to_energy(args.tte_full)
+            out["reference_on_this_host"] = reference_solves_on_host(args.tte_reference)
         if world == 1 and not args.no_cpu_baseline:
-            cb = cpu_baseline(args.config)
-            out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            out["cpu_baseline"] = cpu_leg(args.config)
         print(json.dumps(out), flush=True)
     op.close()
     if tdist is not None:
         tdist.barrier()
         tdist.destroy_process_group()
+    return 0
 
 
 def main():
     args = parse()
+    rc = maybe_spawn(args)
+    if rc is not None:
+        return rc
+    if args.dry_run:
+        return run_dry(args)
     if args.impl == "reference":
-        run_reference(args)
-    else:
-        run_ours(args)
+        return run_reference(args)
+    return run_ours(args)
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())
