@@ -179,6 +179,19 @@ int sbg_solve(sbg_ctx* ctx, int method, int nroots, const sbg_config* cfg, doubl
 int sbg_solve_davidson(sbg_ctx* ctx, int nroots, int max_space, const sbg_config* cfg, double* energies,
                        double* vectors, sbg_stats* stats, sbg_trace_fn trace, void* trace_user);
 
+/* Plain-vector warm start of one SBCI1 state (solve_state_sbci1(op, pre, defl, x0, E0, cfg, alpha, sink),
+ * sbci1.hpp:477-486): seed x0 (host, n_det, nonzero) with image H x0 (one counted sigma) and energy label
+ * e0; the preconditioner shift is *shift (GroundShiftPreconditioner, precond.hpp:19-47; cfg->clamp_delta
+ * is its clamp); with alpha == 0 the shift tracks the Rayleigh quotient and its final value is written
+ * back to *shift (sbci1.hpp:381, 416). Deflated against ndefl unit, mutually orthogonal vectors defl_x
+ * (host, ndefl x n_det) with energies defl_e; their images defl_hx may be NULL, then they are rebuilt
+ * with one (uncounted) sigma each. Outputs: *energy, vector (unit, nullable), image (H vector, nullable),
+ * stats (nroots = 1). Errors as sbg_solve. */
+int sbg_solve_state_sbci1(sbg_ctx* ctx, const double* x0, double e0, double* shift, int alpha, int ndefl,
+                          const double* defl_x, const double* defl_hx, const double* defl_e, const sbg_config* cfg,
+                          double* energy, double* vector, double* image, sbg_stats* stats, sbg_trace_fn trace,
+                          void* trace_user);
+
 /* self test of the DMMA fragment layouts used by the sigma kernels (GPU) */
 int sbg_selftest(void);
 

@@ -265,7 +265,8 @@ def baseline_problem(idx, rest=None):
 
 
 class RefGpu:
-    """oracle/_ref/libsbci_ref_gpu.so: the reference's own drivers on the B200 sigma."""
+    """oracle/_ref/libsbci_ref_gpu.so: the reference's own drivers on the B200 operator and the
+    product's C++ drop-in header include/sbg.hpp (oracle/ref_gpu_shim.cpp)."""
 
     PATH = os.path.join(HERE, "_ref", "libsbci_ref_gpu.so")
 
@@ -277,10 +278,36 @@ class RefGpu:
         self.lib = C.CDLL(self.PATH)
         self.lib.refgpu_last_error.restype = C.c_char_p
 
+    def _err(self):
+        return self.lib.refgpu_last_error().decode()
+
     def solve(self, P, nroots, method=1):
         e = np.zeros(nroots); it = np.zeros(nroots, np.int32); mv = np.zeros(1, np.uint64)
         rc = self.lib.refgpu_solve(*P.args(), method, nroots, _dp(e), it.ctypes.data_as(C.c_void_p),
                                    mv.ctypes.data_as(C.c_void_p))
         if rc != 0:
-            raise RuntimeError(self.lib.refgpu_last_error().decode())
+            raise RuntimeError(self._err())
         return dict(energies=e, iterations=it, matvecs=int(mv[0]))
+
+    def device_solve(self, P, nroots, method=1, t_max=-1):
+        """sbci::gpu::solve_n_states_* (include/sbg.hpp). Returns (rc, result dict)."""
+        e = np.zeros(nroots); it = np.zeros(nroots, np.int32); mv = np.zeros(1, np.uint64)
+        fs = C.c_int(-1)
+        rc = self.lib.refgpu_device_solve(*P.args(), method, nroots, C.c_long(t_max), _dp(e),
+                                          it.ctypes.data_as(C.c_void_p), mv.ctypes.data_as(C.c_void_p), C.byref(fs))
+        return rc, dict(energies=e, iterations=it, matvecs=int(mv[0]), failed_state=fs.value, error=self._err())
+
+    def concurrent_applies(self, P, nthreads, napply):
+        bad = C.c_int(-2)
+        rc = self.lib.refgpu_concurrent_applies(*P.args(), int(nthreads), int(napply), C.byref(bad))
+        if rc != 0:
+            raise RuntimeError(self._err())
+        return bad.value
+
+    def warm_start(self, P, with_defl):
+        out = np.zeros(8)
+        rc = self.lib.refgpu_warm_start(*P.args(), int(with_defl), _dp(out))
+        if rc != 0:
+            raise RuntimeError(self._err())
+        return dict(e_ref=out[0], e_dev=out[1], it_ref=int(out[2]), it_dev=int(out[3]), overlap=out[4],
+                    shift_ref=out[5], shift_dev=out[6])

@@ -5,7 +5,7 @@ from .fci import (K_DEFAULT_DETERMINANT_GUARD, FciOperator, FciProblem, FcidumpE
                   determinant_count, parse_fcidump, parse_fcidump_file, sigma_apply, synthetic_problem)
 from .solver import (ConvergedEigenpair, MultiStateResult, NonConvergenceError, RunSummary, SolverConfig,
                      StateSummary, TraceRecord, solve_n_states_sbci1, solve_n_states_sbci2,
-                     davidson_solve)
+                     davidson_solve, solve_state_sbci1, Sbci1Result)
 from .trace import (CsvTraceSink, MemoryTraceSink, TeeTraceSink, read_trace_csv, read_trace_csv_file,
                     trace_csv_header)
 
@@ -13,5 +13,5 @@ __all__ = ["K_DEFAULT_DETERMINANT_GUARD", "FciOperator", "FciProblem", "FcidumpE
            "determinant_count", "parse_fcidump", "parse_fcidump_file", "sigma_apply", "synthetic_problem",
            "ConvergedEigenpair", "MultiStateResult", "NonConvergenceError", "RunSummary", "SolverConfig",
            "StateSummary", "TraceRecord", "solve_n_states_sbci1", "solve_n_states_sbci2",
-           "davidson_solve", "CsvTraceSink", "MemoryTraceSink", "TeeTraceSink", "read_trace_csv",
+           "davidson_solve", "solve_state_sbci1", "Sbci1Result", "CsvTraceSink", "MemoryTraceSink", "TeeTraceSink", "read_trace_csv",
            "read_trace_csv_file", "trace_csv_header"]

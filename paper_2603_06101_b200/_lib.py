@@ -101,6 +101,8 @@ def lib() -> C.CDLL:
         "sbg_solve": (C.c_int, [P, C.c_int, C.c_int, C.POINTER(Config), D, D, C.POINTER(Stats), TRACE_FN, P]),
         "sbg_solve_davidson": (C.c_int, [P, C.c_int, C.c_int, C.POINTER(Config), D, D, C.POINTER(Stats), TRACE_FN,
                                          P]),
+        "sbg_solve_state_sbci1": (C.c_int, [P, D, C.c_double, D, C.c_int, C.c_int, D, D, D, C.POINTER(Config), D, D,
+                                            D, C.POINTER(Stats), TRACE_FN, P]),
         "sbg_selftest": (C.c_int, []),
         "sbg_selftest_nccl": (C.c_int, []),
     }
@@ -120,7 +122,8 @@ EXPORTED = ["sbg_last_error", "sbg_version", "sbg_binomial", "sbg_determinant_co
             "sbg_padded_len", "sbg_pack", "sbg_unpack", "sbg_sigma_padded", "sbg_apply_count",
             "sbg_reset_apply_count", "sbg_kernel_launches", "sbg_sigma_flops", "sbg_profile_reset", "sbg_profile_read",
             "sbg_spin_squared", "sbg_spin_squared_padded", "sbg_local_group_create", "sbg_local_group_destroy",
-            "sbg_create_local", "sbg_solve", "sbg_solve_davidson", "sbg_selftest", "sbg_selftest_nccl"]
+            "sbg_create_local", "sbg_solve", "sbg_solve_davidson", "sbg_solve_state_sbci1", "sbg_selftest",
+            "sbg_selftest_nccl"]
 
 
 class SbgError(RuntimeError):

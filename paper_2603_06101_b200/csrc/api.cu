@@ -12,6 +12,7 @@
 #include "../../include/sbg.h"
 #include "context.hpp"
 #include "solver.hpp"
+#include "solver_detail.hpp"
 
 // One operator handle. The reference's apply is const and callable from several threads at once
 // (operator.hpp:14-18, 47; test_operator.cpp:49-64): every entry point that touches the context's
@@ -88,6 +89,39 @@ void require_ctx(const sbg_ctx* ctx) {
     std::unique_lock<std::mutex> lk(ctx->mu);
     SBG_CUDA(cudaSetDevice(ctx->c->device));
     return lk;
+}
+
+// sbg::TraceRec -> sbg_trace_record callback (empty when trace is NULL)
+std::function<void(const sbg::TraceRec&)> make_trace(sbg_trace_fn trace, void* trace_user) {
+    if (!trace) return {};
+    return [trace, trace_user](const sbg::TraceRec& r) {
+        sbg_trace_record rec{};
+        rec.state = r.state;
+        rec.t = r.t;
+        rec.energy = r.energy;
+        rec.dE = r.dE;
+        rec.res_norm = r.res_norm;
+        rec.x_norm = r.x_norm;
+        rec.kinetic = r.kinetic;
+        rec.matvecs = r.matvecs;
+        rec.restart_reason = r.restart_reason;
+        rec.b = r.b;
+        rec.c = r.c;
+        rec.method = r.method;
+        rec.pair_partner = r.pair_partner;
+        rec.b_ab = r.b_ab;
+        rec.b_ba = r.b_ba;
+        rec.b_bb = r.b_bb;
+        rec.c_ab = r.c_ab;
+        rec.c_ba = r.c_ba;
+        rec.c_bb = r.c_bb;
+        rec.a_ab = r.a_ab;
+        rec.a_ba = r.a_ba;
+        rec.energy_partner = r.energy_partner;
+        rec.x_norm_partner = r.x_norm_partner;
+        rec.res_norm_partner = r.res_norm_partner;
+        trace(&rec, trace_user);
+    };
 }
 }  // namespace
 
@@ -453,36 +487,7 @@ static int solve_impl(sbg_ctx* ctx, int method, int nroots, int max_space, const
         if (nroots < 1 || nroots > sbg::detail_max_roots)
             throw std::invalid_argument("sbg_solve: nroots must be in 1..9 (at most 8 deflated states)");
         auto& c = *ctx->c;
-        std::function<void(const sbg::TraceRec&)> tf;
-        if (trace)
-            tf = [&](const sbg::TraceRec& r) {
-                sbg_trace_record rec{};
-                rec.state = r.state;
-                rec.t = r.t;
-                rec.energy = r.energy;
-                rec.dE = r.dE;
-                rec.res_norm = r.res_norm;
-                rec.x_norm = r.x_norm;
-                rec.kinetic = r.kinetic;
-                rec.matvecs = r.matvecs;
-                rec.restart_reason = r.restart_reason;
-                rec.b = r.b;
-                rec.c = r.c;
-                rec.method = r.method;
-                rec.pair_partner = r.pair_partner;
-                rec.b_ab = r.b_ab;
-                rec.b_ba = r.b_ba;
-                rec.b_bb = r.b_bb;
-                rec.c_ab = r.c_ab;
-                rec.c_ba = r.c_ba;
-                rec.c_bb = r.c_bb;
-                rec.a_ab = r.a_ab;
-                rec.a_ba = r.a_ba;
-                rec.energy_partner = r.energy_partner;
-                rec.x_norm_partner = r.x_norm_partner;
-                rec.res_norm_partner = r.res_norm_partner;
-                trace(&rec, trace_user);
-            };
+        const std::function<void(const sbg::TraceRec&)> tf = make_trace(trace, trace_user);
         const uint64_t launches0 = c.launches;
         try {
             sbg::MultiStateResult r = method == 1   ? sbg::solve_n_states_sbci1(c, nroots, to_cfg(cfg), tf)
@@ -533,6 +538,83 @@ int sbg_solve(sbg_ctx* ctx, int method, int nroots, const sbg_config* cfg, doubl
 int sbg_solve_davidson(sbg_ctx* ctx, int nroots, int max_space, const sbg_config* cfg, double* energies,
                        double* vectors, sbg_stats* stats, sbg_trace_fn trace, void* trace_user) {
     return solve_impl(ctx, 3, nroots, max_space, cfg, energies, vectors, stats, trace, trace_user);
+}
+
+int sbg_solve_state_sbci1(sbg_ctx* ctx, const double* x0, double e0, double* shift, int alpha, int ndefl,
+                          const double* defl_x, const double* defl_hx, const double* defl_e, const sbg_config* cfg,
+                          double* energy, double* vector, double* image, sbg_stats* stats, sbg_trace_fn trace,
+                          void* trace_user) {
+    return guarded([&] {
+        auto lk = lock_ctx(ctx);
+        if (!x0 || !shift || !energy) throw std::invalid_argument("sbg_solve_state_sbci1: null argument");
+        if (ndefl < 0 || ndefl > sbg::detail_max_roots - 1 || (ndefl > 0 && (!defl_x || !defl_e)))
+            throw std::invalid_argument("sbg_solve_state_sbci1: bad deflation set");
+        if (alpha < 0) throw std::invalid_argument("sbg_solve_state_sbci1: alpha must be >= 0");
+        auto& c = *ctx->c;
+        const sbg::SolverConfig scfg = to_cfg(cfg);
+        scfg.validate();
+        sbg::detail::Ops o(c);
+        // deflation set: stored vectors (+ images, rebuilt by sigma when not given; those builds are
+        // not applications of the caller's solve)
+        sbg::detail::Deflation defl;
+        for (int i = 0; i < ndefl; ++i) {
+            sbg::DBuf xv = c.vec(), hv = c.vec();
+            c.upload_local(defl_x + (size_t)i * c.ndet, xv.p, c.st);
+            if (defl_hx) {
+                c.upload_local(defl_hx + (size_t)i * c.ndet, hv.p, c.st);
+            } else {
+                o.apply(xv, hv);
+                c.applies().fetch_sub(1);
+            }
+            defl.add_with_image(o, std::move(xv), std::move(hv), defl_e[i]);
+        }
+        const uint64_t applies1 = c.applies().load();
+        // Seed{x0, H x0, E0} (sbci1.hpp:481-485)
+        sbg::detail::Seed seed;
+        seed.x = c.vec();
+        seed.hx = c.vec();
+        c.upload_local(x0, seed.x.p, c.st);
+        if (o.norm(seed.x) == 0.0) throw std::invalid_argument("solve_state_sbci1: x0 must be nonzero");
+        o.apply(seed.x, seed.hx);
+        seed.energy = e0;
+        sbg::detail::Precond pre{&c.diagonal(), *shift, scfg.clamp_delta};
+        if (!(pre.clamp > 0.0)) throw std::invalid_argument("clamp_delta must be positive");
+        sbg::detail::Sbci1Result r;
+        const auto t0 = std::chrono::steady_clock::now();
+        try {
+            r = sbg::detail::solve_state_sbci1(c, scfg, make_trace(trace, trace_user), pre, defl, std::move(seed), alpha,
+                                               alpha == 0);
+        } catch (const sbg::NonConvergenceError& e) {
+            if (stats) {
+                std::memset(stats, 0, sizeof(*stats));
+                stats->failed_state = e.state;
+                stats->best_energy = e.best_energy;
+                stats->best_residual = e.best_residual;
+            }
+            throw;
+        }
+        if (alpha == 0) pre.update_shift(r.pair.energy);
+        *shift = pre.shift;
+        *energy = r.pair.energy;
+        if (vector) c.download_local(r.pair.vector.p, vector + c.row_lo * c.NB, c.st);
+        if (image) c.download_local(r.converged_image.p, image + c.row_lo * c.NB, c.st);
+        SBG_CUDA(cudaStreamSynchronize(c.st));
+        if (stats) {
+            std::memset(stats, 0, sizeof(*stats));
+            stats->nroots = 1;
+            stats->iterations[0] = r.pair.iterations;
+            stats->restarts[0] = r.pair.restarts;
+            stats->final_residual[0] = r.pair.final_residual;
+            stats->matvecs = c.applies().load() - applies1;
+            stats->total_iterations = r.pair.iterations;
+            stats->total_restarts = r.pair.restarts;
+            stats->hx_refreshes = r.hx_refreshes;
+            stats->peak_vectors = 7 + ndefl;
+            stats->wall_time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            stats->failed_state = -1;
+            stats->s_squared[0] = c.spin_squared(r.pair.vector.p);
+        }
+    });
 }
 
 int sbg_selftest(void) {

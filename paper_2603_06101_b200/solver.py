@@ -132,6 +132,20 @@ class MultiStateResult:
     summary: RunSummary
 
 
+def _trace_cb(sink, name):
+    if sink is None:
+        return TRACE_FN(0)
+
+    def _cb(rec_p, _user):
+        r = rec_p.contents
+        sink(TraceRecord(METHODS.get(r.method, name), r.state, r.t, r.energy, r.dE, r.res_norm, r.x_norm,
+                         r.kinetic, r.matvecs,
+                         RESTART_REASONS[r.restart_reason] if r.restart_reason >= 0 else "", r.b, r.c,
+                         r.pair_partner, r.b_ab, r.b_ba, r.b_bb, r.c_ab, r.c_ba, r.c_bb, r.a_ab, r.a_ba,
+                         r.energy_partner, r.x_norm_partner, r.res_norm_partner))
+    return TRACE_FN(_cb)
+
+
 def _solve(op, method: int, n: int, cfg: SolverConfig | None, sink, want_vectors: bool, max_space: int = 0):
     cfg = cfg or SolverConfig()
     cfg.validate()
@@ -143,16 +157,7 @@ def _solve(op, method: int, n: int, cfg: SolverConfig | None, sink, want_vectors
     vec = np.zeros((n, dim)) if want_vectors else None
     st = Stats()
     cc = cfg.to_c()
-    cb = TRACE_FN(0)
-    if sink is not None:
-        def _cb(rec_p, _user):
-            r = rec_p.contents
-            sink(TraceRecord(METHODS.get(r.method, name), r.state, r.t, r.energy, r.dE, r.res_norm, r.x_norm,
-                             r.kinetic, r.matvecs,
-                             RESTART_REASONS[r.restart_reason] if r.restart_reason >= 0 else "", r.b, r.c,
-                             r.pair_partner, r.b_ab, r.b_ba, r.b_bb, r.c_ab, r.c_ba, r.c_bb, r.a_ab, r.a_ba,
-                             r.energy_partner, r.x_norm_partner, r.res_norm_partner))
-        cb = TRACE_FN(_cb)
+    cb = _trace_cb(sink, name)
     ep = e.ctypes.data_as(C.POINTER(C.c_double))
     vp = vec.ctypes.data_as(C.POINTER(C.c_double)) if vec is not None else None
     if method == 3 and max_space:
@@ -193,3 +198,51 @@ def davidson_solve(op, nroots: int, cfg: SolverConfig | None = None, sink=None, 
     operator, with the SBCI solvers' (D - E0)^-1 preconditioner. max_space = DavidsonConfig::max_space
     (davidson.hpp:19-38): 0 = 12*nroots, else >= 2*nroots."""
     return _solve(op, 3, nroots, cfg, sink, want_vectors, max_space)
+
+
+@dataclass
+class Sbci1Result:
+    """Sbci1Result (sbci1.hpp:344-349) of a single-state solve; next_seed is not exposed."""
+    pair: ConvergedEigenpair
+    converged_image: np.ndarray
+    hx_refreshes: int
+    matvecs: int
+    s_squared: float
+    shift: float    # the preconditioner's shift after the solve (tracks E for alpha == 0)
+
+
+def solve_state_sbci1(op, x0, E0: float, shift: float, deflation=(), cfg: SolverConfig | None = None, alpha: int = 0,
+                      sink=None) -> Sbci1Result:
+    """Plain-vector warm start (solve_state_sbci1(op, pre, defl, x0, E0, cfg, alpha, sink),
+    sbci1.hpp:477-486): pre = GroundShiftPreconditioner(op.diagonal(), shift, cfg.clamp_delta);
+    `deflation` is a sequence of (unit vector, energy) or (vector, image, energy) entries
+    (DeflationSet::add / add_with_image, precond.hpp:54-70)."""
+    cfg = cfg or SolverConfig()
+    cfg.validate()
+    n = op.dim()
+    x0 = np.ascontiguousarray(x0, np.float64)
+    if x0.shape != (n,):
+        raise ValueError("SymmetricOperator::apply: dimension mismatch")
+    dx = [np.ascontiguousarray(d[0], np.float64) for d in deflation]
+    dh = [np.ascontiguousarray(d[1], np.float64) for d in deflation if len(d) == 3]
+    de = np.array([float(d[-1]) for d in deflation])
+    if dh and len(dh) != len(dx):
+        raise ValueError("deflation entries must all carry images, or none")
+    X = np.stack(dx) if dx else None
+    H = np.stack(dh) if dh else None
+    dp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double)) if a is not None else None  # noqa: E731
+    sh = C.c_double(shift)
+    en = C.c_double()
+    vec = np.zeros(n)
+    img = np.zeros(n)
+    st = Stats()
+    cc = cfg.to_c()
+    cb = _trace_cb(sink, "sbci1")
+    rc = lib().sbg_solve_state_sbci1(op.handle, dp(x0), float(E0), C.byref(sh), int(alpha), len(dx), dp(X), dp(H),
+                                     dp(de) if len(dx) else None, C.byref(cc), C.byref(en), dp(vec), dp(img),
+                                     C.byref(st), cb, None)
+    if rc == 2:
+        raise NonConvergenceError(lib().sbg_last_error().decode(), st.failed_state, st.best_energy, st.best_residual)
+    check(rc)
+    pair = ConvergedEigenpair(int(alpha), en.value, vec, st.iterations[0], st.restarts[0], st.final_residual[0])
+    return Sbci1Result(pair, img, st.hx_refreshes, st.matvecs, float(st.s_squared[0]), sh.value)
