@@ -77,6 +77,9 @@ typedef struct sbg_stats {
     uint64_t kernel_launches;   /* kernels launched by the library during the call */
     /* <S^2> of each returned state (fci/spin.hpp:17-51, the CLI summary's s_squared column) */
     double s_squared[SBG_MAX_ROOTS];
+    /* length-n_det solver vectors resident in HBM at once during the call (peak_vectors keeps the
+     * reference's own formula, 7 + deflated states for SBCI1) */
+    int32_t device_vectors_peak;
 } sbg_stats;
 
 /* Per-iteration trace record (TraceRecord trace.hpp:22-44). Fields a method does not produce are NaN. */

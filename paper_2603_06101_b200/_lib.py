@@ -31,7 +31,7 @@ class Stats(C.Structure):
                 ("hx_refreshes", C.c_int32), ("peak_vectors", C.c_int32), ("wall_time_s", C.c_double),
                 ("failed_state", C.c_int32), ("best_energy", C.c_double), ("best_residual", C.c_double),
                 ("sigma_seconds", C.c_double), ("kernel_launches", C.c_uint64),
-                ("s_squared", C.c_double * SBG_MAX_ROOTS)]
+                ("s_squared", C.c_double * SBG_MAX_ROOTS), ("device_vectors_peak", C.c_int32)]
 
 
 class TraceRecordC(C.Structure):

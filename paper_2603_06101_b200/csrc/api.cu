@@ -489,6 +489,7 @@ static int solve_impl(sbg_ctx* ctx, int method, int nroots, int max_space, const
         auto& c = *ctx->c;
         const std::function<void(const sbg::TraceRec&)> tf = make_trace(trace, trace_user);
         const uint64_t launches0 = c.launches;
+        c.pool().reset_peak();
         try {
             sbg::MultiStateResult r = method == 1   ? sbg::solve_n_states_sbci1(c, nroots, to_cfg(cfg), tf)
                                       : method == 2 ? sbg::solve_n_states_sbci2(c, nroots, to_cfg(cfg), tf)
@@ -516,6 +517,7 @@ static int solve_impl(sbg_ctx* ctx, int method, int nroots, int max_space, const
                 stats->wall_time_s = r.wall_time_s;
                 stats->failed_state = -1;
                 stats->kernel_launches = c.launches - launches0;
+                stats->device_vectors_peak = c.pool().peak;
                 for (int k = 0; k < nroots; ++k) stats->s_squared[k] = s2[k];
             }
         } catch (const sbg::NonConvergenceError& e) {
@@ -569,6 +571,7 @@ int sbg_solve_state_sbci1(sbg_ctx* ctx, const double* x0, double e0, double* shi
             defl.add_with_image(o, std::move(xv), std::move(hv), defl_e[i]);
         }
         const uint64_t applies1 = c.applies().load();
+        c.pool().reset_peak();
         // Seed{x0, H x0, E0} (sbci1.hpp:481-485)
         sbg::detail::Seed seed;
         seed.x = c.vec();
@@ -610,6 +613,7 @@ int sbg_solve_state_sbci1(sbg_ctx* ctx, const double* x0, double e0, double* shi
             stats->total_restarts = r.pair.restarts;
             stats->hx_refreshes = r.hx_refreshes;
             stats->peak_vectors = 7 + ndefl;
+            stats->device_vectors_peak = c.pool().peak;
             stats->wall_time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
             stats->failed_state = -1;
             stats->s_squared[0] = c.spin_squared(r.pair.vector.p);

@@ -51,13 +51,14 @@ DBuf& DBuf::operator=(DBuf&& o) noexcept {
 double* VecPool::take(int64_t count) {
     if (n == 0) n = count;
     if (count != n) throw std::invalid_argument("VecPool: all pooled vectors have the padded local length");
-    if (!free_.empty()) {
-        double* p = free_.back();
-        free_.pop_back();
-        return p;
-    }
     double* p = nullptr;
-    SBG_CUDA(cudaMalloc(&p, (size_t)count * sizeof(double)));
+    if (!free_.empty()) {
+        p = free_.back();
+        free_.pop_back();
+    } else {
+        SBG_CUDA(cudaMalloc(&p, (size_t)count * sizeof(double)));
+    }
+    peak = std::max(peak, ++live);
     return p;
 }
 VecPool::~VecPool() {

@@ -29,9 +29,14 @@ namespace sbg {
 struct VecPool {
     std::vector<double*> free_;
     int64_t n = 0;
+    int live = 0, peak = 0;  // pooled vectors in use now / at most since reset_peak
     ~VecPool();
     double* take(int64_t count);
-    void give(double* p) { free_.push_back(p); }
+    void give(double* p) {
+        free_.push_back(p);
+        --live;
+    }
+    void reset_peak() { peak = live; }
 };
 
 struct DBuf {
@@ -75,6 +80,7 @@ public:
     DBuf alloc_vec() const;  // zero-initialised padded local vector
     // pooled zero-initialised padded local vector; the zero fill is ordered on st (solver work)
     DBuf vec() { return DBuf(*pool_, padded_len(), st); }
+    VecPool& pool() { return *pool_; }
     // persistent staging vectors of the host-pointer entry points (sbg_sigma, sbg_sigma_device)
     double* io_x(int slot = 0) {
         if (io_x_[slot].empty()) io_x_[slot] = alloc_vec();

@@ -267,19 +267,16 @@ public:
         // the cancellation guard (sbci2.hpp:299-306) needs; the spares are swapped in only if it
         // passes, so a rejected step leaves the state untouched as in the reference
         {
-            if (sp_ya_.empty()) {
-                sp_ya_ = c_.vec();
-                sp_yb_ = c_.vec();
-                sp_xa_ = c_.vec();
-                sp_xb_ = c_.vec();
-            }
+            // with the four spares: guard + commit in one pass; without room for them (or with
+            // SBG_GUARD_TWO_PASS=1): a read-only pass for the norms, then the commit in place
+            const bool merged = spares();
             Lin L;
             const int sya = L.in(st.ya.p), syb = L.in(st.yb.p), sza = L.in(za_.p), szb = L.in(zb_.p),
                       sxa = L.in(st.xa.p), sxb = L.in(st.xb.p);
-            const int ya = L.out(sp_ya_.p, {{sya, 1.0}, {sza, -co.c_aa}, {szb, -co.c_ab}, {sxb, co.a_ab}});
-            const int yb = L.out(sp_yb_.p, {{syb, 1.0}, {sza, -co.c_ba}, {szb, -co.c_bb}, {sxa, co.a_ba}});
-            const int xa = L.out(sp_xa_.p, {{sxa, 1.0}, {ya, co.b_aa}, {yb, co.b_ab}});
-            const int xb = L.out(sp_xb_.p, {{sxb, 1.0}, {ya, co.b_ba}, {yb, co.b_bb}});
+            const int ya = L.out(merged ? sp_ya_.p : nullptr, {{sya, 1.0}, {sza, -co.c_aa}, {szb, -co.c_ab}, {sxb, co.a_ab}});
+            const int yb = L.out(merged ? sp_yb_.p : nullptr, {{syb, 1.0}, {sza, -co.c_ba}, {szb, -co.c_bb}, {sxa, co.a_ba}});
+            const int xa = L.out(merged ? sp_xa_.p : nullptr, {{sxa, 1.0}, {ya, co.b_aa}, {yb, co.b_ab}});
+            const int xb = L.out(merged ? sp_xb_.p : nullptr, {{sxb, 1.0}, {ya, co.b_ba}, {yb, co.b_bb}});
             for (int k : {ya, yb, xa, xb, sxa, sxb}) L.dot(k, k);
             const auto r = L.run(c_);
             const double ya_nm = std::sqrt(r[0]), yb_nm = std::sqrt(r[1]);
@@ -290,10 +287,21 @@ public:
                 out.outcome = StepOutcome::restart(RestartReason::StallSmallB);
                 return out;
             }
-            std::swap(st.ya, sp_ya_);
-            std::swap(st.yb, sp_yb_);
-            std::swap(st.xa, sp_xa_);
-            std::swap(st.xb, sp_xb_);
+            if (merged) {
+                std::swap(st.ya, sp_ya_);
+                std::swap(st.yb, sp_yb_);
+                std::swap(st.xa, sp_xa_);
+                std::swap(st.xb, sp_xb_);
+            } else {
+                Lin W;
+                const int wya = W.in(st.ya.p), wyb = W.in(st.yb.p), wza = W.in(za_.p), wzb = W.in(zb_.p),
+                          wxa = W.in(st.xa.p), wxb = W.in(st.xb.p);
+                const int ya2 = W.out(st.ya.p, {{wya, 1.0}, {wza, -co.c_aa}, {wzb, -co.c_ab}, {wxb, co.a_ab}});
+                const int yb2 = W.out(st.yb.p, {{wyb, 1.0}, {wza, -co.c_ba}, {wzb, -co.c_bb}, {wxa, co.a_ba}});
+                W.out(st.xa.p, {{wxa, 1.0}, {ya2, co.b_aa}, {yb2, co.b_ab}});
+                W.out(st.xb.p, {{wxb, 1.0}, {ya2, co.b_ba}, {yb2, co.b_bb}});
+                W.run(c_);
+            }
             out.xa_norm = std::sqrt(r[2]);
             out.xb_norm = std::sqrt(r[3]);
         }
@@ -321,6 +329,7 @@ public:
             out.zrb_norm = std::sqrt(r[1]);
             ovl.assign(r.begin() + 2, r.end());
             if (!fused_ovl) ovl = deflation_overlaps(c_, defl, st.zra);
+            ovl = defl.sequential(std::move(ovl));
         }
         out.committed = true;
         st.coeffs = co;
@@ -363,6 +372,23 @@ public:
     SolverConfig cfg_;
     DBuf za_, zb_, hza_, hzb_, zrb_next_;
     DBuf sp_ya_, sp_yb_, sp_xa_, sp_xb_;  // candidate y', x' of the merged guard + commit pass
+    bool two_pass_ = std::getenv("SBG_GUARD_TWO_PASS") && std::atoi(std::getenv("SBG_GUARD_TWO_PASS")) != 0;
+    bool spares() {
+        if (two_pass_) return false;
+        if (!sp_ya_.empty()) return true;
+        try {
+            sp_ya_ = c_.vec();
+            sp_yb_ = c_.vec();
+            sp_xa_ = c_.vec();
+            sp_xb_ = c_.vec();
+            return true;
+        } catch (const DeviceError&) {
+            cudaGetLastError();
+            for (DBuf* b : {&sp_ya_, &sp_yb_, &sp_xa_, &sp_xb_}) *b = DBuf();
+            two_pass_ = true;
+            return false;
+        }
+    }
 };
 
 struct Sbci2PairResult {
@@ -514,7 +540,9 @@ MultiStateResult solve_n_states_sbci2(Context& c, int n, const SolverConfig& cfg
     if (!(pre.clamp > 0.0)) throw std::invalid_argument("clamp_delta must be positive");
     Deflation defl;
     MultiStateResult out;
-    PairDriver dr(c, cfg);
+    std::optional<PairDriver> pdr;
+    pdr.emplace(c, cfg);
+    PairDriver& dr = *pdr;
 
     Seed lower;
     lower.x = o.clone(guesses.front().x);
@@ -556,7 +584,10 @@ MultiStateResult solve_n_states_sbci2(Context& c, int n, const SolverConfig& cfg
         out.pairs.push_back(std::move(res.pair));
         lower = std::move(res.carry);
     }
-    // highest state: the single-state procedure
+    // highest state: the single-state procedure. The pair driver's buffers and the rotated guesses
+    // go back to the pool first, so the SBCI1 driver reuses them instead of adding its own
+    pdr.reset();
+    guesses.clear();
     Sbci1Result last = solve_state_sbci1(c, cfg, trace, pre, defl, std::move(lower), n - 1, false);
     out.total_iterations += last.pair.iterations;
     out.total_restarts += last.pair.restarts;

@@ -45,6 +45,11 @@ std::optional<RestartReason> check_restart(int alpha, double b, double dE, doubl
     return std::nullopt;
 }
 
+static std::vector<double> h_ovl(Context& c, int n) {
+    const double* h = c.finish_dots(n);
+    return std::vector<double>(h, h + n);
+}
+
 std::vector<double> precondition(Context& c, const DBuf& zres, const Precond& pre, const Deflation& defl, DBuf& z,
                                  const DBuf& x, const DBuf* y) {
     PrecArgs pa{};
@@ -60,8 +65,8 @@ std::vector<double> precondition(Context& c, const DBuf& zres, const Precond& pr
         pa.mode = 0;
         launch_precond(pa, c.rws, c.st);
         c.launches += 2;
-        const double* h = c.finish_dots(pa.nxc);
-        for (int i = 0; i < pa.nxc; ++i) pa.o[i] = h[i];
+        const auto o = defl.sequential(std::vector<double>(h_ovl(c, pa.nxc)));
+        for (int i = 0; i < pa.nxc; ++i) pa.o[i] = o[i];
     }
     pa.mode = 1;
     pa.z = z.p;
@@ -181,14 +186,46 @@ public:
         // (a rejected step leaves the state untouched, as in the reference)
         double zz2, xx2;
         std::vector<double> ovl;
-        {
-            if (sp_y_.empty()) {
-                sp_y_ = c_.vec();
-                sp_hy_ = c_.vec();
-                sp_x_ = c_.vec();
-                sp_hx_ = c_.vec();
-                sp_z_ = c_.vec();
+        if (!spares()) {
+            // two-pass form when the five spares do not fit in HBM (or SBG_GUARD_TWO_PASS=1): the
+            // candidate norms first (read-only pass, the same per-element arithmetic and reduction
+            // tree, so the same values), then — only if the guard passes — the commit in place
+            Lin L;
+            const int sx = L.in(st.x.p), sy = L.in(st.y.p), sz = L.in(z_.p), shx = L.in(st.hx.p),
+                      shy = L.in(st.hy.p), shz = L.in(hz_.p);
+            std::vector<int> sxc;
+            const bool fused_ovl = L.fits((int)defl.size());
+            if (fused_ovl)
+                for (auto& mm : defl.m) sxc.push_back(L.in(mm.x.p));
+            const int yn = use_three ? L.out(nullptr, {{sy, 1.0}, {sz, -c}}) : L.out(nullptr, {{sz, -c}});
+            const int hyn = use_three ? L.out(nullptr, {{shy, 1.0}, {shz, -c}}) : L.out(nullptr, {{shz, -c}});
+            const int xn = L.out(nullptr, {{sx, 1.0}, {yn, b}});
+            const int hxn = L.out(nullptr, {{shx, 1.0}, {hyn, b}});
+            const int zn = L.out(nullptr, {{hxn, 1.0 / k}, {xn, -e_new / k}});
+            L.dot(zn, zn);
+            L.dot(xn, xn);
+            L.dot(yn, yn);
+            for (int s : sxc) L.dot(s, zn);
+            const auto r = L.run(c_);
+            zz2 = r[0];
+            xx2 = r[1];
+            if (std::sqrt(nxx) + std::abs(b) * std::sqrt(r[2]) > 1e6 * std::max(std::sqrt(xx2), 1e-300)) {
+                out.outcome = StepOutcome::restart(RestartReason::StallSmallB);
+                return out;
             }
+            Lin W;
+            const int wx = W.in(st.x.p), wy = W.in(st.y.p), wz = W.in(z_.p), whx = W.in(st.hx.p), why = W.in(st.hy.p),
+                      whz = W.in(hz_.p);
+            const int y2 = use_three ? W.out(st.y.p, {{wy, 1.0}, {wz, -c}}) : W.out(st.y.p, {{wz, -c}});
+            const int hy2 = use_three ? W.out(st.hy.p, {{why, 1.0}, {whz, -c}}) : W.out(st.hy.p, {{whz, -c}});
+            const int x2 = W.out(st.x.p, {{wx, 1.0}, {y2, b}});
+            const int hx2 = W.out(st.hx.p, {{whx, 1.0}, {hy2, b}});
+            W.out(st.zres.p, {{hx2, 1.0 / k}, {x2, -e_new / k}});
+            W.run(c_);
+            ovl.assign(r.begin() + 3, r.end());
+            if (!fused_ovl) ovl = deflation_overlaps(c_, defl, st.zres);
+            ovl = defl.sequential(std::move(ovl));
+        } else {
             Lin L;
             const int sx = L.in(st.x.p), sy = L.in(st.y.p), sz = L.in(z_.p), shx = L.in(st.hx.p),
                       shy = L.in(st.hy.p), shz = L.in(hz_.p);
@@ -219,6 +256,7 @@ public:
             std::swap(st.zres, sp_z_);
             ovl.assign(r.begin() + 3, r.end());
             if (!fused_ovl) ovl = deflation_overlaps(c_, defl, st.zres);
+            ovl = defl.sequential(std::move(ovl));
         }
         g_ph[4] += ms_since(tp);
         out.committed = true;
@@ -294,6 +332,27 @@ public:
     const std::function<void(const TraceRec&)>& trace_;
     DBuf z_, hz_;
     DBuf sp_y_, sp_hy_, sp_x_, sp_hx_, sp_z_;  // candidate state of the merged guard + commit pass
+    bool two_pass_ = std::getenv("SBG_GUARD_TWO_PASS") && std::atoi(std::getenv("SBG_GUARD_TWO_PASS")) != 0;
+
+    // the merged guard + commit pass needs five spare vectors; without room for them the step
+    // falls back to the two-pass form for the rest of the solve (large sectors)
+    bool spares() {
+        if (two_pass_) return false;
+        if (!sp_y_.empty()) return true;
+        try {
+            sp_y_ = c_.vec();
+            sp_hy_ = c_.vec();
+            sp_x_ = c_.vec();
+            sp_hx_ = c_.vec();
+            sp_z_ = c_.vec();
+            return true;
+        } catch (const DeviceError&) {
+            cudaGetLastError();  // the failed cudaMalloc leaves no sticky error
+            for (DBuf* b : {&sp_y_, &sp_hy_, &sp_x_, &sp_hx_, &sp_z_}) *b = DBuf();
+            two_pass_ = true;
+            return false;
+        }
+    }
 };
 
 

@@ -202,16 +202,31 @@ struct Deflation {  // DeflationSet (precond.hpp:54-102) with cached images
         double e;
     };
     std::vector<Member> m;
+    std::vector<std::vector<double>> gram;  // gram[i][j] = x_i . x_j for j < i (|.| <= 1e-10 by add)
     bool empty() const { return m.empty(); }
     size_t size() const { return m.size(); }
 
     void add_with_image(Ops& o, DBuf x, DBuf hx, double e) {
         const double n = o.norm(x);
         if (std::abs(n - 1.0) > 1e-12) throw std::invalid_argument("DeflationSet::add: vector must be unit norm");
-        for (auto& mm : m)
-            if (std::abs(o.dot(mm.x, x)) > 1e-10)
-                throw std::invalid_argument("DeflationSet::add: vector not orthogonal to stored set");
+        std::vector<double> g;
+        for (auto& mm : m) {
+            const double d = o.dot(mm.x, x);
+            if (std::abs(d) > 1e-10) throw std::invalid_argument("DeflationSet::add: vector not orthogonal to stored set");
+            g.push_back(d);
+        }
         m.push_back({std::move(x), std::move(hx), e});
+        gram.push_back(std::move(g));
+    }
+    // The fused passes compute every overlap x_c . v from the unprojected v at once; the reference
+    // projects member by member (project_out, precond.hpp:78-80: axpy(-dot(x_c, v), x_c, v)), so
+    // member c sees v already stripped of members j < c. In exact arithmetic that overlap is
+    // o'_c = x_c . v - sum_{j<c} o'_j (x_c . x_j): this turns the one-pass overlaps into the
+    // sequential projection's, which then runs as v - sum_c o'_c x_c in one pass.
+    std::vector<double> sequential(std::vector<double> o) const {
+        for (size_t c = 1; c < o.size() && c < gram.size(); ++c)
+            for (size_t j = 0; j < c; ++j) o[c] -= o[j] * gram[c][j];
+        return o;
     }
     // v -= x_i (x_i . v), sequentially over members (precond.hpp:78-80)
     void project_out(Ops& o, DBuf& v) {

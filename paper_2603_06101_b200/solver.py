@@ -89,6 +89,7 @@ class RunSummary:
     peak_vectors: int = 0
     wall_time_s: float = 0.0
     kernel_launches: int = 0
+    device_vectors_peak: int = 0   # length-n_det solver vectors resident at once (HBM footprint)
 
     def energies(self):
         return [s.energy for s in self.states]
@@ -174,7 +175,7 @@ def _solve(op, method: int, n: int, cfg: SolverConfig | None, sink, want_vectors
         states.append(StateSummary(k, float(e[k]), st.iterations[k], st.restarts[k], st.final_residual[k],
                                    float(st.s_squared[k])))
     summ = RunSummary(name, states, st.total_iterations, st.total_restarts, st.matvecs, st.hx_refreshes,
-                      st.peak_vectors, st.wall_time_s, st.kernel_launches)
+                      st.peak_vectors, st.wall_time_s, st.kernel_launches, st.device_vectors_peak)
     return MultiStateResult(pairs, summ)
 
 

@@ -710,3 +710,24 @@ def test_sharded_sigma_generic_kernels(dev, rest, spec, world):
         op.close()
     g.close()
     single.close()
+
+
+@pytest.mark.parametrize("method", ["sbci1", "sbci2"])
+def test_two_pass_guard_fallback_same_trajectory(dev, rest, gold_dir, monkeypatch, method):
+    """The merged guard + commit pass needs spare vectors; the two-pass fallback (used when they do
+    not fit, forced here with SBG_GUARD_TWO_PASS=1) computes the same norms with the same arithmetic,
+    so the c1 four-root trajectory is the reference's either way, with fewer resident vectors."""
+    q = baseline_problem(1, rest)
+    g = gold(gold_dir, "c1")[method]
+    solve = P.solve_n_states_sbci1 if method == "sbci1" else P.solve_n_states_sbci2
+    op = P.FciOperator(to_product(q), max_determinants=2 ** 62)
+    runs = []
+    for two_pass in ("0", "1"):
+        monkeypatch.setenv("SBG_GUARD_TWO_PASS", two_pass)
+        r = solve(op, 4, want_vectors=False)
+        e = np.array([pp.energy for pp in r.pairs])
+        assert np.abs(e - np.array(g["energies"])).max() <= E_TOL
+        assert [pp.iterations for pp in r.pairs] == g["iterations"] and r.summary.matvecs == g["matvecs"]
+        runs.append(r.summary.device_vectors_peak)
+    assert 0 < runs[1] < runs[0], runs
+    op.close()
