@@ -59,6 +59,7 @@ void launch_sigma_ab_direct(const double* x_full, double* y_local, const double*
 // ---- sigma_ss.cu: same-spin term via the (n-2)-electron intermediate, K4/K5 ----
 struct SsPlan {
     int norb, nel, P, KSS, warps, npa;
+    int rem = 0;  // leftover pair columns (P % 4 <= 2) handled as epilogue rank-1 terms
     int64_t NK;
     size_t smem;
 };
