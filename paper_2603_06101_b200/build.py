@@ -35,6 +35,20 @@ def nvcc():
     raise RuntimeError("nvcc not found")
 
 
+def nccl_link():
+    """Link the NCCL that PyTorch ships (nvidia-nccl wheel, 2.28) when present, else the system one.
+    Both arrive as soname libnccl.so.2 in one process: whichever loads first serves both, so libsbg
+    must bind the newer one or a later `import torch` fails on symbols 2.27 lacks."""
+    try:
+        import nvidia.nccl
+        d = os.path.join(list(nvidia.nccl.__path__)[0], "lib")
+        if os.path.exists(os.path.join(d, "libnccl.so.2")):
+            return ["-L" + d, "-l:libnccl.so.2", "-Xlinker", "-rpath," + d]
+    except ImportError:
+        pass
+    return ["-lnccl", "-Xlinker", "-rpath,/usr/lib/x86_64-linux-gnu"]
+
+
 def _compile(src, ptxas_verbose):
     out = os.path.join(OBJ, src.replace(".cu", ".o"))
     cmd = [nvcc(), *ARCH, *FLAGS, *EXTRA, *PER_FILE.get(src, []), "-c", os.path.join(CSRC, src), "-o", out]
@@ -58,7 +72,7 @@ def build(ptxas_verbose=False, force=False):
         for _, err in results:
             sys.stderr.write(err)
     objs = [o for o, _ in results]
-    cmd = [nvcc(), *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-lnccl", "-Xlinker", "-rpath,/usr/lib/x86_64-linux-gnu"]
+    cmd = [nvcc(), *ARCH, "-shared", "-o", LIB + ".tmp", *objs, *nccl_link()]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + r.stderr)

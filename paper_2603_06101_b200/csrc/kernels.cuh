@@ -31,6 +31,7 @@ struct AbPlan {
     int k0e;  // ws kernel: occupation column k = 0 as an epilogue rank-1 term (K - 1 divisible by 4)
     int tall; // ws kernel: balanced warp assignment for 5-7 m16 blocks (warps 4-7 span the rest)
     int npass = 1;    // pair-row blocks of 128 rows (npair > 136); 1 = one pass over all rows
+    int tma = 0;      // ws red kernel: D rows and reduction lists by bulk copies (UBLKCP) on mbarriers
     int code_ld = 0;  // rows per beta string of the scatter-code table (npad, or npass * 128)
     int64_t NA, NB, ld;
     size_t smem;
@@ -59,7 +60,6 @@ void launch_sigma_ab_direct(const double* x_full, double* y_local, const double*
 // ---- sigma_ss.cu: same-spin term via the (n-2)-electron intermediate, K4/K5 ----
 struct SsPlan {
     int norb, nel, P, KSS, warps, npa;
-    int rem = 0;  // leftover pair columns (P % 4 <= 2) handled as epilogue rank-1 terms
     int64_t NK;
     size_t smem;
 };

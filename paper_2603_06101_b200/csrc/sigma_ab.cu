@@ -59,6 +59,7 @@ struct AbParams {
     const uint32_t* tile_ent32; // [ntiles+1] offsets into ent32 (multiples of 4)
     int m0;                     // first pair row of this pass (pair-row blocks when npair > 136)
     int add_ecore;              // this pass adds e_core * x
+    int tma;                    // k_sigma_ab_ws red mode: D rows and reduction lists by bulk copies
 };
 
 // Software pipeline per alpha row, one __syncthreads per tile: iteration `it` prefetches D(it+1)
@@ -313,7 +314,9 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
     constexpr int K0 = K0E ? 1 : 0;
     const int KP = K0 + KS * 4;
     const int ntiles = (int)(p.ld / NT);
-    double* srow = smem;                     // [ld], absent in red mode
+    // mbarriers of the bulk-copy pipeline: [0..1] D stage b landed, [2..3] list stage b landed
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
+    double* srow = smem + 4;                 // [ld], absent in red mode
     double* Ds = srow + (p.red ? 0 : p.ld);
     double* sAe = Ds + STAGES * KP * DSTRIDE;
     double* Gs = sAe + KP * 8;
@@ -505,6 +508,135 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
         for (int i = stid; i <= ntiles; i += kWsHalf) {
             sTT[i] = p.red ? 0u : p.tile_tgt[i];
             sTE[i] = p.red ? p.tile_ent32[i] : p.tile_ent[i];
+        }
+        if (p.tma) {
+            if (stid == 0) {
+                for (int i = 0; i < 4; ++i) mbar_init(mbar + i, 1);
+                mbar_init_fence();
+            }
+            // bulk-copy pipeline (red mode): warp 8 issues every D row (one 256-byte copy per linked
+            // alpha row) and the tile's reduction list (one copy) on the TMA engine; D(it) and
+            // lists(it) complete on mbar[it & 1] / mbar[2 + (it & 1)], whose phase parity every
+            // loader thread tracks in phD / phL (one completion per tile of that stage)
+            uint32_t phD = 0, phL = 0;
+            const bool prod = (stid >> 5) == 0;
+            const int plane = stid & 31;
+            for (int64_t ia = p.row_lo + blockIdx.x; ia < p.row_hi; ia += gridDim.x) {
+                bar_sync(0, kWsThreads);  // row start: the MMA warps are done with the previous K-list
+                const uint64_t sa = string_unrank((uint64_t)ia, p.na_el, norb);
+                for (int k = stid; k < KP; k += kWsHalf) {  // K-list (as below)
+                    int J = (int)ia, pr = -2;
+                    double sg = 0.0;
+                    if (k == 0) {
+                        pr = -1;
+                        sg = 1.0;
+                    } else if (k < p.K) {
+                        const int nv = norb - p.na_el;
+                        const int qi = (k - 1) / nv, pi = (k - 1) % nv;
+                        uint64_t m = sa;
+                        for (int i = 0; i < qi; ++i) m &= m - 1;
+                        const int q = __ffsll((long long)m) - 1;
+                        uint64_t v = ~sa & (((uint64_t)1 << norb) - 1);
+                        for (int i = 0; i < pi; ++i) v &= v - 1;
+                        const int pp = __ffsll((long long)v) - 1;
+                        const uint64_t rem = sa ^ ((uint64_t)1 << q);
+                        J = (int)string_rank(rem | ((uint64_t)1 << pp));
+                        sg = ((pop_below(sa, q) + pop_below(rem, pp)) & 1) ? -1.0 : 1.0;
+                        pr = pair_sym(pp, q);
+                    }
+                    sJ[k] = J;
+                    sPair[k] = pr;
+                    sSign[k] = sg;
+                }
+                bar_sync(BAR_SINT, kWsHalf);  // sJ visible to the producer warp; previous row's lists read
+                bar_arrive(BAR_KLIST, kWsThreads);
+                const bool d_bulk = p.tma >= 2;
+                auto gather_d = [&](int stage, int jt) {  // tma == 1: D rows by cp.async, all loader threads
+                    if (p.dbg & 4) return;
+                    double* dst = Ds + stage * KP * DSTRIDE;
+                    for (int c = stid; c < KP * (NT / 2); c += kWsHalf) {
+                        const int k = c / (NT / 2), part = c % (NT / 2);
+                        cp_async16(dst + k * DSTRIDE + part * 2, p.x + (int64_t)sJ[k] * p.ld + (int64_t)jt * NT + part * 2);
+                    }
+                    cp_async_commit();
+                };
+                auto issue_d = [&](int stage, int jt) {  // producer warp only
+                    if (p.dbg & 4) {
+                        if (plane == 0) mbar_arrive_expect_tx(mbar + stage, 0);
+                        return;
+                    }
+                    fence_proxy_async_smem();  // the MMA warps' reads of this stage precede the refill
+                    if (plane == 0) mbar_arrive_expect_tx(mbar + stage, (uint32_t)(KP * NT * 8));
+                    __syncwarp();
+                    double* dst = Ds + stage * KP * DSTRIDE;
+                    for (int k = plane; k < KP; k += 32)
+                        bulk_g2s(dst + k * DSTRIDE, p.x + (int64_t)sJ[k] * p.ld + (int64_t)jt * NT, NT * 8, mbar + stage);
+                };
+                auto issue_l = [&](int stage, int jt) {
+                    if (plane == 0) {
+                        const uint32_t e0 = sTE[jt], bytes = (sTE[jt + 1] - e0) * 4;
+                        fence_proxy_async_smem();
+                        mbar_arrive_expect_tx(mbar + 2 + stage, bytes);
+                        if (bytes) bulk_g2s(Le + stage * p.maxE, p.ent32 + e0, bytes, mbar + 2 + stage);
+                    }
+                };
+                for (int jt = 0; jt < 2 && jt < ntiles; ++jt) {
+                    if (prod) {
+                        if (d_bulk) issue_d(jt, jt);
+                        issue_l(jt, jt);
+                    }
+                    if (!d_bulk) gather_d(jt, jt);
+                }
+                if (!d_bulk) {
+                    cp_async_wait<0>();
+                    bar_sync(BAR_SINT, kWsHalf);
+                }
+                for (int jt = 0; jt < 2 && jt < ntiles; ++jt) {
+                    if (d_bulk) {
+                        mbar_wait_parity(mbar + jt, (phD >> jt) & 1u);
+                        phD ^= 1u << jt;
+                    }
+                    bar_arrive(BAR_DREADY + jt, kWsThreads);
+                }
+                double* yrow = p.y + (ia - p.row_lo) * p.ld;
+                for (int it = 0; it < ntiles; ++it) {
+                    const int b = it & 1;
+                    bar_sync(BAR_FULL + b, kWsThreads);   // G(it) staged; D stage b free
+                    if (it + 2 < ntiles) {
+                        if (!d_bulk) gather_d(b, it + 2);
+                        else if (prod) issue_d(b, it + 2);
+                    }
+                    mbar_wait_parity(mbar + 2 + b, (phL >> b) & 1u);  // lists(it) landed
+                    phL ^= 1u << b;
+                    if (!(p.dbg & 1)) {
+                        const double* G = Gs + b * p.grows * GSTRIDE;
+                        const uint32_t* l32 = reinterpret_cast<const uint32_t*>(Le + b * p.maxE);
+                        const uint32_t n = sTE[it + 1] - sTE[it];
+#pragma unroll RED_UNROLL
+                        for (uint32_t i = stid; i < n; i += kWsHalf) {
+                            const uint32_t en = l32[i];
+                            if (en == 0xFFFFFFFFu) continue;  // 16-byte padding
+                            const long long bits = __double_as_longlong(G[en & 0x7FFFu]) ^ ((long long)(en & 0x8000u) << 48);
+                            red_add_f64(yrow + (en >> 16), __longlong_as_double(bits));
+                        }
+                    }
+                    bar_arrive(BAR_EMPTY + b, kWsThreads);
+                    if (!d_bulk) cp_async_wait<0>();      // this thread's rows of D(it+2)
+                    bar_sync(BAR_SINT, kWsHalf);          // lists stage b read by all; (cp.async) D(it+2) landed
+                    if (it + 2 < ntiles) {
+                        if (prod) issue_l(b, it + 2);
+                        if (d_bulk) {
+                            mbar_wait_parity(mbar + b, (phD >> b) & 1u);   // D(it+2) landed
+                            phD ^= 1u << b;
+                        }
+                        bar_arrive(BAR_DREADY + b, kWsThreads);
+                    }
+                }
+                const double* xr = p.x + ia * p.ld;  // e_core * x, reduced like the tiles
+                if (p.e_core != 0.0 && p.add_ecore)
+                    for (int64_t c = stid; c < p.NB; c += kWsHalf) red_add_f64(yrow + c, p.e_core * xr[c]);
+            }
+            return;
         }
         for (int64_t ia = p.row_lo + blockIdx.x; ia < p.row_hi; ia += gridDim.x) {
             bar_sync(0, kWsThreads);  // row start: the MMA warps are done with the previous K-list
@@ -762,7 +894,7 @@ AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int
             pl.maxE = 2 * 4 * ((nt * (nb_el + nb_el * (norb - nb_el)) + 3) / 4);
         }
         const int64_t ntiles = ld / nt;
-        pl.smem = (size_t)(pl.red ? 0 : ld) * 8 + (size_t)STAGES * KP * (nt + 4) * 8 + (size_t)KP * 8 * 8 +
+        pl.smem = 32 + (size_t)(pl.red ? 0 : ld) * 8 + (size_t)STAGES * KP * (nt + 4) * 8 + (size_t)KP * 8 * 8 +
                   (size_t)STAGES * pl.npad * (nt + 8) * 8 + (size_t)STAGES * (pl.maxT * 4 + pl.maxE * 2) +
                   (size_t)(ntiles + 1) * 8 + (size_t)KP * 16 + 16;
     };
@@ -783,6 +915,13 @@ AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int
     pl.tall = pl.ws && pl.nt == 32 && !pl.extra && pl.mb16 >= 5 && pl.mb16 <= 7 && pl.KS <= 13 &&
               !(tall_env && atoi(tall_env) == 0);
     if (pl.ws) pl.threads = kWsThreads;
+    // bulk copies (TMA engine) for the gathers and lists of the reduction kernel; SBG_AB_TMA=0 keeps
+    // the 256-thread cp.async gathers
+    // 1 = reduction lists by bulk copy (D rows by cp.async), 2 = D rows too (one 256-byte bulk copy
+    // per linked row: measured slower at c4, 107.7 vs 100.7 ms — the 2-stage ring does not hide its
+    // latency), 0 = cp.async for both
+    const char* tma_env = getenv("SBG_AB_TMA");
+    pl.tma = (pl.ws && pl.red) ? (tma_env ? atoi(tma_env) : 1) : 0;
     return pl;
 }
 
@@ -869,6 +1008,7 @@ void launch_sigma_ab(const AbPlan& pl, const AbScatter& sc, const double* x_full
     prm.ent32 = sc.ent32;
     prm.tile_ent32 = sc.tile_ent32;
     prm.m0 = pass * 128;
+    prm.tma = pl.tma;
     prm.add_ecore = pass == 0;
     if (pass > 0 && !(pl.red && pl.ws)) throw InvalidArgument("sigma_ab: pair-row passes need the reduction kernel");
     if (pl.red && !accumulate) throw InvalidArgument("sigma_ab: reduction mode needs an initialised y");

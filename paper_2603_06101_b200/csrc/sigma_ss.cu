@@ -13,7 +13,6 @@
 // scattered rows; the batch dimension (the other spin) is contiguous, so gathers are coalesced
 // row reads and the scatter is a coalesced fp64 reduction (red.global.add.f64) into L2.
 #include <algorithm>
-#include <cstdlib>
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -37,7 +36,6 @@ struct SsParams {
     double* y;  // column c of row I lives at y[I * ldy + c - ycol0] (a column window of the output)
     const double* Va;
     int norb, nel, P, npa;
-    int rem;    // pair columns 4*KSS .. P-1 (<= 2) added in the epilogue instead of a padded k-step
     int64_t ldx, col_lo, col_hi;
     int tpc;  // column tiles per CTA
     int64_t ldy, ycol0;
@@ -49,9 +47,7 @@ template <int KSS>
 // looser caps
 __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS > 24 ? 1 : (KSS > 16 ? 2 : SBG_SS_MINB))
     k_sigma_ss(const SsParams p) {
-    // gathered rows: the 4*KSS DMMA k columns plus up to 2 remainder columns (rank-1 epilogue terms,
-    // so P = 45 (16 orbitals, 8 electrons) runs 11 k-steps + 1 column instead of 12 padded k-steps)
-    const int KPP = KSS * 4 + p.rem;
+    constexpr int KPP = KSS * 4;
     extern __shared__ __align__(16) double smem[];
     double* Xs = smem;                        // [2][KPP][XSTRIDE]
     const int ysrows = max(KPP, 16 * (int)(blockDim.x >> 5));
@@ -103,22 +99,13 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
         sRowY[i] = (int64_t)sJ[i] * p.ldy;
     }
 
-    auto aval = [&](int i, int jj) -> double {
-        return (i < P && jj < P) ? sPhi[i] * sPhi[jj] * p.Va[(size_t)sPi[i] * p.npa + sPi[jj]] : 0.0;
-    };
     double a0[KSS], a1[KSS];
     const int i0 = 16 * w + g;
 #pragma unroll
     for (int j = 0; j < KSS; ++j) {
-        a0[j] = aval(i0, 4 * j + t);
-        a1[j] = aval(i0 + 8, 4 * j + t);
-    }
-    const int rem = p.rem, kr = 4 * KSS;
-    double ar0[2], ar1[2];  // remainder columns of this thread's two rows
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-        ar0[r] = r < rem ? aval(i0, kr + r) : 0.0;
-        ar1[r] = r < rem ? aval(i0 + 8, kr + r) : 0.0;
+        const int jj = 4 * j + t;
+        a0[j] = (i0 < P && jj < P) ? sPhi[i0] * sPhi[jj] * p.Va[(size_t)sPi[i0] * p.npa + sPi[jj]] : 0.0;
+        a1[j] = (i0 + 8 < P && jj < P) ? sPhi[i0 + 8] * sPhi[jj] * p.Va[(size_t)sPi[i0 + 8] * p.npa + sPi[jj]] : 0.0;
     }
     __syncthreads();
 
@@ -158,18 +145,6 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
             const double* Xk = X + (4 * j + t) * XSTRIDE + g;
 #pragma unroll
             for (int nb = 0; nb < NTS / 8; ++nb) dmma_16x8x4(acc[nb], a0[j], a1[j], Xk[nb * 8]);
-        }
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {  // rank-1 remainder terms: acc += A(:, kr + r) X(kr + r, :)
-            if (r >= rem) break;
-#pragma unroll
-            for (int nb = 0; nb < NTS / 8; ++nb) {
-                const double2 xv = *reinterpret_cast<const double2*>(X + (kr + r) * XSTRIDE + nb * 8 + 2 * t);
-                acc[nb][0] = fma(ar0[r], xv.x, acc[nb][0]);
-                acc[nb][1] = fma(ar0[r], xv.y, acc[nb][1]);
-                acc[nb][2] = fma(ar1[r], xv.x, acc[nb][2]);
-                acc[nb][3] = fma(ar1[r], xv.y, acc[nb][3]);
-            }
         }
 #pragma unroll
         for (int nb = 0; nb < NTS / 8; ++nb) {
@@ -356,17 +331,9 @@ SsPlan plan_sigma_ss(int norb, int nel) {
     const int nv = norb - nel + 2;
     pl.P = nv * (nv - 1) / 2;
     pl.NK = (int64_t)binom_host_calc(norb, nel - 2);
-    // P % 4 <= 2 leftover pair columns ride in the epilogue (rank-1 FMAs) instead of a padded k-step
-    const char* rem_env = getenv("SBG_SS_REM");
-    const bool use_rem = !(rem_env && atoi(rem_env) == 0);
-    pl.rem = (use_rem && pl.P % 4 <= 2) ? pl.P % 4 : 0;
-    pl.KSS = pl.rem ? pl.P / 4 : (pl.P + 3) / 4;
-    if (pl.KSS == 0) {  // P <= 2: one padded k-step
-        pl.KSS = 1;
-        pl.rem = 0;
-    }
+    pl.KSS = (pl.P + 3) / 4;
     pl.warps = (pl.P + 15) / 16;
-    const int KPP = pl.KSS * 4 + 2;
+    const int KPP = pl.KSS * 4;
     const int rows = std::max(KPP, 16 * pl.warps);
     pl.smem = (size_t)(2 * KPP * XSTRIDE + rows * YSTRIDE) * 8 + (size_t)KPP * 8 * 5 + 16;
     if (pl.KSS > 32 || pl.warps > 8) throw InvalidArgument("sigma_ss: orbital space too large for this build");
@@ -387,7 +354,7 @@ void launch_sigma_ss(const SsPlan& pl, const double* x, double* y, const double*
     // (measured: c4 same-spin 33.4 -> 32.8 ms, c3 1.87 ms kept)
     int tpc = ntiles >= 256 ? kMaxTilesPerCta : std::min(kMaxTilesPerCta, 32);
     while (tpc > 4 && pl.NK * ((ntiles + tpc - 1) / tpc) < 8LL * nsm) tpc /= 2;
-    SsParams prm{x, y, Va, pl.norb, pl.nel, pl.P, pl.npa, pl.rem, ldx, col_lo, col_hi, tpc, ldy, ycol0};
+    SsParams prm{x, y, Va, pl.norb, pl.nel, pl.P, pl.npa, ldx, col_lo, col_hi, tpc, ldy, ycol0};
     const int64_t gy = (ntiles + tpc - 1) / tpc;
     dim3 grid((unsigned)pl.NK, (unsigned)gy);
     switch (pl.KSS) {
