@@ -567,9 +567,9 @@ void Context::run_ab(const double* x_full, double* y_rows, int64_t lo, int64_t h
 }
 
 void Context::run_ss(int spin, const double* x, double* y, int64_t ldx, int64_t col_lo, int64_t col_hi,
-                     cudaStream_t s, int64_t ldy, int64_t ycol0) {
+                     cudaStream_t s, int64_t ldy, int64_t ycol0, int64_t col_pad) {
     if (ss_csr_[spin]) launch_sigma_ss_csr(csr_dev_[spin], x, y, ldx, col_lo, col_hi, s, ldy, ycol0);
-    else launch_sigma_ss(spin ? ssb_ : ssa_, x, y, d_Va_, ldx, col_lo, col_hi, s, ldy, ycol0);
+    else launch_sigma_ss(spin ? ssb_ : ssa_, x, y, d_Va_, ldx, col_lo, col_hi, s, ldy, ycol0, col_pad);
 }
 
 // rows [lo, hi) of block i of nchunks: equal blocks on a 32-row grid
@@ -597,7 +597,7 @@ void Context::sigma_rowblocks(const double* x_local, double* y_local, cudaStream
         if (ssb_.P > 0) {
             launch_transpose(x_local + lo * ld, hi - lo, NB, ld, xT_.p + lo, ldT, NB, hi - lo, 0, s);
             SBG_CUDA(cudaMemset2DAsync(sT_.p + lo, ldT * 8, 0, (hi - lo) * 8, NB, s));
-            launch_sigma_ss(ssb_, xT_.p, sT_.p, d_Va_, ldT, lo, hi, s);
+            launch_sigma_ss(ssb_, xT_.p, sT_.p, d_Va_, ldT, lo, hi, s, 0, 0, hi == nrows ? ldT : 0);
             launch_transpose(sT_.p + lo, NB, hi - lo, ldT, y_local + lo * ld, ld, hi - lo, ld, 0, s);
             launches += 3;
         } else {
@@ -606,7 +606,7 @@ void Context::sigma_rowblocks(const double* x_local, double* y_local, cudaStream
     }
     // ---- alpha-alpha (all rows: x complete)
     if (ssa_.P > 0) {
-        launch_sigma_ss(ssa_, x_local, y_local, d_Va_, ld, 0, NB, s);
+        launch_sigma_ss(ssa_, x_local, y_local, d_Va_, ld, 0, NB, s, 0, 0, ld);
         launches += 1;
     }
     if (ev) {
@@ -686,7 +686,7 @@ void Context::sigma(const double* x_local, double* y_local, cudaStream_t s) {
         // x^T of the local rows: [NB][ldT], column r = local alpha row r
         launch_transpose(x_local, nrows, NB, ld, xT_.p, ldT, NB, ldT, 0, s);
         SBG_CUDA(cudaMemsetAsync(sT_.p, 0, (size_t)NB * ldT * 8, s));
-        run_ss(1, xT_.p, sT_.p, ldT, 0, nrows, s);
+        run_ss(1, xT_.p, sT_.p, ldT, 0, nrows, s, 0, 0, ldT);
         // y[r][c] = sT[c][r]
         launch_transpose(sT_.p, NB, nrows, ldT, y_local, ld, nrows, ld, 0, s);
         launches += 3;
@@ -704,12 +704,12 @@ void Context::sigma(const double* x_local, double* y_local, cudaStream_t s) {
     bool exchange = false;
     if (has_ss(0)) {
         if (world == 1) {
-            run_ss(0, xf, y_local, ld, 0, NB, s);
+            run_ss(0, xf, y_local, ld, 0, NB, s, 0, 0, ld);
             launches += 1;
         } else {
             const int64_t clo = aa_lo_, chi = aa_hi_;
             if (chi > clo) SBG_CUDA(cudaMemset2DAsync(saa_.p + (clo - aa_c0_), ldw_ * 8, 0, (chi - clo) * 8, NA, s));
-            run_ss(0, xf, saa_.p, ld, clo, chi, s, ldw_, aa_c0_);
+            run_ss(0, xf, saa_.p, ld, clo, chi, s, ldw_, aa_c0_, chi == NB ? ld : 0);
             launches += 1;
             SBG_CUDA(cudaEventRecord(ev_aa_, s));
             exchange = true;

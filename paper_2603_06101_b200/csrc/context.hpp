@@ -165,8 +165,9 @@ private:
     double csr_nnz_[2] = {0.0, 0.0};
     bool has_ss(int spin) const { return ss_csr_[spin] || (spin ? ssb_.P : ssa_.P) > 0; }
     // same-spin term of one spin on a column window (x, y: rows = that spin's strings)
+    // col_pad: see launch_sigma_ss (zero padding columns of x past col_hi inside y's rows)
     void run_ss(int spin, const double* x, double* y, int64_t ldx, int64_t col_lo, int64_t col_hi, cudaStream_t s,
-                int64_t ldy = 0, int64_t ycol0 = 0);
+                int64_t ldy = 0, int64_t ycol0 = 0, int64_t col_pad = 0);
     // world > 1: the alpha-alpha term's beta-column window [aa_lo_, aa_hi_) lives in saa_ as
     // [NA][ldw_] starting at the aligned column aa_c0_
     int64_t aa_lo_ = 0, aa_hi_ = 0, aa_c0_ = 0, ldw_ = 0;

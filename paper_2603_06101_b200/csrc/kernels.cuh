@@ -62,6 +62,7 @@ struct SsPlan {
     int norb, nel, P, KSS, warps, npa;
     int64_t NK;
     size_t smem;
+    int bulk = 1;  // staged tiles reduced into y by TMA bulk reductions (UBLKRED)
 };
 SsPlan plan_sigma_ss(int norb, int nel);
 // generic fallback outside plan_sigma_ss's limits: the one-spin two-body operator as CSR
@@ -81,8 +82,10 @@ void build_ss_csr(int norb, int nel, const double* Va, SsCsr& out);
 // y may be a column window of the output: column c of row I at y[I * ldy + c - ycol0] (ldy 0 = ldx)
 void launch_sigma_ss_csr(const SsCsrDev& m, const double* x, double* y, int64_t ldx, int64_t col_lo, int64_t col_hi,
                          cudaStream_t st, int64_t ldy = 0, int64_t ycol0 = 0);
+// col_pad > col_hi: columns [col_hi, col_pad) are zero padding of x inside y's rows (whole tiles may
+// reduce across them)
 void launch_sigma_ss(const SsPlan& pl, const double* x, double* y, const double* Va, int64_t ldx, int64_t col_lo,
-                     int64_t col_hi, cudaStream_t st, int64_t ldy = 0, int64_t ycol0 = 0);
+                     int64_t col_hi, cudaStream_t st, int64_t ldy = 0, int64_t ycol0 = 0, int64_t col_pad = 0);
 // dst[c][r] = src[r][c] (+ dst if accumulate), for r < R, c < C; dst columns r in [R, dst_cols) zeroed,
 // columns >= dst_cols untouched (a column window of a wider destination).
 void launch_transpose(const double* src, int64_t R, int64_t C, int64_t lds, double* dst, int64_t ldd, int64_t dst_rows,

@@ -13,6 +13,7 @@
 // scattered rows; the batch dimension (the other spin) is contiguous, so gathers are coalesced
 // row reads and the scatter is a coalesced fp64 reduction (red.global.add.f64) into L2.
 #include <algorithm>
+#include <cstdlib>
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -39,6 +40,9 @@ struct SsParams {
     int64_t ldx, col_lo, col_hi;
     int tpc;  // column tiles per CTA
     int64_t ldy, ycol0;
+    int bulk;        // full tiles reduced by bulk copies (TMA engine) instead of per-lane reds
+    int64_t col_pad; // columns [col_hi, col_pad) are padding (x = 0 there, inside the y rows): a tile
+                     // ending there still reduces whole (it adds exact zeros)
 };
 
 template <int KSS>
@@ -128,6 +132,70 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
     };
     if (ntt > 0) load(0);
     cp_async_commit();
+    if (p.bulk) {
+        // One block barrier per tile. Each warp stages ITS OWN 16 rows of the tile in Ys and reduces
+        // them into y itself — whole rows by bulk reductions issued from lanes 0-15 (one 256-byte
+        // row segment each, executed by the TMA engine, not the LSU), edge tiles of a column window
+        // by per-lane reds — so no barrier is needed between the DMMAs and the reductions. A lane
+        // waits until the engine has read its previous row (wait_group.read) before the warp
+        // overwrites it.
+        const int64_t full_end = p.col_pad > p.col_hi ? p.col_pad : p.col_hi;
+        for (int tt = 0; tt < ntt; ++tt) {
+            const int64_t c0 = c_begin + (int64_t)tt * NTS;
+            cp_async_wait<0>();
+            __syncthreads();  // X(tt) visible; every warp is done with X(tt-1), whose buffer load(tt+1) refills
+            if (tt + 1 < ntt) load(tt + 1);
+            cp_async_commit();
+            const double* X = Xs + (tt & 1) * KPP * XSTRIDE;
+            double acc[NTS / 8][4];
+#pragma unroll
+            for (int nb = 0; nb < NTS / 8; ++nb)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) acc[nb][e] = 0.0;
+            // B fragments double-buffered in registers: k-step j+1's loads are in flight while the
+            // DMMAs of step j issue
+            double bq[2][NTS / 8];
+#pragma unroll
+            for (int nb = 0; nb < NTS / 8; ++nb) bq[0][nb] = X[t * XSTRIDE + g + nb * 8];
+#pragma unroll
+            for (int j = 0; j < KSS; ++j) {
+                const int cur = j & 1;
+                if (j + 1 < KSS) {
+#pragma unroll
+                    for (int nb = 0; nb < NTS / 8; ++nb) bq[cur ^ 1][nb] = X[(4 * (j + 1) + t) * XSTRIDE + g + nb * 8];
+                }
+#pragma unroll
+                for (int nb = 0; nb < NTS / 8; ++nb) dmma_16x8x4(acc[nb], a0[j], a1[j], bq[cur][nb]);
+            }
+            if (lane < 16) bulk_wait_read_all();  // this lane's previous row segment has been read
+            __syncwarp();
+#pragma unroll
+            for (int nb = 0; nb < NTS / 8; ++nb) {
+                const int col = nb * 8 + 2 * t;
+                *reinterpret_cast<double2*>(Ys + i0 * YSTRIDE + col) = make_double2(acc[nb][0], acc[nb][1]);
+                *reinterpret_cast<double2*>(Ys + (i0 + 8) * YSTRIDE + col) = make_double2(acc[nb][2], acc[nb][3]);
+            }
+            const bool whole = c0 >= p.col_lo && c0 + NTS <= full_end;
+            if (whole) {
+                fence_proxy_async_smem();  // the staged row is visible to the bulk-copy engine
+                __syncwarp();
+                const int r = 16 * w + lane;
+                if (lane < 16 && r < P) {
+                    bulk_reduce_add_f64(p.y + sRowY[r] + (c0 - p.ycol0), Ys + r * YSTRIDE, NTS * 8);
+                    bulk_commit();
+                }
+            } else {
+                __syncwarp();
+                if (c0 + lane >= p.col_lo && c0 + lane < p.col_hi) {
+                    double* ybase = p.y + (c0 + lane - p.ycol0);
+                    for (int r = 16 * w; r < 16 * w + 16 && r < P; ++r) red_add_f64(ybase + sRowY[r], Ys[r * YSTRIDE + lane]);
+                }
+            }
+        }
+        if (lane < 16) bulk_wait_all();  // every bulk reduction of this CTA has completed
+        cp_async_wait<0>();
+        return;
+    }
     for (int tt = 0; tt < ntt; ++tt) {
         const int64_t c0 = c_begin + (int64_t)tt * NTS;
         if (tt + 1 < ntt) load(tt + 1);
@@ -171,8 +239,8 @@ void launch_kss(const SsPlan& pl, const SsParams& prm, dim3 grid, cudaStream_t s
     static thread_local int configured = -1;
     int dev = 0;
     cudaGetDevice(&dev);
-    if (configured != dev) {
-        SBG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+    if (configured != dev) {  // the largest dynamic allocation any plan of this KSS may ask for
+        SBG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         configured = dev;
     }
     kern<<<grid, pl.warps * 32, pl.smem, st>>>(prm);
@@ -336,12 +404,16 @@ SsPlan plan_sigma_ss(int norb, int nel) {
     const int KPP = pl.KSS * 4;
     const int rows = std::max(KPP, 16 * pl.warps);
     pl.smem = (size_t)(2 * KPP * XSTRIDE + rows * YSTRIDE) * 8 + (size_t)KPP * 8 * 5 + 16;
+    // staged tiles reach y through TMA bulk reductions (cp.reduce.async.bulk .add.f64, one 256-byte
+    // row segment per instruction); SBG_SS_BULK=0 keeps the per-lane red.global.add form
+    const char* bulk_env = getenv("SBG_SS_BULK");
+    pl.bulk = !(bulk_env && atoi(bulk_env) == 0);
     if (pl.KSS > 32 || pl.warps > 8) throw InvalidArgument("sigma_ss: orbital space too large for this build");
     return pl;
 }
 
 void launch_sigma_ss(const SsPlan& pl, const double* x, double* y, const double* Va, int64_t ldx, int64_t col_lo,
-                     int64_t col_hi, cudaStream_t st, int64_t ldy, int64_t ycol0) {
+                     int64_t col_hi, cudaStream_t st, int64_t ldy, int64_t ycol0, int64_t col_pad) {
     if (ldy == 0) ldy = ldx;
     ensure_binomials();
     if (pl.P == 0 || pl.NK == 0 || col_hi <= col_lo) return;
@@ -354,7 +426,10 @@ void launch_sigma_ss(const SsPlan& pl, const double* x, double* y, const double*
     // (measured: c4 same-spin 33.4 -> 32.8 ms, c3 1.87 ms kept)
     int tpc = ntiles >= 256 ? kMaxTilesPerCta : std::min(kMaxTilesPerCta, 32);
     while (tpc > 4 && pl.NK * ((ntiles + tpc - 1) / tpc) < 8LL * nsm) tpc /= 2;
-    SsParams prm{x, y, Va, pl.norb, pl.nel, pl.P, pl.npa, ldx, col_lo, col_hi, tpc, ldy, ycol0};
+    if (const char* e = getenv("SBG_SS_TILES")) tpc = std::max(1, std::min(atoi(e), 4096));  // experiments
+    // bulk reductions need 16-byte aligned row segments (any padded library buffer is 256-byte aligned)
+    const int bulk = pl.bulk && ((uintptr_t)y % 16 == 0) && (ldy % 2 == 0) && (ycol0 % 2 == 0);
+    SsParams prm{x, y, Va, pl.norb, pl.nel, pl.P, pl.npa, ldx, col_lo, col_hi, tpc, ldy, ycol0, bulk, col_pad};
     const int64_t gy = (ntiles + tpc - 1) / tpc;
     dim3 grid((unsigned)pl.NK, (unsigned)gy);
     switch (pl.KSS) {

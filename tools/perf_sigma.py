@@ -1,5 +1,6 @@
 """Times sigma builds (device-resident, padded layout) per config with CUDA events."""
-import sys, time, json
+import sys, time, json, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 import paper_2603_06101_b200 as P
