@@ -156,6 +156,11 @@ int64_t sbg_padded_len(const sbg_ctx* ctx);
 int sbg_pack(sbg_ctx* ctx, const double* d_dense_full, double* d_padded_local, void* stream);
 int sbg_unpack(sbg_ctx* ctx, const double* d_padded_local, double* d_dense_local, void* stream);
 int sbg_sigma_padded(sbg_ctx* ctx, const double* d_x_padded_local, double* d_y_padded_local, void* stream);
+/* nvec sigma builds in one pass (padded device buffers, counts nvec applications): on one GPU the
+ * opposite-spin and alpha-alpha kernels take every vector in one launch, paying their per-row /
+ * per-string set-up once; SBCI2's pair and Davidson's expansion block use it. Any nvec >= 1. */
+int sbg_sigma_padded_multi(sbg_ctx* ctx, int nvec, const double* const* d_x_padded_local,
+                           double* const* d_y_padded_local, void* stream);
 uint64_t sbg_apply_count(const sbg_ctx* ctx);
 void sbg_reset_apply_count(sbg_ctx* ctx);
 uint64_t sbg_kernel_launches(const sbg_ctx* ctx);

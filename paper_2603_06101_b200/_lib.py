@@ -86,6 +86,7 @@ def lib() -> C.CDLL:
         "sbg_pack": (C.c_int, [P, P, P, P]),
         "sbg_unpack": (C.c_int, [P, P, P, P]),
         "sbg_sigma_padded": (C.c_int, [P, P, P, P]),
+        "sbg_sigma_padded_multi": (C.c_int, [P, C.c_int, C.POINTER(P), C.POINTER(P), P]),
         "sbg_apply_count": (C.c_uint64, [P]),
         "sbg_reset_apply_count": (None, [P]),
         "sbg_kernel_launches": (C.c_uint64, [P]),
@@ -119,7 +120,7 @@ EXPORTED = ["sbg_last_error", "sbg_version", "sbg_binomial", "sbg_determinant_co
             "sbg_config_validate", "sbg_synthetic_integrals", "sbg_shard_range", "sbg_device_count", "sbg_create",
             "sbg_create_dist", "sbg_nccl_unique_id", "sbg_destroy", "sbg_dim", "sbg_sector", "sbg_local_rows",
             "sbg_diagonal", "sbg_table_sizes", "sbg_string_tables", "sbg_sigma", "sbg_sigma_device",
-            "sbg_padded_len", "sbg_pack", "sbg_unpack", "sbg_sigma_padded", "sbg_apply_count",
+            "sbg_padded_len", "sbg_pack", "sbg_unpack", "sbg_sigma_padded", "sbg_sigma_padded_multi", "sbg_apply_count",
             "sbg_reset_apply_count", "sbg_kernel_launches", "sbg_sigma_flops", "sbg_profile_reset", "sbg_profile_read",
             "sbg_spin_squared", "sbg_spin_squared_padded", "sbg_local_group_create", "sbg_local_group_destroy",
             "sbg_create_local", "sbg_solve", "sbg_solve_davidson", "sbg_solve_state_sbci1", "sbg_selftest",

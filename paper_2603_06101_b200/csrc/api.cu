@@ -417,6 +417,17 @@ int sbg_sigma_padded(sbg_ctx* ctx, const double* dx, double* dy, void* stream) {
     });
 }
 
+int sbg_sigma_padded_multi(sbg_ctx* ctx, int nvec, const double* const* dx, double* const* dy, void* stream) {
+    return guarded([&] {
+        auto lk = lock_ctx(ctx);
+        if (nvec < 0 || (nvec > 0 && (!dx || !dy))) throw std::invalid_argument("sbg_sigma_padded_multi: bad arguments");
+        auto& c = *ctx->c;
+        cudaStream_t s = stream ? (cudaStream_t)stream : c.st;
+        for (int v0 = 0; v0 < nvec; v0 += sbg::kMaxSigmaVec)
+            c.sigma_multi(dx + v0, dy + v0, std::min(sbg::kMaxSigmaVec, nvec - v0), s);
+    });
+}
+
 int sbg_sigma_device(sbg_ctx* ctx, const double* d_x, double* d_y, void* stream) {
     return guarded([&] {
         auto lk = lock_ctx(ctx);

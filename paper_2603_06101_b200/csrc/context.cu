@@ -633,6 +633,49 @@ void Context::order_end(cudaStream_t s) {
     order_recorded_ = true;
 }
 
+void Context::sigma_multi(const double* const* x, double* const* y, int nvec, cudaStream_t s) {
+    const bool fused = nvec > 1 && nvec <= kMaxSigmaVec && world == 1 && have_ab_ && !direct_ab_ && ab_.tma &&
+                       ab_.npass == 1 && !ss_csr_[0] && !ss_csr_[1] && (ssa_.P == 0 || ssa_.bulk);
+    if (!fused) {
+        for (int v = 0; v < nvec; ++v) sigma(x[v], y[v], s);
+        return;
+    }
+    order_begin(s);
+    EvSet* ev = next_evset();
+    if (ev) {
+        SBG_CUDA(cudaEventRecord(ev->e[0], s));
+        SBG_CUDA(cudaEventRecord(ev->e[1], s));
+    }
+    // beta-beta per vector (the transposed operands are one vector's worth of scratch)
+    for (int v = 0; v < nvec; ++v) {
+        if (has_ss(1)) {
+            launch_transpose(x[v], nrows, NB, ld, xT_.p, ldT, NB, ldT, 0, s);
+            SBG_CUDA(cudaMemsetAsync(sT_.p, 0, (size_t)NB * ldT * 8, s));
+            run_ss(1, xT_.p, sT_.p, ldT, 0, nrows, s, 0, 0, ldT);
+            launch_transpose(sT_.p, NB, nrows, ldT, y[v], ld, nrows, ld, 0, s);
+            launches += 3;
+        } else {
+            SBG_CUDA(cudaMemsetAsync(y[v], 0, (size_t)nrows * ld * 8, s));
+        }
+    }
+    // alpha-alpha: every vector in one launch
+    if (ssa_.P > 0) {
+        launch_sigma_ss_multi(ssa_, x, y, nvec, d_Va_, ld, 0, NB, s, 0, 0, ld);
+        launches += 1;
+    }
+    if (ev) {
+        SBG_CUDA(cudaEventRecord(ev->e[2], s));
+        SBG_CUDA(cudaEventRecord(ev->e[3], s));
+    }
+    // alpha-beta + one-body + e_core: every vector in one launch
+    launch_sigma_ab_multi(ab_, AbScatter{d_sc_tgt_, d_sc_ent_, d_sc_tt_, d_sc_te_, red_pass_[0].first, red_pass_[0].second},
+                          x, y, nvec, d_Vp_, row_lo, row_hi, e_core, 1, nsm, s, 0);
+    launches += 1;
+    if (ev) SBG_CUDA(cudaEventRecord(ev->e[4], s));
+    order_end(s);
+    applies_.fetch_add((uint64_t)nvec, std::memory_order_relaxed);
+}
+
 Context::EvSet* Context::next_evset() {
     if (ev_used_ == ev_pool_.size()) {
         if (ev_pool_.size() >= 256) return nullptr;  // profile ring full: stop recording until read/reset

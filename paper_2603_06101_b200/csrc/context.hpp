@@ -106,6 +106,10 @@ public:
     void upload_rows(const double* host_dense_full, double* d_padded, int64_t lo, int64_t hi, cudaStream_t s) const;
     void download_rows(const double* d_padded, double* host_dense_local, int64_t lo, int64_t hi, cudaStream_t s) const;
     void sigma(const DBuf& x, DBuf& y) { sigma(x.p, y.p, st); }
+    // y_v = H x_v for nvec vectors; single GPU with the reduction kernels: the alpha-beta and
+    // alpha-alpha kernels take all vectors in one launch (per-row / per-K set-up paid once), the
+    // beta-beta term runs per vector; anything else: one sigma per vector. Counts nvec applications.
+    void sigma_multi(const double* const* x, double* const* y, int nvec, cudaStream_t s);
     // <S^2> of a padded local vector (fci/spin.hpp:17-51); collective over ranks
     double spin_squared(const double* x_local);
 

@@ -266,12 +266,22 @@ MultiStateResult davidson_solve(Context& c, int nroots, const SolverConfig& cfg,
             const double nm = o.norm(t);
             if (nm < std::sqrt(dcfg.lindep) * before) continue;  // direction already represented
             o.scale(t, 1.0 / nm);
-            DBuf h = c.vec();
-            o.apply(t, h);
-            dv.images_.push_back(std::move(h));
+            // the image is built after the loop, with the other new directions (orthogonalising the
+            // next correction needs the basis, not the images): one multi-vector sigma per block
             dv.basis_.push_back(std::move(t));
             t = c.vec();
             ++added;
+        }
+        if (added > 0) {  // images of the expansion block (davidson.hpp:184-194), in basis order
+            std::vector<const DBuf*> xs;
+            std::vector<DBuf*> ys;
+            const size_t first = dv.basis_.size() - (size_t)added;
+            for (int k = 0; k < added; ++k) dv.images_.push_back(c.vec());
+            for (int k = 0; k < added; ++k) {
+                xs.push_back(&dv.basis_[first + k]);
+                ys.push_back(&dv.images_[first + k]);
+            }
+            o.apply_multi(xs, ys);
         }
         peak_space = std::max(peak_space, (int)dv.basis_.size());
         if (added == 0 && !all_done) {

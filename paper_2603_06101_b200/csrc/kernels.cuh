@@ -25,6 +25,8 @@ void launch_diag(const uint64_t* sa, const uint64_t* sb, const double* ea, const
 void launch_scatter_codes(const uint64_t* sb, int64_t nb, int64_t ld, int norb, int npair, int npad, uint16_t* out,
                           cudaStream_t st);
 
+constexpr int kMaxSigmaVec = 4;  // vectors per multi-vector sigma launch
+
 // ---- sigma_ab.cu: opposite-spin term (+ folded one-body, + e_core), K6 ----
 struct AbPlan {
     int norb, na_el, nb_el, npair, npad, mb16, extra, K, KS, threads, maxT, maxE, nt, ws, red;
@@ -52,6 +54,10 @@ void build_ab_red_list(const AbPlan& pl, const std::vector<uint16_t>& codes, std
 void launch_sigma_ab(const AbPlan& pl, const AbScatter& sc, const double* x_full, double* y_local, const double* Vp,
                      int64_t row_lo, int64_t row_hi, double e_core, int accumulate, int grid, cudaStream_t st,
                      int pass = 0);
+// the same for nvec <= kMaxSigmaVec vectors in one launch (bulk-copy reduction kernel, pl.tma)
+void launch_sigma_ab_multi(const AbPlan& pl, const AbScatter& sc, const double* const* x_full, double* const* y_local,
+                           int nvec, const double* Vp, int64_t row_lo, int64_t row_hi, double e_core, int accumulate,
+                           int grid, cudaStream_t st, int pass = 0);
 // generic fallback outside plan_sigma_ab's limits: y(local rows) += sigma_ab + e_core x from the link tables
 void launch_sigma_ab_direct(const double* x_full, double* y_local, const double* Vp, int npair, const Excitation* la,
                             int La, const Excitation* lb, int Lb, int64_t row_lo, int64_t row_hi, int64_t NB, int64_t ld,
@@ -86,6 +92,10 @@ void launch_sigma_ss_csr(const SsCsrDev& m, const double* x, double* y, int64_t 
 // reduce across them)
 void launch_sigma_ss(const SsPlan& pl, const double* x, double* y, const double* Va, int64_t ldx, int64_t col_lo,
                      int64_t col_hi, cudaStream_t st, int64_t ldy = 0, int64_t ycol0 = 0, int64_t col_pad = 0);
+// nvec <= kMaxSigmaVec vectors (same layout each) in one launch (bulk-reduction kernel)
+void launch_sigma_ss_multi(const SsPlan& pl, const double* const* x, double* const* y, int nvec, const double* Va,
+                           int64_t ldx, int64_t col_lo, int64_t col_hi, cudaStream_t st, int64_t ldy = 0,
+                           int64_t ycol0 = 0, int64_t col_pad = 0);
 // dst[c][r] = src[r][c] (+ dst if accumulate), for r < R, c < C; dst columns r in [R, dst_cols) zeroed,
 // columns >= dst_cols untouched (a column window of a wider destination).
 void launch_transpose(const double* src, int64_t R, int64_t C, int64_t lds, double* dst, int64_t ldd, int64_t dst_rows,

@@ -194,8 +194,7 @@ public:
             out.dz = o_.norm(st.zra);
             return out;
         }
-        o_.apply(za_, hza_);
-        o_.apply(zb_, hzb_);
+        o_.apply_multi({&za_, &zb_}, {&hza_, &hzb_});  // the pair's two sigma builds in one pass (sbci2.hpp:209-210)
 
         const bool first = st.t == 0;
         SubspaceSolve sub;
@@ -503,8 +502,7 @@ Sbci2PairResult solve_pair(PairDriver& dr, Precond& pre, Deflation& defl, Seed l
                 o.zero(st.hyb);
                 ++st.restart_count;
                 if (cfg.hx_refresh_restarts > 0 && st.restart_count % cfg.hx_refresh_restarts == 0) {
-                    o.apply(st.xa, st.hxa);
-                    o.apply(st.xb, st.hxb);
+                    o.apply_multi({&st.xa, &st.xb}, {&st.hxa, &st.hxb});
                     result.hx_refreshes += 2;
                 }
                 o.combine(st.zra, 1.0, st.hxa, -st.ea, st.xa);

@@ -60,6 +60,11 @@ struct AbParams {
     int m0;                     // first pair row of this pass (pair-row blocks when npair > 136)
     int add_ecore;              // this pass adds e_core * x
     int tma;                    // k_sigma_ab_ws red mode: D rows and reduction lists by bulk copies
+    // several vectors in one launch (tma path): tile T of a row is tile T % ntiles of vector
+    // T / ntiles, so the per-row set-up (K-list, A fragments, pipeline fill) is paid once per row
+    int nvec;
+    const double* xv[kMaxSigmaVec];
+    double* yv[kMaxSigmaVec];
 };
 
 // Software pipeline per alpha row, one __syncthreads per tile: iteration `it` prefetches D(it+1)
@@ -314,6 +319,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
     constexpr int K0 = K0E ? 1 : 0;
     const int KP = K0 + KS * 4;
     const int ntiles = (int)(p.ld / NT);
+    const int ntot = ntiles * p.nvec;  // tiles per alpha row over all vectors
     // mbarriers of the bulk-copy pipeline: [0..1] D stage b landed, [2..3] list stage b landed
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
     double* srow = smem + 4;                 // [ld], absent in red mode
@@ -377,7 +383,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                         ak1[mb] = (K0E && ok) ? aval(rh + 8, 0) : 0.0;
                     }
                     bar_sync(BAR_MINT, kWsHalf);
-                    for (int it = 0; it < ntiles; ++it) {
+                    for (int it = 0; it < ntot; ++it) {
                         const int b = it & 1;
                         bar_sync(BAR_DREADY + b, kWsThreads);
                         if (it >= 2) bar_sync(BAR_EMPTY + b, kWsThreads);
@@ -414,7 +420,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                         }
                         bar_arrive(BAR_FULL + b, kWsThreads);
                     }
-                    for (int it = ntiles - 2 < 0 ? 0 : ntiles - 2; it < ntiles; ++it)
+                    for (int it = ntot - 2 < 0 ? 0 : ntot - 2; it < ntot; ++it)
                         bar_sync(BAR_EMPTY + (it & 1), kWsThreads);
                     continue;  // next row
                 }
@@ -436,7 +442,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
 #pragma unroll
             for (int j = 0; j < KS; ++j) aer[j] = do_extra ? sAe[(K0 + 4 * j + t) * 8 + g] : 0.0;
             const double ae0 = (K0E && do_extra) ? sAe[g] : 0.0;
-            for (int it = 0; it < ntiles; ++it) {
+            for (int it = 0; it < ntot; ++it) {
                 const int b = it & 1;
                 bar_sync(BAR_DREADY + b, kWsThreads);
                 if (it >= 2) bar_sync(BAR_EMPTY + b, kWsThreads);
@@ -500,7 +506,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                 }
                 bar_arrive(BAR_FULL + b, kWsThreads);
             }
-            for (int it = ntiles - 2 < 0 ? 0 : ntiles - 2; it < ntiles; ++it) bar_sync(BAR_EMPTY + (it & 1), kWsThreads);
+            for (int it = ntot - 2 < 0 ? 0 : ntot - 2; it < ntot; ++it) bar_sync(BAR_EMPTY + (it & 1), kWsThreads);
         }
     } else {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 " SBG_STR(SBG_WS_SREG) ";\n");
@@ -551,16 +557,20 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                 bar_sync(BAR_SINT, kWsHalf);  // sJ visible to the producer warp; previous row's lists read
                 bar_arrive(BAR_KLIST, kWsThreads);
                 const bool d_bulk = p.tma >= 2;
-                auto gather_d = [&](int stage, int jt) {  // tma == 1: D rows by cp.async, all loader threads
+                auto gather_d = [&](int stage, int T) {  // tma == 1: D rows by cp.async, all loader threads
                     if (p.dbg & 4) return;
+                    const int jt = T % ntiles;
+                    const double* xs = p.xv[T / ntiles];
                     double* dst = Ds + stage * KP * DSTRIDE;
                     for (int c = stid; c < KP * (NT / 2); c += kWsHalf) {
                         const int k = c / (NT / 2), part = c % (NT / 2);
-                        cp_async16(dst + k * DSTRIDE + part * 2, p.x + (int64_t)sJ[k] * p.ld + (int64_t)jt * NT + part * 2);
+                        cp_async16(dst + k * DSTRIDE + part * 2, xs + (int64_t)sJ[k] * p.ld + (int64_t)jt * NT + part * 2);
                     }
                     cp_async_commit();
                 };
-                auto issue_d = [&](int stage, int jt) {  // producer warp only
+                auto issue_d = [&](int stage, int T) {  // producer warp only
+                    const int jt = T % ntiles;
+                    const double* xs = p.xv[T / ntiles];
                     if (p.dbg & 4) {
                         if (plane == 0) mbar_arrive_expect_tx(mbar + stage, 0);
                         return;
@@ -570,9 +580,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                     __syncwarp();
                     double* dst = Ds + stage * KP * DSTRIDE;
                     for (int k = plane; k < KP; k += 32)
-                        bulk_g2s(dst + k * DSTRIDE, p.x + (int64_t)sJ[k] * p.ld + (int64_t)jt * NT, NT * 8, mbar + stage);
+                        bulk_g2s(dst + k * DSTRIDE, xs + (int64_t)sJ[k] * p.ld + (int64_t)jt * NT, NT * 8, mbar + stage);
                 };
-                auto issue_l = [&](int stage, int jt) {
+                auto issue_l = [&](int stage, int T) {
+                    const int jt = T % ntiles;
                     if (plane == 0) {
                         const uint32_t e0 = sTE[jt], bytes = (sTE[jt + 1] - e0) * 4;
                         fence_proxy_async_smem();
@@ -580,7 +591,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                         if (bytes) bulk_g2s(Le + stage * p.maxE, p.ent32 + e0, bytes, mbar + 2 + stage);
                     }
                 };
-                for (int jt = 0; jt < 2 && jt < ntiles; ++jt) {
+                for (int jt = 0; jt < 2 && jt < ntot; ++jt) {
                     if (prod) {
                         if (d_bulk) issue_d(jt, jt);
                         issue_l(jt, jt);
@@ -591,18 +602,18 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                     cp_async_wait<0>();
                     bar_sync(BAR_SINT, kWsHalf);
                 }
-                for (int jt = 0; jt < 2 && jt < ntiles; ++jt) {
+                for (int jt = 0; jt < 2 && jt < ntot; ++jt) {
                     if (d_bulk) {
                         mbar_wait_parity(mbar + jt, (phD >> jt) & 1u);
                         phD ^= 1u << jt;
                     }
                     bar_arrive(BAR_DREADY + jt, kWsThreads);
                 }
-                double* yrow = p.y + (ia - p.row_lo) * p.ld;
-                for (int it = 0; it < ntiles; ++it) {
-                    const int b = it & 1;
+                for (int it = 0; it < ntot; ++it) {
+                    const int b = it & 1, lt = it % ntiles;
+                    double* yrow = p.yv[it / ntiles] + (ia - p.row_lo) * p.ld;
                     bar_sync(BAR_FULL + b, kWsThreads);   // G(it) staged; D stage b free
-                    if (it + 2 < ntiles) {
+                    if (it + 2 < ntot) {
                         if (!d_bulk) gather_d(b, it + 2);
                         else if (prod) issue_d(b, it + 2);
                     }
@@ -611,7 +622,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                     if (!(p.dbg & 1)) {
                         const double* G = Gs + b * p.grows * GSTRIDE;
                         const uint32_t* l32 = reinterpret_cast<const uint32_t*>(Le + b * p.maxE);
-                        const uint32_t n = sTE[it + 1] - sTE[it];
+                        const uint32_t n = sTE[lt + 1] - sTE[lt];
 #pragma unroll RED_UNROLL
                         for (uint32_t i = stid; i < n; i += kWsHalf) {
                             const uint32_t en = l32[i];
@@ -623,7 +634,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                     bar_arrive(BAR_EMPTY + b, kWsThreads);
                     if (!d_bulk) cp_async_wait<0>();      // this thread's rows of D(it+2)
                     bar_sync(BAR_SINT, kWsHalf);          // lists stage b read by all; (cp.async) D(it+2) landed
-                    if (it + 2 < ntiles) {
+                    if (it + 2 < ntot) {
                         if (prod) issue_l(b, it + 2);
                         if (d_bulk) {
                             mbar_wait_parity(mbar + b, (phD >> b) & 1u);   // D(it+2) landed
@@ -632,9 +643,12 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                         bar_arrive(BAR_DREADY + b, kWsThreads);
                     }
                 }
-                const double* xr = p.x + ia * p.ld;  // e_core * x, reduced like the tiles
-                if (p.e_core != 0.0 && p.add_ecore)
-                    for (int64_t c = stid; c < p.NB; c += kWsHalf) red_add_f64(yrow + c, p.e_core * xr[c]);
+                if (p.e_core != 0.0 && p.add_ecore)  // e_core * x, reduced like the tiles
+                    for (int v = 0; v < p.nvec; ++v) {
+                        const double* xr = p.xv[v] + ia * p.ld;
+                        double* yrow = p.yv[v] + (ia - p.row_lo) * p.ld;
+                        for (int64_t c = stid; c < p.NB; c += kWsHalf) red_add_f64(yrow + c, p.e_core * xr[c]);
+                    }
             }
             return;
         }
@@ -994,11 +1008,24 @@ void build_ab_red_list(const AbPlan& pl, const std::vector<uint16_t>& codes, std
 
 void launch_sigma_ab(const AbPlan& pl, const AbScatter& sc, const double* x_full, double* y_local, const double* Vp,
                      int64_t row_lo, int64_t row_hi, double e_core, int accumulate, int grid, cudaStream_t st, int pass) {
+    launch_sigma_ab_multi(pl, sc, &x_full, &y_local, 1, Vp, row_lo, row_hi, e_core, accumulate, grid, st, pass);
+}
+
+void launch_sigma_ab_multi(const AbPlan& pl, const AbScatter& sc, const double* const* x_full, double* const* y_local,
+                           int nvec, const double* Vp, int64_t row_lo, int64_t row_hi, double e_core, int accumulate,
+                           int grid, cudaStream_t st, int pass) {
     ensure_binomials();
     if (row_hi <= row_lo) return;
+    if (nvec < 1 || nvec > kMaxSigmaVec || (nvec > 1 && !pl.tma))
+        throw InvalidArgument("sigma_ab: several vectors per launch need the bulk-copy reduction kernel");
     AbParams prm{};
-    prm.x = x_full;
-    prm.y = y_local;
+    prm.x = x_full[0];
+    prm.y = y_local[0];
+    prm.nvec = nvec;
+    for (int v = 0; v < nvec; ++v) {
+        prm.xv[v] = x_full[v];
+        prm.yv[v] = y_local[v];
+    }
     prm.Vp = Vp;
     prm.tgt = sc.tgt;
     prm.ent = sc.ent;

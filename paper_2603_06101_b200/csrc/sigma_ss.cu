@@ -43,6 +43,11 @@ struct SsParams {
     int bulk;        // full tiles reduced by bulk copies (TMA engine) instead of per-lane reds
     int64_t col_pad; // columns [col_hi, col_pad) are padding (x = 0 there, inside the y rows): a tile
                      // ending there still reduces whole (it adds exact zeros)
+    // several vectors per launch (bulk path): the CTA's tile sequence runs over its column tiles of
+    // vector 0, then of vector 1, ... so the per-K set-up is paid once
+    int nvec;
+    const double* xv[kMaxSigmaVec];
+    double* yv[kMaxSigmaVec];
 };
 
 template <int KSS>
@@ -120,14 +125,15 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
     const int64_t c_begin = (p.col_lo / NTS + (int64_t)blockIdx.y * p.tpc) * NTS;
     const int64_t c_end = ((p.col_hi + NTS - 1) / NTS) * NTS;
     const int ntt = (int)std::min<int64_t>(p.tpc, (c_end - c_begin) / NTS);
-    auto load = [&](int tt) {
-        const int64_t c0 = c_begin + (int64_t)tt * NTS;
+    auto load = [&](int tt) {  // tile tt of the sequence: column tile tt % ntt of vector tt / ntt
+        const int64_t c0 = c_begin + (int64_t)(tt % ntt) * NTS;
+        const double* xs = p.xv[tt / ntt];
         double* dst = Xs + (tt & 1) * KPP * XSTRIDE;
         for (int c = tid; c < KPP * (NTS / 2); c += nthr) {
             const int k = c / (NTS / 2), part = c % (NTS / 2);
             // the last tile may overhang the padded row: those columns are never reduced
             if (c0 + part * 2 < p.ldx)
-                cp_async16(dst + k * XSTRIDE + part * 2, p.x + (int64_t)sJ[k] * p.ldx + c0 + part * 2);
+                cp_async16(dst + k * XSTRIDE + part * 2, xs + (int64_t)sJ[k] * p.ldx + c0 + part * 2);
         }
     };
     if (ntt > 0) load(0);
@@ -140,11 +146,13 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
         // waits until the engine has read its previous row (wait_group.read) before the warp
         // overwrites it.
         const int64_t full_end = p.col_pad > p.col_hi ? p.col_pad : p.col_hi;
-        for (int tt = 0; tt < ntt; ++tt) {
-            const int64_t c0 = c_begin + (int64_t)tt * NTS;
+        const int nseq = ntt * p.nvec;
+        for (int tt = 0; tt < nseq; ++tt) {
+            const int64_t c0 = c_begin + (int64_t)(tt % ntt) * NTS;
+            double* const yv = p.yv[tt / ntt];
             cp_async_wait<0>();
             __syncthreads();  // X(tt) visible; every warp is done with X(tt-1), whose buffer load(tt+1) refills
-            if (tt + 1 < ntt) load(tt + 1);
+            if (tt + 1 < nseq) load(tt + 1);
             cp_async_commit();
             const double* X = Xs + (tt & 1) * KPP * XSTRIDE;
             double acc[NTS / 8][4];
@@ -181,13 +189,13 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
                 __syncwarp();
                 const int r = 16 * w + lane;
                 if (lane < 16 && r < P) {
-                    bulk_reduce_add_f64(p.y + sRowY[r] + (c0 - p.ycol0), Ys + r * YSTRIDE, NTS * 8);
+                    bulk_reduce_add_f64(yv + sRowY[r] + (c0 - p.ycol0), Ys + r * YSTRIDE, NTS * 8);
                     bulk_commit();
                 }
             } else {
                 __syncwarp();
                 if (c0 + lane >= p.col_lo && c0 + lane < p.col_hi) {
-                    double* ybase = p.y + (c0 + lane - p.ycol0);
+                    double* ybase = yv + (c0 + lane - p.ycol0);
                     for (int r = 16 * w; r < 16 * w + 16 && r < P; ++r) red_add_f64(ybase + sRowY[r], Ys[r * YSTRIDE + lane]);
                 }
             }
@@ -414,6 +422,14 @@ SsPlan plan_sigma_ss(int norb, int nel) {
 
 void launch_sigma_ss(const SsPlan& pl, const double* x, double* y, const double* Va, int64_t ldx, int64_t col_lo,
                      int64_t col_hi, cudaStream_t st, int64_t ldy, int64_t ycol0, int64_t col_pad) {
+    launch_sigma_ss_multi(pl, &x, &y, 1, Va, ldx, col_lo, col_hi, st, ldy, ycol0, col_pad);
+}
+
+void launch_sigma_ss_multi(const SsPlan& pl, const double* const* xv, double* const* yvs, int nvec, const double* Va,
+                           int64_t ldx, int64_t col_lo, int64_t col_hi, cudaStream_t st, int64_t ldy, int64_t ycol0,
+                           int64_t col_pad) {
+    const double* x = xv[0];
+    double* y = yvs[0];
     if (ldy == 0) ldy = ldx;
     ensure_binomials();
     if (pl.P == 0 || pl.NK == 0 || col_hi <= col_lo) return;
@@ -428,8 +444,15 @@ void launch_sigma_ss(const SsPlan& pl, const double* x, double* y, const double*
     while (tpc > 4 && pl.NK * ((ntiles + tpc - 1) / tpc) < 8LL * nsm) tpc /= 2;
     if (const char* e = getenv("SBG_SS_TILES")) tpc = std::max(1, std::min(atoi(e), 4096));  // experiments
     // bulk reductions need 16-byte aligned row segments (any padded library buffer is 256-byte aligned)
-    const int bulk = pl.bulk && ((uintptr_t)y % 16 == 0) && (ldy % 2 == 0) && (ycol0 % 2 == 0);
-    SsParams prm{x, y, Va, pl.norb, pl.nel, pl.P, pl.npa, ldx, col_lo, col_hi, tpc, ldy, ycol0, bulk, col_pad};
+    int bulk = pl.bulk && (ldy % 2 == 0) && (ycol0 % 2 == 0);
+    for (int v = 0; v < nvec; ++v) bulk = bulk && ((uintptr_t)yvs[v] % 16 == 0);
+    if (nvec < 1 || nvec > kMaxSigmaVec || (nvec > 1 && !bulk))
+        throw InvalidArgument("sigma_ss: several vectors per launch need the bulk-reduction kernel");
+    SsParams prm{x, y, Va, pl.norb, pl.nel, pl.P, pl.npa, ldx, col_lo, col_hi, tpc, ldy, ycol0, bulk, col_pad, nvec};
+    for (int v = 0; v < nvec; ++v) {
+        prm.xv[v] = xv[v];
+        prm.yv[v] = yvs[v];
+    }
     const int64_t gy = (ntiles + tpc - 1) / tpc;
     dim3 grid((unsigned)pl.NK, (unsigned)gy);
     switch (pl.KSS) {

@@ -114,6 +114,19 @@ public:
         L.run(c_);
     }
     void apply(const DBuf& x, DBuf& y) { c_.sigma(x, y); }
+    // several sigma builds at once (Context::sigma_multi; batches of kMaxSigmaVec)
+    void apply_multi(const std::vector<const DBuf*>& xs, const std::vector<DBuf*>& ys) {
+        for (size_t v0 = 0; v0 < xs.size(); v0 += kMaxSigmaVec) {
+            const double* xp[kMaxSigmaVec];
+            double* yp[kMaxSigmaVec];
+            const int n = (int)std::min<size_t>(kMaxSigmaVec, xs.size() - v0);
+            for (int v = 0; v < n; ++v) {
+                xp[v] = xs[v0 + v]->p;
+                yp[v] = ys[v0 + v]->p;
+            }
+            c_.sigma_multi(xp, yp, n, c_.st);
+        }
+    }
 
     // global element read / unit vector (rank-aware)
     double read(const DBuf& v, int64_t gidx) {

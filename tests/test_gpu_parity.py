@@ -731,3 +731,48 @@ def test_two_pass_guard_fallback_same_trajectory(dev, rest, gold_dir, monkeypatc
         runs.append(r.summary.device_vectors_peak)
     assert 0 < runs[1] < runs[0], runs
     op.close()
+
+
+@pytest.mark.parametrize("spec", [(10, 10, 0), (12, 12, 0), (8, 4, 0), (13, 5, 1), (17, 4, 0)])
+def test_multi_vector_sigma_matches_single(dev, rest, spec):
+    """sbg_sigma_padded_multi (SBCI2's pair and Davidson's expansion block): one launch of the
+    opposite-spin and alpha-alpha kernels over several vectors equals one sigma per vector; nvec = 5
+    spans two batches; sectors the fused path does not cover ((17o): pair-row passes) fall back."""
+    import ctypes as C
+    import torch
+    norb, nelec, ms2 = spec
+    if (norb, nelec) in ((10, 10), (12, 12)):
+        q = baseline_problem(1 if norb == 10 else 2, rest)
+    else:
+        h1, eri = rest.synthetic(norb, 31, 0.07)
+        q = Problem(norb, nelec, ms2, 0.3, h1, eri, "multi")
+    op = P.FciOperator(to_product(q), max_determinants=2 ** 62)
+    L = _lib.lib()
+    h = op.handle
+    n = op.dim()
+    pl = L.sbg_padded_len(h)
+    nv = 5
+    X = np.stack([seeded(n, 50 + k) for k in range(nv)])
+    ref = np.stack([rest.sigma(q, x, exact=True) for x in X])
+    s = torch.cuda.Stream()
+    sp = C.c_void_p(s.cuda_stream)
+    ptr = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    dx = [torch.from_numpy(x).cuda() for x in X]
+    torch.cuda.synchronize()
+    px = [torch.zeros(pl, dtype=torch.float64, device="cuda") for _ in range(nv)]
+    py = [torch.zeros(pl, dtype=torch.float64, device="cuda") for _ in range(nv)]
+    for a, b in zip(dx, px):
+        _lib.check(L.sbg_pack(h, ptr(a), ptr(b), sp))
+    for nvec in (2, 3, 5):
+        op.reset_apply_count()
+        xs = (C.c_void_p * nvec)(*[t.data_ptr() for t in px[:nvec]])
+        ys = (C.c_void_p * nvec)(*[t.data_ptr() for t in py[:nvec]])
+        _lib.check(L.sbg_sigma_padded_multi(h, nvec, xs, ys, sp))
+        assert op.apply_count() == nvec
+        out = torch.zeros(n, dtype=torch.float64, device="cuda")
+        for k in range(nvec):
+            _lib.check(L.sbg_unpack(h, ptr(py[k]), ptr(out), sp))
+            s.synchronize()
+            y = out.cpu().numpy()
+            assert np.abs(y - ref[k]).max() <= SIGMA_RTOL * np.abs(ref[k]).max(), (nvec, k)
+    op.close()
