@@ -118,6 +118,11 @@ struct LinArgs {
     double coef[kMaxOut][kMaxIn + kMaxOut];
     unsigned char da[kMaxDot], db[kMaxDot];  // dot slots
     unsigned int dmask;                       // slots read by the dots (set by launch_lincomb)
+    // optional weighted dot: dot index kdot accumulates s[da]^2 (kD_i - kshift) instead of
+    // s[da] s[db] (the trace's kinetic scalar y^T (D - E0) y, sbci1.hpp:135-139), kdot < 0: none
+    int kdot;
+    const double* kD;
+    double kshift;
 };
 struct ReduceWs {
     double* partial;  // [grid][kMaxRed]

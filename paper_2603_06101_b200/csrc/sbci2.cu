@@ -176,6 +176,8 @@ struct Sbci2StepData {
     double dE = 0.0, dz = 0.0;
     bool committed = false;
     double xa_norm = 0.0, xb_norm = 0.0, zrb_norm = 0.0;  // valid when committed
+    bool have_kinetic = false;  // kinetic scalar of the committed y'_a (traced solves, fused in the commit pass)
+    double kinetic = 0.0;
 };
 
 class PairDriver {
@@ -277,7 +279,12 @@ public:
             const int xa = L.out(merged ? sp_xa_.p : nullptr, {{sxa, 1.0}, {ya, co.b_aa}, {yb, co.b_ab}});
             const int xb = L.out(merged ? sp_xb_.p : nullptr, {{sxb, 1.0}, {ya, co.b_ba}, {yb, co.b_bb}});
             for (int k : {ya, yb, xa, xb, sxa, sxb}) L.dot(k, k);
+            if (want_kinetic) L.kinetic(ya, pre.D->p, pre.shift);
             const auto r = L.run(c_);
+            if (want_kinetic) {
+                out.have_kinetic = true;
+                out.kinetic = r[6];
+            }
             const double ya_nm = std::sqrt(r[0]), yb_nm = std::sqrt(r[1]);
             const double ingredients_a = std::sqrt(r[4]) + std::abs(co.b_aa) * ya_nm + std::abs(co.b_ab) * yb_nm;
             const double ingredients_b = std::sqrt(r[5]) + std::abs(co.b_ba) * ya_nm + std::abs(co.b_bb) * yb_nm;
@@ -371,6 +378,7 @@ public:
     SolverConfig cfg_;
     DBuf za_, zb_, hza_, hzb_, zrb_next_;
     DBuf sp_ya_, sp_yb_, sp_xa_, sp_xb_;  // candidate y', x' of the merged guard + commit pass
+    bool want_kinetic = false;            // traced solve: the commit pass also forms y'_a^T (D - E0) y'_a
     bool two_pass_ = std::getenv("SBG_GUARD_TWO_PASS") && std::atoi(std::getenv("SBG_GUARD_TWO_PASS")) != 0;
     bool spares() {
         if (two_pass_) return false;
@@ -407,6 +415,7 @@ Sbci2PairResult solve_pair(PairDriver& dr, Precond& pre, Deflation& defl, Seed l
     const int max_cycle = cfg.effective_max_cycle(kSbci2DefaultMaxCycle);
     Sbci2State st = init_pair(c, o, defl, std::move(lower), std::move(upper), cfg.lindep, alpha);
     if (track) pre.update_shift(st.ea);
+    dr.want_kinetic = (bool)trace;
     Sbci2PairResult result;
     {  // lower seed already converged: no update step, the upper seed carries over untouched
         const auto d = precondition(c, st.zra, pre, defl, dr.za_, st.xa, nullptr);
@@ -435,9 +444,13 @@ Sbci2PairResult solve_pair(PairDriver& dr, Precond& pre, Deflation& defl, Seed l
             rec.dE = step.dE;
             rec.res_norm = step.dz;
             rec.x_norm = step.committed ? step.xa_norm : o.norm(st.xa);
-            launch_kinetic(st.ya.p, pre.D->p, pre.shift, c.padded_len(), c.rws, c.st);
-            c.launches += 2;
-            rec.kinetic = c.finish_dots(1)[0];
+            if (step.committed && step.have_kinetic) {
+                rec.kinetic = step.kinetic;
+            } else {
+                launch_kinetic(st.ya.p, pre.D->p, pre.shift, c.padded_len(), c.rws, c.st);
+                c.launches += 2;
+                rec.kinetic = c.finish_dots(1)[0];
+            }
             rec.matvecs = c.applies().load();
             rec.b = st.coeffs.b_aa;
             rec.c = st.coeffs.c_aa;

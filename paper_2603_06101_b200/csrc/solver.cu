@@ -34,6 +34,8 @@ struct StepData {
     bool three = false;
     bool committed = false;
     double x_norm = 0.0;  // |x| after the step (valid when committed)
+    bool have_kinetic = false;  // kinetic scalar of the committed y' (traced solves, fused in the commit pass)
+    double kinetic = 0.0;
 };
 
 std::optional<RestartReason> check_restart(int alpha, double b, double dE, double x_norm, double dz, int t,
@@ -206,12 +208,17 @@ public:
             L.dot(xn, xn);
             L.dot(yn, yn);
             for (int s : sxc) L.dot(s, zn);
+            if (trace_) L.kinetic(yn, pre.D->p, pre.shift);
             const auto r = L.run(c_);
             zz2 = r[0];
             xx2 = r[1];
             if (std::sqrt(nxx) + std::abs(b) * std::sqrt(r[2]) > 1e6 * std::max(std::sqrt(xx2), 1e-300)) {
                 out.outcome = StepOutcome::restart(RestartReason::StallSmallB);
                 return out;
+            }
+            if (trace_) {
+                out.have_kinetic = true;
+                out.kinetic = r.back();
             }
             Lin W;
             const int wx = W.in(st.x.p), wy = W.in(st.y.p), wz = W.in(z_.p), whx = W.in(st.hx.p), why = W.in(st.hy.p),
@@ -222,7 +229,7 @@ public:
             const int hx2 = W.out(st.hx.p, {{whx, 1.0}, {hy2, b}});
             W.out(st.zres.p, {{hx2, 1.0 / k}, {x2, -e_new / k}});
             W.run(c_);
-            ovl.assign(r.begin() + 3, r.end());
+            ovl.assign(r.begin() + 3, r.begin() + 3 + sxc.size());
             if (!fused_ovl) ovl = deflation_overlaps(c_, defl, st.zres);
             ovl = defl.sequential(std::move(ovl));
         } else {
@@ -242,6 +249,7 @@ public:
             L.dot(xn, xn);
             L.dot(yn, yn);
             for (int s : sxc) L.dot(s, zn);
+            if (trace_) L.kinetic(yn, pre.D->p, pre.shift);  // folded here instead of a pass of its own
             const auto r = L.run(c_);
             zz2 = r[0];
             xx2 = r[1];
@@ -249,12 +257,16 @@ public:
                 out.outcome = StepOutcome::restart(RestartReason::StallSmallB);
                 return out;
             }
+            if (trace_) {
+                out.have_kinetic = true;
+                out.kinetic = r.back();
+            }
             std::swap(st.y, sp_y_);
             std::swap(st.hy, sp_hy_);
             std::swap(st.x, sp_x_);
             std::swap(st.hx, sp_hx_);
             std::swap(st.zres, sp_z_);
-            ovl.assign(r.begin() + 3, r.end());
+            ovl.assign(r.begin() + 3, r.begin() + 3 + sxc.size());
             if (!fused_ovl) ovl = deflation_overlaps(c_, defl, st.zres);
             ovl = defl.sequential(std::move(ovl));
         }
@@ -403,9 +415,13 @@ Sbci1Result solve_state(Driver& dr, Precond& pre, Deflation& defl, Seed seed, in
             rec.dE = step.dE;
             rec.res_norm = step.dz;
             rec.x_norm = step.committed ? step.x_norm : o.norm(st.x);
-            launch_kinetic(st.y.p, pre.D->p, pre.shift, c.padded_len(), c.rws, c.st);
-            c.launches += 2;
-            rec.kinetic = c.finish_dots(1)[0];
+            if (step.have_kinetic) {
+                rec.kinetic = step.kinetic;
+            } else {  // no commit this step: y is unchanged, one pass of its own
+                launch_kinetic(st.y.p, pre.D->p, pre.shift, c.padded_len(), c.rws, c.st);
+                c.launches += 2;
+                rec.kinetic = c.finish_dots(1)[0];
+            }
             rec.matvecs = c.applies().load();
             rec.b = st.b_prev;
             rec.c = st.c_prev;

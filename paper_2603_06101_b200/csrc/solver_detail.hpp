@@ -30,7 +30,18 @@ inline double ms_since(Clk::time_point t) { return std::chrono::duration<double,
 // ------------------------------------------------------------------ fused pass builder
 struct Lin {
     LinArgs a{};
-    Lin() { std::memset(&a, 0, sizeof(a)); }
+    Lin() {
+        std::memset(&a, 0, sizeof(a));
+        a.kdot = -1;
+    }
+    // sum_i s[slot]_i^2 (D_i - shift) as one more dot of the pass (the trace's kinetic scalar)
+    int kinetic(int slot, const double* D, double shift) {
+        const int d = dot(slot, slot);
+        a.kdot = d;
+        a.kD = D;
+        a.kshift = shift;
+        return d;
+    }
     bool fits(int more_in) const { return a.nin + more_in <= kMaxIn; }
     int in(const double* p) {
         if (a.nin >= kMaxIn) throw std::invalid_argument("fused pass: too many inputs");

@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(kThreads, ND > 4 ? 2 : SBG_VEC_MINB) k_lincomb
 #pragma unroll
         for (int k = 0; k < NI; ++k)
             if (k < a.nin) in[k] = reinterpret_cast<const double2*>(a.in[k])[i];
+        const double2 kd = (ND > 0 && a.kdot >= 0) ? reinterpret_cast<const double2*>(a.kD)[i] : make_double2(0.0, 0.0);
         double2 outv[NO];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -92,7 +93,12 @@ __global__ void __launch_bounds__(kThreads, ND > 4 ? 2 : SBG_VEC_MINB) k_lincomb
 #pragma unroll
                 for (int d = 0; d < ND; ++d) {
                     if (d >= a.ndot) break;
-                    acc[d] = fma(stage[a.da[d]][threadIdx.x], stage[a.db[d]][threadIdx.x], acc[d]);
+                    if (d == a.kdot) {
+                        const double yy = stage[a.da[d]][threadIdx.x];
+                        acc[d] += __dmul_rn(__dmul_rn(yy, yy), __dsub_rn(h ? kd.y : kd.x, a.kshift));
+                    } else {
+                        acc[d] = fma(stage[a.da[d]][threadIdx.x], stage[a.db[d]][threadIdx.x], acc[d]);
+                    }
                 }
             }
         }
@@ -472,6 +478,8 @@ void launch_lincomb(const LinArgs& args, const ReduceWs& ws, cudaStream_t st) {
     for (int d = 0; d < a.ndot; ++d) a.dmask |= (1u << a.da[d]) | (1u << a.db[d]);
     for (int k = 0; k < a.nin; ++k) check_aligned(a.in[k]);
     for (int j = 0; j < a.nout; ++j) check_aligned(a.out[j]);
+    if (a.kdot >= a.ndot || (a.kdot >= 0 && !a.kD)) throw InvalidArgument("launch_lincomb: bad weighted dot");
+    if (a.kdot >= 0) check_aligned(a.kD);
     if (a.nin <= 3) run_lincomb_no<3>(a, ws, st);
     else if (a.nin <= 6) run_lincomb_no<6>(a, ws, st);
     else run_lincomb_no<kMaxIn>(a, ws, st);

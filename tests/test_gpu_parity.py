@@ -776,3 +776,30 @@ def test_multi_vector_sigma_matches_single(dev, rest, spec):
             y = out.cpu().numpy()
             assert np.abs(y - ref[k]).max() <= SIGMA_RTOL * np.abs(ref[k]).max(), (nvec, k)
     op.close()
+
+
+@pytest.mark.parametrize("method", ["sbci1", "sbci2"])
+def test_trace_matches_reference_trace(dev, gold_dir, tmp_path, method):
+    """Per-iteration trace records (trace.hpp:22-44) of the device solve against the reference's own
+    CSV trace of the same solve on the h6_4e fixture: same rows, restart tags and matvec counts, and
+    the scalars — including the kinetic y^T (D - E0) y that the device forms inside the commit pass
+    (sbci1.hpp:135-139) — to rounding."""
+    from oracle import Reference
+    if not Reference.available():
+        pytest.skip("oracle/_ref/libsbci_ref.so not built")
+    p, q = fixture(gold_dir, "h6_4e")
+    m = 1 if method == "sbci1" else 2
+    path = tmp_path / "ref.csv"
+    Reference().solve(q, 3, method=m, trace_csv=str(path))
+    ref = P.read_trace_csv_file(str(path))
+    op = P.as_operator(p, p.ms2)
+    mine = []
+    (P.solve_n_states_sbci1 if m == 1 else P.solve_n_states_sbci2)(op, 3, sink=mine.append)
+    assert len(mine) == len(ref) > 10
+    for a, b in zip(mine, ref):
+        assert (a.method, a.state, a.pair_partner, a.t, a.matvecs, a.restart_reason) == \
+               (b.method, b.state, b.pair_partner, b.t, b.matvecs, b.restart_reason)
+        for f in ("energy", "x_norm", "kinetic"):
+            va, vb = getattr(a, f), getattr(b, f)
+            assert abs(va - vb) <= 1e-9 * max(1.0, abs(vb)), (f, a.state, a.t, va, vb)
+    op.close()
