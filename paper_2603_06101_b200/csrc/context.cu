@@ -231,6 +231,7 @@ Context::Context(int norb_, int nelec_, int ms2_, double e_core_, const double* 
     SBG_CUDA(cudaEventCreate(&ev0_));
     SBG_CUDA(cudaEventCreate(&ev1_));
     SBG_CUDA(cudaEventCreateWithFlags(&ev_order_, cudaEventDisableTiming));
+    SBG_CUDA(cudaEventCreateWithFlags(&ev_dots_, cudaEventDisableTiming));
 
     if (world > 1) {
         if (local_group && local_group->world != world) throw InvalidArgument("local group: world mismatch");
@@ -270,6 +271,7 @@ Context::~Context() {
     if (ev0_) cudaEventDestroy(ev0_);
     if (ev1_) cudaEventDestroy(ev1_);
     if (ev_order_) cudaEventDestroy(ev_order_);
+    if (ev_dots_) cudaEventDestroy(ev_dots_);
     for (cudaEvent_t e : {ev_in_, ev_gathered_, ev_aa_, ev_xdone_, ev_ab_})
         if (e) cudaEventDestroy(e);
     if (comm_st_) {
@@ -540,6 +542,17 @@ double Context::spin_squared(const double* x_local) {
 
 void Context::allreduce_inplace_device(double* d, int count) {
     if (world > 1 && count > 0) comm_->all_reduce_sum(d, (size_t)count, st);
+}
+
+void Context::post_dots(int ndot) {
+    allreduce_inplace_device(rws.result, ndot);
+    SBG_CUDA(cudaMemcpyAsync(rws.host, rws.result, ndot * 8, cudaMemcpyDeviceToHost, st));
+    SBG_CUDA(cudaEventRecord(ev_dots_, st));
+}
+
+const double* Context::wait_dots() {
+    SBG_CUDA(cudaEventSynchronize(ev_dots_));
+    return rws.host;
 }
 
 const double* Context::finish_dots(int ndot) {

@@ -127,6 +127,10 @@ public:
     // reductions: dot buffer all-reduced over ranks and copied to host
     ReduceWs rws;
     const double* finish_dots(int ndot);  // sync; returns host pointer
+    // the same split in two: post_dots enqueues the all-reduce and the copy to the host and records
+    // an event; wait_dots waits for that event only — kernels enqueued in between keep running
+    void post_dots(int ndot);
+    const double* wait_dots();
     void allreduce_inplace_device(double* d, int count);
 
     // per-phase CUDA-event profile of sigma calls (sbg_profile_*)
@@ -181,6 +185,7 @@ private:
     // device-side order of sigma builds issued on different streams (they share xT_, sT_, xfull_, the
     // alpha-alpha buffers): every build waits for the previous one's completion event
     cudaEvent_t ev_order_ = nullptr;
+    cudaEvent_t ev_dots_ = nullptr;  // post_dots -> wait_dots
     bool order_recorded_ = false;
     void order_begin(cudaStream_t s);
     void order_end(cudaStream_t s);

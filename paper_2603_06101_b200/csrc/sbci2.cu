@@ -189,7 +189,7 @@ public:
     Sbci2StepData step(Sbci2State& st, const Precond& pre, const Deflation& defl, int max_cycle) {
         Sbci2StepData out;
         const auto da = precondition(c_, st.zra, pre, defl, za_, st.xa, nullptr);
-        precondition(c_, st.zrb, pre, defl, zb_, st.xb, nullptr);
+        precondition_post(c_, st.zrb, pre, defl, zb_, st.xb, nullptr);  // z_b's dots are not used: no wait
         if (std::sqrt(da[2]) < cfg_.lindep * std::sqrt(da[0])) {
             st.ea = rayleigh(o_, st.xa, st.hxa);
             out.outcome = StepOutcome::converged();

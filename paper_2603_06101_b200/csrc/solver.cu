@@ -52,8 +52,10 @@ static std::vector<double> h_ovl(Context& c, int n) {
     return std::vector<double>(h, h + n);
 }
 
-std::vector<double> precondition(Context& c, const DBuf& zres, const Precond& pre, const Deflation& defl, DBuf& z,
-                                 const DBuf& x, const DBuf* y) {
+// precondition() up to the dots: z is enqueued, its dots are posted (Context::post_dots); returns
+// their count. The caller collects them with Context::wait_dots.
+int precondition_post(Context& c, const DBuf& zres, const Precond& pre, const Deflation& defl, DBuf& z,
+                      const DBuf& x, const DBuf* y) {
     PrecArgs pa{};
     pa.n = c.padded_len();
     pa.zres = zres.p;
@@ -77,7 +79,14 @@ std::vector<double> precondition(Context& c, const DBuf& zres, const Precond& pr
     launch_precond(pa, c.rws, c.st);
     c.launches += 2;
     const int nd = y ? 6 : 3;
-    const double* h = c.finish_dots(nd);
+    c.post_dots(nd);
+    return nd;
+}
+
+std::vector<double> precondition(Context& c, const DBuf& zres, const Precond& pre, const Deflation& defl, DBuf& z,
+                                 const DBuf& x, const DBuf* y) {
+    const int nd = precondition_post(c, zres, pre, defl, z, x, y);
+    const double* h = c.wait_dots();
     return std::vector<double>(h, h + nd);  // xx, xz, zz [, xy, yy, yz]
 }
 
@@ -95,8 +104,22 @@ public:
         StepData out;
         bool use_three = st.t >= 1;
         auto tp = Clk::now();
-        const auto d = make_z(st, pre, defl, use_three);
+        // H z is enqueued right behind z, before the host reads z's dots: the Gram-Schmidt scalars
+        // are formed while the sigma kernels run. The branches that end the step before the
+        // reference applies the operator (sbci1.hpp:153-184) take that application back from the
+        // counter, so matvec counts stay the reference's.
+        const int nd = precondition_post(c_, st.zres, pre, defl, z_, st.x, use_three ? &st.y : nullptr);
+        if (speculate_) o_.apply(z_, hz_);
+        const double* hd = c_.wait_dots();
+        const std::vector<double> d(hd, hd + nd);
         g_ph[0] += ms_since(tp);
+        struct Unapply {  // the speculative sigma is not an application of the reference's step
+            Context& c;
+            bool on;
+            ~Unapply() {
+                if (on) c.applies().fetch_sub(1, std::memory_order_relaxed);
+            }
+        } unapply{c_, speculate_};
         const double nxx = d[0], nxz = d[1], nzz = d[2];
         if (std::sqrt(nzz) < cfg_.lindep * std::sqrt(nxx)) {
             const double xhx = o_.dot(st.x, st.hx);
@@ -124,8 +147,9 @@ public:
                 return out;
             }
         }
+        unapply.on = false;  // the step applies the operator here (sbci1.hpp:186)
         tp = Clk::now();
-        o_.apply(z_, hz_);
+        if (!speculate_) o_.apply(z_, hz_);
         g_ph[1] += ms_since(tp);
         tp = Clk::now();
 
@@ -345,6 +369,7 @@ public:
     DBuf z_, hz_;
     DBuf sp_y_, sp_hy_, sp_x_, sp_hx_, sp_z_;  // candidate state of the merged guard + commit pass
     bool two_pass_ = std::getenv("SBG_GUARD_TWO_PASS") && std::atoi(std::getenv("SBG_GUARD_TWO_PASS")) != 0;
+    bool speculate_ = !(std::getenv("SBG_SPECULATE") && std::atoi(std::getenv("SBG_SPECULATE")) == 0);
 
     // the merged guard + commit pass needs five spare vectors; without room for them the step
     // falls back to the two-pass form for the rest of the solve (large sectors)

@@ -294,6 +294,9 @@ constexpr int kMaxDeflated = 8;  // precondition() folds up to 8 deflated states
 // dots xx, xz, zz [, xy, yy, yz] of x (and y when given) against the new z
 std::vector<double> precondition(Context& c, const DBuf& zres, const Precond& pre, const Deflation& defl, DBuf& z,
                                  const DBuf& x, const DBuf* y);
+// the same without waiting: the dots are posted (Context::post_dots / wait_dots); returns their count
+int precondition_post(Context& c, const DBuf& zres, const Precond& pre, const Deflation& defl, DBuf& z,
+                      const DBuf& x, const DBuf* y);
 
 struct Sbci1Result {
     StateResult pair;
