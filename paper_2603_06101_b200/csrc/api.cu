@@ -3,6 +3,7 @@
 #include <nccl.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <numeric>
@@ -335,7 +336,11 @@ int sbg_sigma(sbg_ctx* ctx, const double* x, double* y, int nvec) {
         // term of block i starts as soon as block i has landed, and block i of y is copied out as
         // soon as its alpha-beta launch is done — so the first upload and the last download overlap
         // the sigma they feed instead of standing alone.
-        const int nb = c.rowblocks_ok() ? 4 : 1;
+        static const int io_blocks = [] {
+            const char* e = std::getenv("SBG_IO_BLOCKS");
+            return e ? std::max(1, std::min(64, std::atoi(e))) : 4;
+        }();
+        const int nb = c.rowblocks_ok() ? io_blocks : 1;
         cudaStream_t cin = c.copy_stream(0), cout = c.copy_stream(1);
         std::vector<cudaEvent_t> up((size_t)nvec * nb), yd((size_t)nvec * nb), down(nvec);
         auto mk = [](cudaEvent_t& e) { SBG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)); };
