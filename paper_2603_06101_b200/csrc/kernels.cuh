@@ -123,7 +123,18 @@ struct LinArgs {
     int kdot;
     const double* kD;
     double kshift;
+    // coefficients read from device memory ([kMaxOut][kMaxIn + kMaxOut], written by an earlier kernel
+    // of the same stream) instead of coef: the SBCI1 commit pass after launch_step_scalars
+    const double* dcoef;
 };
+// ---- step_scalars.cu: the SBCI1 step's 2x2/3x3 algebra on one device thread ----
+struct StepScalarArgs {
+    double Ax, Bx, By, Cx, Cy, Cz;  // Gram-Schmidt triangle (ortho.hpp:45-76)
+    int three;                      // 3-vector {x, y, z} form
+};
+// dots: the subspace pass's m x m cross dots; coef: the commit pass's coefficient table; out[0..8]:
+// restart flag, k, b, c, E', second Ritz value, its x/y/z coefficients
+void launch_step_scalars(const double* dots, const StepScalarArgs& a, double* coef, double* out, cudaStream_t st);
 struct ReduceWs {
     double* partial;  // [grid][kMaxRed]
     double* result;   // [kMaxRed] device

@@ -171,51 +171,18 @@ public:
         launch_subspace(sa, c_.rws, c_.st);
         c_.launches += 2;
         const int m = use_three ? 3 : 2;
-        const double* h = c_.finish_dots(m * m);
-        SmallMatrix v(m);
-        for (int i = 0; i < m; ++i)
-            for (int j = i; j < m; ++j) v(i, j) = v(j, i) = 0.5 * (h[i * m + j] + h[j * m + i]);
-        g_ph[2] += ms_since(tp);
-        tp = Clk::now();
-        const SmallEigResult eig = jacobi_symmetric_eig(v);
-        g_ph[3] += ms_since(tp);
-        tp = Clk::now();
-
-        const double vx = eig.eigenvectors(0, 0), vy = use_three ? eig.eigenvectors(1, 0) : 0.0,
-                     vz = eig.eigenvectors(m - 1, 0);
-        const double wx = eig.eigenvectors(0, 1), wy = use_three ? eig.eigenvectors(1, 1) : 0.0,
-                     wz = eig.eigenvectors(m - 1, 1);
-        const double e_new = eig.eigenvalues[0];
-        const double k_den = vx * gs.A_x + vy * gs.B_x + vz * gs.C_x;
-        if (std::abs(k_den) < 1e-14) {
-            out.outcome = StepOutcome::restart(RestartReason::StallSmallB);
-            return out;
-        }
-        const double k = 1.0 / k_den;
-        double b, c;
-        if (use_three) {
-            const double b_den = vy * gs.B_y + vz * gs.C_y;
-            if (std::abs(b_den) < 1e-14) {
-                out.outcome = StepOutcome::restart(RestartReason::StallSmallB);
-                return out;
-            }
-            b = k * b_den;
-            c = -vz * gs.C_z / b_den;
-        } else {
-            b = 1.0;
-            c = -k * vz * gs.C_z;
-        }
-        // guard + commit in one pass (sbci1.hpp:259-267): y' = y - c z, Hy' = Hy - c Hz,
-        // x' = x + b y', Hx' = Hx + b Hy', z' = (1/k) Hx' - (E'/k) x' are written into spare
-        // buffers with |z'|^2, |x'|^2, |y'|^2 and the deflation overlaps x_c . z'; the cancellation
-        // guard is then evaluated from those norms and the spares are swapped in only if it passes
-        // (a rejected step leaves the state untouched, as in the reference)
+        double e_new = 0.0, k = 0.0, b = 0.0, c = 0.0;
         double zz2, xx2;
         std::vector<double> ovl;
-        if (!spares()) {
-            // two-pass form when the five spares do not fit in HBM (or SBG_GUARD_TWO_PASS=1): the
-            // candidate norms first (read-only pass, the same per-element arithmetic and reduction
-            // tree, so the same values), then — only if the guard passes — the commit in place
+        if (device_scalars_ && spares()) {
+            // The subspace matrix, its Jacobi eigenpairs, k, b, c and the commit coefficients are
+            // formed on one device thread (step_scalars.cu, the host's arithmetic bit for bit) and
+            // the commit pass reads its coefficients from device memory: no host round trip between
+            // the subspace pass and the commit pass. The scalars come back with the commit's dots.
+            StepScalarArgs sca{gs.A_x, gs.B_x, gs.B_y, gs.C_x, gs.C_y, gs.C_z, use_three ? 1 : 0};
+            launch_step_scalars(c_.rws.result, sca, dcoef_.p, dscal_.p, c_.st);
+            c_.launches += 1;
+            SBG_CUDA(cudaMemcpyAsync(hscal_, dscal_.p, 9 * sizeof(double), cudaMemcpyDeviceToHost, c_.st));
             Lin L;
             const int sx = L.in(st.x.p), sy = L.in(st.y.p), sz = L.in(z_.p), shx = L.in(st.hx.p),
                       shy = L.in(st.hy.p), shz = L.in(hz_.p);
@@ -223,58 +190,33 @@ public:
             const bool fused_ovl = L.fits((int)defl.size());
             if (fused_ovl)
                 for (auto& mm : defl.m) sxc.push_back(L.in(mm.x.p));
-            const int yn = use_three ? L.out(nullptr, {{sy, 1.0}, {sz, -c}}) : L.out(nullptr, {{sz, -c}});
-            const int hyn = use_three ? L.out(nullptr, {{shy, 1.0}, {shz, -c}}) : L.out(nullptr, {{shz, -c}});
-            const int xn = L.out(nullptr, {{sx, 1.0}, {yn, b}});
-            const int hxn = L.out(nullptr, {{shx, 1.0}, {hyn, b}});
-            const int zn = L.out(nullptr, {{hxn, 1.0 / k}, {xn, -e_new / k}});
+            // the same pass shape as below; the coefficients themselves come from dcoef_
+            const int yn = use_three ? L.out(sp_y_.p, {{sy, 1.0}, {sz, 1.0}}) : L.out(sp_y_.p, {{sz, 1.0}});
+            const int hyn = use_three ? L.out(sp_hy_.p, {{shy, 1.0}, {shz, 1.0}}) : L.out(sp_hy_.p, {{shz, 1.0}});
+            const int xn = L.out(sp_x_.p, {{sx, 1.0}, {yn, 1.0}});
+            const int hxn = L.out(sp_hx_.p, {{shx, 1.0}, {hyn, 1.0}});
+            const int zn = L.out(sp_z_.p, {{hxn, 1.0}, {xn, 1.0}});
+            L.a.dcoef = dcoef_.p;
             L.dot(zn, zn);
             L.dot(xn, xn);
             L.dot(yn, yn);
-            for (int s : sxc) L.dot(s, zn);
+            for (int s2 : sxc) L.dot(s2, zn);
             if (trace_) L.kinetic(yn, pre.D->p, pre.shift);
-            const auto r = L.run(c_);
-            zz2 = r[0];
-            xx2 = r[1];
-            if (std::sqrt(nxx) + std::abs(b) * std::sqrt(r[2]) > 1e6 * std::max(std::sqrt(xx2), 1e-300)) {
+            const auto r = L.run(c_);  // synchronises: hscal_ is valid too
+            g_ph[2] += ms_since(tp);
+            tp = Clk::now();
+            if (hscal_[0] != 0.0) {  // |k_den| or |b_den| < 1e-14 (sbci1.hpp:230-246): restart, no commit
                 out.outcome = StepOutcome::restart(RestartReason::StallSmallB);
                 return out;
             }
-            if (trace_) {
-                out.have_kinetic = true;
-                out.kinetic = r.back();
-            }
-            Lin W;
-            const int wx = W.in(st.x.p), wy = W.in(st.y.p), wz = W.in(z_.p), whx = W.in(st.hx.p), why = W.in(st.hy.p),
-                      whz = W.in(hz_.p);
-            const int y2 = use_three ? W.out(st.y.p, {{wy, 1.0}, {wz, -c}}) : W.out(st.y.p, {{wz, -c}});
-            const int hy2 = use_three ? W.out(st.hy.p, {{why, 1.0}, {whz, -c}}) : W.out(st.hy.p, {{whz, -c}});
-            const int x2 = W.out(st.x.p, {{wx, 1.0}, {y2, b}});
-            const int hx2 = W.out(st.hx.p, {{whx, 1.0}, {hy2, b}});
-            W.out(st.zres.p, {{hx2, 1.0 / k}, {x2, -e_new / k}});
-            W.run(c_);
-            ovl.assign(r.begin() + 3, r.begin() + 3 + sxc.size());
-            if (!fused_ovl) ovl = deflation_overlaps(c_, defl, st.zres);
-            ovl = defl.sequential(std::move(ovl));
-        } else {
-            Lin L;
-            const int sx = L.in(st.x.p), sy = L.in(st.y.p), sz = L.in(z_.p), shx = L.in(st.hx.p),
-                      shy = L.in(st.hy.p), shz = L.in(hz_.p);
-            std::vector<int> sxc;
-            const bool fused_ovl = L.fits((int)defl.size());
-            if (fused_ovl)
-                for (auto& mm : defl.m) sxc.push_back(L.in(mm.x.p));
-            const int yn = use_three ? L.out(sp_y_.p, {{sy, 1.0}, {sz, -c}}) : L.out(sp_y_.p, {{sz, -c}});
-            const int hyn = use_three ? L.out(sp_hy_.p, {{shy, 1.0}, {shz, -c}}) : L.out(sp_hy_.p, {{shz, -c}});
-            const int xn = L.out(sp_x_.p, {{sx, 1.0}, {yn, b}});
-            const int hxn = L.out(sp_hx_.p, {{shx, 1.0}, {hyn, b}});
-            const int zn = L.out(sp_z_.p, {{hxn, 1.0 / k}, {xn, -e_new / k}});
-            L.dot(zn, zn);
-            L.dot(xn, xn);
-            L.dot(yn, yn);
-            for (int s : sxc) L.dot(s, zn);
-            if (trace_) L.kinetic(yn, pre.D->p, pre.shift);  // folded here instead of a pass of its own
-            const auto r = L.run(c_);
+            k = hscal_[1];
+            b = hscal_[2];
+            c = hscal_[3];
+            e_new = hscal_[4];
+            out.ritz_e = hscal_[5];
+            out.sx = hscal_[6];
+            out.sy = hscal_[7];
+            out.sz = hscal_[8];
             zz2 = r[0];
             xx2 = r[1];
             if (std::sqrt(nxx) + std::abs(b) * std::sqrt(r[2]) > 1e6 * std::max(std::sqrt(xx2), 1e-300)) {
@@ -293,6 +235,132 @@ public:
             ovl.assign(r.begin() + 3, r.begin() + 3 + sxc.size());
             if (!fused_ovl) ovl = deflation_overlaps(c_, defl, st.zres);
             ovl = defl.sequential(std::move(ovl));
+        } else {
+            const double* h = c_.finish_dots(m * m);
+            SmallMatrix v(m);
+            for (int i = 0; i < m; ++i)
+                for (int j = i; j < m; ++j) v(i, j) = v(j, i) = 0.5 * (h[i * m + j] + h[j * m + i]);
+            g_ph[2] += ms_since(tp);
+            tp = Clk::now();
+            const SmallEigResult eig = jacobi_symmetric_eig(v);
+            g_ph[3] += ms_since(tp);
+            tp = Clk::now();
+
+            const double vx = eig.eigenvectors(0, 0), vy = use_three ? eig.eigenvectors(1, 0) : 0.0,
+                         vz = eig.eigenvectors(m - 1, 0);
+            const double wx = eig.eigenvectors(0, 1), wy = use_three ? eig.eigenvectors(1, 1) : 0.0,
+                         wz = eig.eigenvectors(m - 1, 1);
+            e_new = eig.eigenvalues[0];
+            const double k_den = vx * gs.A_x + vy * gs.B_x + vz * gs.C_x;
+            if (std::abs(k_den) < 1e-14) {
+                out.outcome = StepOutcome::restart(RestartReason::StallSmallB);
+                return out;
+            }
+            k = 1.0 / k_den;
+            if (use_three) {
+                const double b_den = vy * gs.B_y + vz * gs.C_y;
+                if (std::abs(b_den) < 1e-14) {
+                    out.outcome = StepOutcome::restart(RestartReason::StallSmallB);
+                    return out;
+                }
+                b = k * b_den;
+                c = -vz * gs.C_z / b_den;
+            } else {
+                b = 1.0;
+                c = -k * vz * gs.C_z;
+            }
+            // guard + commit in one pass (sbci1.hpp:259-267): y' = y - c z, Hy' = Hy - c Hz,
+            // x' = x + b y', Hx' = Hx + b Hy', z' = (1/k) Hx' - (E'/k) x' are written into spare
+            // buffers with |z'|^2, |x'|^2, |y'|^2 and the deflation overlaps x_c . z'; the cancellation
+            // guard is then evaluated from those norms and the spares are swapped in only if it passes
+            // (a rejected step leaves the state untouched, as in the reference)
+            // second-lowest Ritz vector coefficients (sbci1.hpp:287-311)
+            out.sx = wx * gs.A_x + wy * gs.B_x + wz * gs.C_x;
+            out.sy = wy * gs.B_y + wz * gs.C_y;
+            out.sz = wz * gs.C_z;
+            out.ritz_e = eig.eigenvalues[1];
+            if (!spares()) {
+                // two-pass form when the five spares do not fit in HBM (or SBG_GUARD_TWO_PASS=1): the
+                // candidate norms first (read-only pass, the same per-element arithmetic and reduction
+                // tree, so the same values), then — only if the guard passes — the commit in place
+                Lin L;
+                const int sx = L.in(st.x.p), sy = L.in(st.y.p), sz = L.in(z_.p), shx = L.in(st.hx.p),
+                          shy = L.in(st.hy.p), shz = L.in(hz_.p);
+                std::vector<int> sxc;
+                const bool fused_ovl = L.fits((int)defl.size());
+                if (fused_ovl)
+                    for (auto& mm : defl.m) sxc.push_back(L.in(mm.x.p));
+                const int yn = use_three ? L.out(nullptr, {{sy, 1.0}, {sz, -c}}) : L.out(nullptr, {{sz, -c}});
+                const int hyn = use_three ? L.out(nullptr, {{shy, 1.0}, {shz, -c}}) : L.out(nullptr, {{shz, -c}});
+                const int xn = L.out(nullptr, {{sx, 1.0}, {yn, b}});
+                const int hxn = L.out(nullptr, {{shx, 1.0}, {hyn, b}});
+                const int zn = L.out(nullptr, {{hxn, 1.0 / k}, {xn, -e_new / k}});
+                L.dot(zn, zn);
+                L.dot(xn, xn);
+                L.dot(yn, yn);
+                for (int s : sxc) L.dot(s, zn);
+                if (trace_) L.kinetic(yn, pre.D->p, pre.shift);
+                const auto r = L.run(c_);
+                zz2 = r[0];
+                xx2 = r[1];
+                if (std::sqrt(nxx) + std::abs(b) * std::sqrt(r[2]) > 1e6 * std::max(std::sqrt(xx2), 1e-300)) {
+                    out.outcome = StepOutcome::restart(RestartReason::StallSmallB);
+                    return out;
+                }
+                if (trace_) {
+                    out.have_kinetic = true;
+                    out.kinetic = r.back();
+                }
+                Lin W;
+                const int wx = W.in(st.x.p), wy = W.in(st.y.p), wz = W.in(z_.p), whx = W.in(st.hx.p), why = W.in(st.hy.p),
+                          whz = W.in(hz_.p);
+                const int y2 = use_three ? W.out(st.y.p, {{wy, 1.0}, {wz, -c}}) : W.out(st.y.p, {{wz, -c}});
+                const int hy2 = use_three ? W.out(st.hy.p, {{why, 1.0}, {whz, -c}}) : W.out(st.hy.p, {{whz, -c}});
+                const int x2 = W.out(st.x.p, {{wx, 1.0}, {y2, b}});
+                const int hx2 = W.out(st.hx.p, {{whx, 1.0}, {hy2, b}});
+                W.out(st.zres.p, {{hx2, 1.0 / k}, {x2, -e_new / k}});
+                W.run(c_);
+                ovl.assign(r.begin() + 3, r.begin() + 3 + sxc.size());
+                if (!fused_ovl) ovl = deflation_overlaps(c_, defl, st.zres);
+                ovl = defl.sequential(std::move(ovl));
+            } else {
+                Lin L;
+                const int sx = L.in(st.x.p), sy = L.in(st.y.p), sz = L.in(z_.p), shx = L.in(st.hx.p),
+                          shy = L.in(st.hy.p), shz = L.in(hz_.p);
+                std::vector<int> sxc;
+                const bool fused_ovl = L.fits((int)defl.size());
+                if (fused_ovl)
+                    for (auto& mm : defl.m) sxc.push_back(L.in(mm.x.p));
+                const int yn = use_three ? L.out(sp_y_.p, {{sy, 1.0}, {sz, -c}}) : L.out(sp_y_.p, {{sz, -c}});
+                const int hyn = use_three ? L.out(sp_hy_.p, {{shy, 1.0}, {shz, -c}}) : L.out(sp_hy_.p, {{shz, -c}});
+                const int xn = L.out(sp_x_.p, {{sx, 1.0}, {yn, b}});
+                const int hxn = L.out(sp_hx_.p, {{shx, 1.0}, {hyn, b}});
+                const int zn = L.out(sp_z_.p, {{hxn, 1.0 / k}, {xn, -e_new / k}});
+                L.dot(zn, zn);
+                L.dot(xn, xn);
+                L.dot(yn, yn);
+                for (int s : sxc) L.dot(s, zn);
+                if (trace_) L.kinetic(yn, pre.D->p, pre.shift);  // folded here instead of a pass of its own
+                const auto r = L.run(c_);
+                zz2 = r[0];
+                xx2 = r[1];
+                if (std::sqrt(nxx) + std::abs(b) * std::sqrt(r[2]) > 1e6 * std::max(std::sqrt(xx2), 1e-300)) {
+                    out.outcome = StepOutcome::restart(RestartReason::StallSmallB);
+                    return out;
+                }
+                if (trace_) {
+                    out.have_kinetic = true;
+                    out.kinetic = r.back();
+                }
+                std::swap(st.y, sp_y_);
+                std::swap(st.hy, sp_hy_);
+                std::swap(st.x, sp_x_);
+                std::swap(st.hx, sp_hx_);
+                std::swap(st.zres, sp_z_);
+                ovl.assign(r.begin() + 3, r.begin() + 3 + sxc.size());
+                if (!fused_ovl) ovl = deflation_overlaps(c_, defl, st.zres);
+                ovl = defl.sequential(std::move(ovl));
+            }
         }
         g_ph[4] += ms_since(tp);
         out.committed = true;
@@ -318,15 +386,11 @@ public:
         st.b_prev = b;
         st.c_prev = c;
         st.k_prev = k;
-        // second-lowest Ritz vector coefficients (sbci1.hpp:287-311); materialized only on convergence
+        // second-lowest Ritz vector (coefficients set above); materialized only on convergence
         out.have_ritz = true;
-        out.sx = wx * gs.A_x + wy * gs.B_x + wz * gs.C_x;
-        out.sy = wy * gs.B_y + wz * gs.C_y;
-        out.sz = wz * gs.C_z;
         out.b = b;
         out.c = c;
         out.three = use_three;
-        out.ritz_e = eig.eigenvalues[1];
 
         if (out.dE < cfg_.eps0 && std::min(out.dz, dz_defl) < cfg_.r0) {
             out.outcome = StepOutcome::converged();
@@ -370,6 +434,15 @@ public:
     DBuf sp_y_, sp_hy_, sp_x_, sp_hx_, sp_z_;  // candidate state of the merged guard + commit pass
     bool two_pass_ = std::getenv("SBG_GUARD_TWO_PASS") && std::atoi(std::getenv("SBG_GUARD_TWO_PASS")) != 0;
     bool speculate_ = !(std::getenv("SBG_SPECULATE") && std::atoi(std::getenv("SBG_SPECULATE")) == 0);
+    // step scalars on the device (SBG_DEVICE_SCALARS=0: on the host, with a round trip per step)
+    bool device_scalars_ = !(std::getenv("SBG_DEVICE_SCALARS") && std::atoi(std::getenv("SBG_DEVICE_SCALARS")) == 0);
+    DBuf dcoef_{(int64_t)kMaxOut * (kMaxIn + kMaxOut)}, dscal_{16};
+    struct PinnedScalars {
+        double* p = nullptr;
+        PinnedScalars() { SBG_CUDA(cudaMallocHost(&p, 16 * sizeof(double))); }
+        ~PinnedScalars() { cudaFreeHost(p); }
+    } pinned_;
+    double* hscal_ = pinned_.p;
 
     // the merged guard + commit pass needs five spare vectors; without room for them the step
     // falls back to the two-pass form for the rest of the solve (large sectors)

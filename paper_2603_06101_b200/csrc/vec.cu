@@ -46,10 +46,17 @@ __device__ __forceinline__ void block_reduce_store(double (&acc)[ND], int ndot, 
 // outputs), ND dot products between any two slots. Two elements per thread per trip (16-byte
 // loads/stores: n is even and every vector base is 16-byte aligned). Slots read by dots are staged
 // in shared memory so the runtime slot indices never force the slot array into local memory.
-template <int NI, int NO, int ND>
+template <int NI, int NO, int ND, bool DC = false>
 __global__ void __launch_bounds__(kThreads, ND > 4 ? 2 : SBG_VEC_MINB) k_lincomb(const LinArgs a, double* partial) {
     constexpr int NDS = ND > 0 ? ND : 1;
     __shared__ double stage[ND > 0 ? kMaxIn + kMaxOut : 1][kThreads];
+    // DC: the coefficient table comes from device memory (written by launch_step_scalars)
+    __shared__ double scoef[DC ? kMaxOut : 1][DC ? kMaxIn + kMaxOut : 1];
+    if constexpr (DC) {
+        for (int t = threadIdx.x; t < kMaxOut * (kMaxIn + kMaxOut); t += blockDim.x)
+            scoef[t / (kMaxIn + kMaxOut)][t % (kMaxIn + kMaxOut)] = a.dcoef[t];
+        __syncthreads();
+    }
     double acc[NDS];
 #pragma unroll
     for (int d = 0; d < NDS; ++d) acc[d] = 0.0;
@@ -73,7 +80,7 @@ __global__ void __launch_bounds__(kThreads, ND > 4 ? 2 : SBG_VEC_MINB) k_lincomb
                 bool first = true;
 #pragma unroll
                 for (int k = 0; k < NI + j; ++k) {
-                    const double c = a.coef[j][k < NI ? k : kMaxIn + (k - NI)];
+                    const double c = DC ? scoef[j][k < NI ? k : kMaxIn + (k - NI)] : a.coef[j][k < NI ? k : kMaxIn + (k - NI)];
                     if (c != 0.0) {
                         const double term = __dmul_rn(c, s[k]);
                         v = first ? term : __dadd_rn(v, term);
@@ -448,6 +455,17 @@ void check_aligned(const void* p) {
 
 template <int NI, int NO, int ND>
 void run_lincomb(const LinArgs& a, const ReduceWs& ws, cudaStream_t st) {
+    if constexpr (NO == kMaxOut && ND > 0) {
+        if (a.dcoef) {
+            const void* fn = reinterpret_cast<const void*>(&k_lincomb<NI, NO, ND, true>);
+            const int g = grid_of(fn, ws);
+            k_lincomb<NI, NO, ND, true><<<g, kThreads, 0, st>>>(a, ws.partial);
+            SBG_LAUNCH_CHECK();
+            launch_reduce_finish(ws, g, a.ndot, st);
+            return;
+        }
+    }
+    if (a.dcoef) throw InvalidArgument("launch_lincomb: device coefficients need 6 outputs and dots");
     const void* fn = reinterpret_cast<const void*>(&k_lincomb<NI, NO, ND>);
     const int g = grid_of(fn, ws);
     k_lincomb<NI, NO, ND><<<g, kThreads, 0, st>>>(a, ws.partial);
