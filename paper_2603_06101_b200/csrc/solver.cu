@@ -180,6 +180,7 @@ public:
             // the commit pass reads its coefficients from device memory: no host round trip between
             // the subspace pass and the commit pass. The scalars come back with the commit's dots.
             StepScalarArgs sca{gs.A_x, gs.B_x, gs.B_y, gs.C_x, gs.C_y, gs.C_z, use_three ? 1 : 0};
+            c_.allreduce_inplace_device(c_.rws.result, m * m);  // world > 1: every rank's partial dots
             launch_step_scalars(c_.rws.result, sca, dcoef_.p, dscal_.p, c_.st);
             c_.launches += 1;
             SBG_CUDA(cudaMemcpyAsync(hscal_, dscal_.p, 9 * sizeof(double), cudaMemcpyDeviceToHost, c_.st));
