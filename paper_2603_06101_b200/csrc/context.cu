@@ -244,6 +244,8 @@ Context::Context(int norb_, int nelec_, int ms2_, double e_core_, const double* 
     rws.grid = 16 * nsm;
     rws.partial = dmalloc<double>((size_t)rws.grid * kMaxRed);
     rws.result = dmalloc<double>(kMaxRed);
+    rws.ticket = dmalloc<unsigned int>(1);
+    SBG_CUDA(cudaMemset(rws.ticket, 0, sizeof(unsigned int)));
     SBG_CUDA(cudaMallocHost(&rws.host, kMaxRed * sizeof(double)));
 
     build_tables(h1, eri);
@@ -253,7 +255,7 @@ Context::~Context() {
     if (st) cudaStreamSynchronize(st);
     for (void* p : {(void*)d_sa_, (void*)d_sb_, (void*)d_la_, (void*)d_lb_, (void*)d_h1_, (void*)d_eri_, (void*)d_Vp_,
                     (void*)d_Va_, (void*)d_codes_, (void*)d_sc_tgt_, (void*)d_sc_ent_,
-                    (void*)d_sc_tt_, (void*)d_sc_te_, (void*)rws.partial, (void*)rws.result})
+                    (void*)d_sc_tt_, (void*)d_sc_te_, (void*)rws.partial, (void*)rws.result, (void*)rws.ticket})
         if (p) cudaFree(p);
     if (rws.host) cudaFreeHost(rws.host);
     for (auto& pr : red_pass_) {
@@ -516,7 +518,7 @@ void Context::gather_full(const double* x_local, cudaStream_t s) {
 double Context::spin_squared(const double* x_local) {
     const double* v[1] = {x_local};
     launch_gram(v, 1, padded_len(), rws, st);
-    launches += 2;
+    launches += 1;
     const double xx = finish_dots(1)[0];
     if (!(xx > 0.0)) throw std::invalid_argument("spin_squared: zero vector");
     const double sz = 0.5 * (na_el - nb_el);

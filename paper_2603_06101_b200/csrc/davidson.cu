@@ -107,7 +107,7 @@ public:
                 a.res[r] = res_[r].p;
             }
             launch_ritz(a, c_.rws, c_.st);
-            c_.launches += 1 + a.last;
+            c_.launches += 1;
             if (a.last) {
                 const double* h = c_.finish_dots(k);
                 norms2.assign(h, h + k);
@@ -257,7 +257,7 @@ MultiStateResult davidson_solve(Context& c, int nroots, const SolverConfig& cfg,
             pa.z = t.p;
             pa.x = dv.res_[k].p;
             launch_precond(pa, c.rws, c.st);
-            c.launches += 2;
+            c.launches += 1;
             const double before = std::sqrt(c.finish_dots(3)[2]);
             if (before == 0.0) continue;
             std::vector<const DBuf*> bs;

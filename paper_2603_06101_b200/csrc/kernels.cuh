@@ -140,6 +140,7 @@ struct ReduceWs {
     double* result;   // [kMaxRed] device
     double* host;     // pinned [kMaxRed]
     int grid;         // capacity of partial in blocks; each pass launches min(grid, resident blocks)
+    unsigned int* ticket;  // device counter electing the block that finishes a pass's sums (0 between passes)
 };
 // returns nothing; results land in ws.result (device). Caller copies to host after collectives.
 void launch_lincomb(const LinArgs& a, const ReduceWs& ws, cudaStream_t st);

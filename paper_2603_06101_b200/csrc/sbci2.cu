@@ -113,7 +113,7 @@ SubspaceSolve pair_subspace_solve(Context& c, const std::vector<const DBuf*>& ve
     std::vector<const double*> vp(m);
     for (int i = 0; i < m; ++i) vp[i] = vecs[i]->p;
     launch_gram(vp.data(), m, c.padded_len(), c.rws, c.st);
-    c.launches += 2;
+    c.launches += 1;
     const double* h = c.finish_dots(m * (m + 1) / 2);
     SmallMatrix raw(m);
     for (int i = 0, d = 0; i < m; ++i)
@@ -148,7 +148,7 @@ SubspaceSolve pair_subspace_solve(Context& c, const std::vector<const DBuf*>& ve
         for (int col = 0; col < trans.rank; ++col) pa.P[i][col] = trans.coeff(i, col);
     }
     launch_pair_subspace(pa, c.rws, c.st);
-    c.launches += 2;
+    c.launches += 1;
     const int r = trans.rank;
     const double* x = c.finish_dots(r * r);
     SmallMatrix g(r);
@@ -448,7 +448,7 @@ Sbci2PairResult solve_pair(PairDriver& dr, Precond& pre, Deflation& defl, Seed l
                 rec.kinetic = step.kinetic;
             } else {
                 launch_kinetic(st.ya.p, pre.D->p, pre.shift, c.padded_len(), c.rws, c.st);
-                c.launches += 2;
+                c.launches += 1;
                 rec.kinetic = c.finish_dots(1)[0];
             }
             rec.matvecs = c.applies().load();

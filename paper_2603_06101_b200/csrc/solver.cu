@@ -68,7 +68,7 @@ int precondition_post(Context& c, const DBuf& zres, const Precond& pre, const De
     if (pa.nxc > 0) {  // overlaps x_c . (D - E0)^-1 zres first, then the deflated z in one pass
         pa.mode = 0;
         launch_precond(pa, c.rws, c.st);
-        c.launches += 2;
+        c.launches += 1;
         const auto o = defl.sequential(std::vector<double>(h_ovl(c, pa.nxc)));
         for (int i = 0; i < pa.nxc; ++i) pa.o[i] = o[i];
     }
@@ -77,7 +77,7 @@ int precondition_post(Context& c, const DBuf& zres, const Precond& pre, const De
     pa.x = x.p;
     pa.y = y ? y->p : nullptr;
     launch_precond(pa, c.rws, c.st);
-    c.launches += 2;
+    c.launches += 1;
     const int nd = y ? 6 : 3;
     c.post_dots(nd);
     return nd;
@@ -169,7 +169,7 @@ public:
         sa.Cz = gs.C_z;
         sa.three = use_three;
         launch_subspace(sa, c_.rws, c_.st);
-        c_.launches += 2;
+        c_.launches += 1;
         const int m = use_three ? 3 : 2;
         double e_new = 0.0, k = 0.0, b = 0.0, c = 0.0;
         double zz2, xx2;
@@ -518,7 +518,7 @@ Sbci1Result solve_state(Driver& dr, Precond& pre, Deflation& defl, Seed seed, in
                 rec.kinetic = step.kinetic;
             } else {  // no commit this step: y is unchanged, one pass of its own
                 launch_kinetic(st.y.p, pre.D->p, pre.shift, c.padded_len(), c.rws, c.st);
-                c.launches += 2;
+                c.launches += 1;
                 rec.kinetic = c.finish_dots(1)[0];
             }
             rec.matvecs = c.applies().load();

@@ -21,10 +21,21 @@ constexpr int kThreads = 256;
 #define SBG_VEC_MINB 3
 #endif
 
+// Where a pass's dot products go: per-block partial sums, the final sums, and the ticket counter
+// that elects the last block to finish them (so a pass is one launch, not pass + finish kernel).
+struct RedOut {
+    double* partial;  // [grid][kMaxRed]
+    double* result;   // [kMaxRed]
+    unsigned int* ticket;
+};
+
+inline RedOut red_out(const ReduceWs& ws) { return RedOut{ws.partial, ws.result, ws.ticket}; }
+
 template <int ND>
-__device__ __forceinline__ void block_reduce_store(double (&acc)[ND], int ndot, double* partial) {
+__device__ __forceinline__ void block_reduce_store(double (&acc)[ND], int ndot, const RedOut ro) {
     static_assert(ND <= kMaxRed, "reduction width");
     __shared__ double red[kThreads / 32][ND];
+    __shared__ bool last;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
     for (int d = 0; d < ND; ++d) {
@@ -38,8 +49,27 @@ __device__ __forceinline__ void block_reduce_store(double (&acc)[ND], int ndot, 
     if (threadIdx.x < ndot) {
         double s = 0.0;
         for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i][threadIdx.x];
-        partial[blockIdx.x * kMaxRed + threadIdx.x] = s;
+        ro.partial[blockIdx.x * kMaxRed + threadIdx.x] = s;
     }
+    if (ndot <= 0) return;
+    // the last block to arrive sums every block's partials — in the fixed order of
+    // k_reduce_finish (lane-strided, then a shuffle tree), so the results do not depend on which
+    // block is last
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(ro.ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const int nblk = gridDim.x, nw = blockDim.x >> 5;
+    for (int d = w; d < ndot; d += nw) {
+        double s = 0.0;
+        for (int b = lane; b < nblk; b += 32) s += __ldcg(ro.partial + b * kMaxRed + d);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) ro.result[d] = s;
+    }
+    if (threadIdx.x == 0) *ro.ticket = 0u;  // ready for the next pass on this stream
 }
 
 // One fused pass: up to NI inputs, NO outputs (each a linear combination of inputs and earlier
@@ -47,7 +77,7 @@ __device__ __forceinline__ void block_reduce_store(double (&acc)[ND], int ndot, 
 // loads/stores: n is even and every vector base is 16-byte aligned). Slots read by dots are staged
 // in shared memory so the runtime slot indices never force the slot array into local memory.
 template <int NI, int NO, int ND, bool DC = false>
-__global__ void __launch_bounds__(kThreads, ND > 4 ? 2 : SBG_VEC_MINB) k_lincomb(const LinArgs a, double* partial) {
+__global__ void __launch_bounds__(kThreads, ND > 4 ? 2 : SBG_VEC_MINB) k_lincomb(const LinArgs a, const RedOut partial) {
     constexpr int NDS = ND > 0 ? ND : 1;
     __shared__ double stage[ND > 0 ? kMaxIn + kMaxOut : 1][kThreads];
     // DC: the coefficient table comes from device memory (written by launch_step_scalars)
@@ -134,7 +164,7 @@ constexpr int kPrecMaxC = 8;  // PrecArgs::xc capacity
 // MAXC: compile-time bound on the deflated states (0 for the ground state: no x_c registers, more
 // resident blocks per SM for this HBM stream)
 template <int MAXC>
-__global__ void __launch_bounds__(kThreads) k_precond(const PrecArgs a, double* partial) {
+__global__ void __launch_bounds__(kThreads) k_precond(const PrecArgs a, const RedOut partial) {
     double acc[8];
 #pragma unroll
     for (int d = 0; d < 8; ++d) acc[d] = 0.0;
@@ -185,7 +215,7 @@ __global__ void __launch_bounds__(kThreads) k_precond(const PrecArgs a, double* 
 }
 
 // basis b = {Ax x, Bx x + By y, (Cx x + Cz z) + Cy y}, images likewise; dots d_ij = b_i . B_j
-__global__ void __launch_bounds__(kThreads) k_subspace(const SubArgs a, double* partial) {
+__global__ void __launch_bounds__(kThreads) k_subspace(const SubArgs a, const RedOut partial) {
     double acc[9];
 #pragma unroll
     for (int d = 0; d < 9; ++d) acc[d] = 0.0;
@@ -238,7 +268,7 @@ __global__ void k_reduce_finish(const double* partial, int nblk, int ndot, doubl
 }
 
 // all dots v_i . v_j (i <= j) of up to 6 vectors in one pass
-__global__ void __launch_bounds__(kThreads) k_gram(const PairSubArgs a, double* partial) {
+__global__ void __launch_bounds__(kThreads) k_gram(const PairSubArgs a, const RedOut partial) {
     double acc[21];
 #pragma unroll
     for (int d = 0; d < 21; ++d) acc[d] = 0.0;
@@ -272,7 +302,7 @@ __global__ void __launch_bounds__(kThreads) k_gram(const PairSubArgs a, double* 
 // sbci2.hpp:144-176 per element: w_i = v_i * inv_n_i (scaled copy), basis b_c = sum_i P[i][c] w_i
 // accumulated in input order from zero (apply_transform, ortho.hpp:220-230), images likewise;
 // cross dots b_c . B_d for c, d < r
-__global__ void __launch_bounds__(kThreads) k_pair_subspace(const PairSubArgs a, double* partial) {
+__global__ void __launch_bounds__(kThreads) k_pair_subspace(const PairSubArgs a, const RedOut partial) {
     double acc[36];
 #pragma unroll
     for (int d = 0; d < 36; ++d) acc[d] = 0.0;
@@ -324,7 +354,7 @@ __global__ void __launch_bounds__(kThreads) k_pair_subspace(const PairSubArgs a,
     block_reduce_store<36>(out, a.r * a.r, partial);
 }
 
-__global__ void __launch_bounds__(kThreads) k_ritz(const RitzArgs a, double* partial) {
+__global__ void __launch_bounds__(kThreads) k_ritz(const RitzArgs a, const RedOut partial) {
     double acc[kMaxRoots];
 #pragma unroll
     for (int r = 0; r < kMaxRoots; ++r) acc[r] = 0.0;
@@ -412,7 +442,7 @@ __global__ void k_argmin_after(const double* D, int64_t nrows, int64_t ncols, in
 
 // sum_i y_i^2 (D_i - shift)  (kinetic_scalar, sbci1.hpp:135-139)
 __global__ void __launch_bounds__(kThreads) k_kinetic(const double* y, const double* D, double shift, int64_t n,
-                                                      double* partial) {
+                                                      const RedOut partial) {
     double acc[1] = {0.0};
     const int64_t n2 = n >> 1, stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += stride) {
@@ -459,18 +489,16 @@ void run_lincomb(const LinArgs& a, const ReduceWs& ws, cudaStream_t st) {
         if (a.dcoef) {
             const void* fn = reinterpret_cast<const void*>(&k_lincomb<NI, NO, ND, true>);
             const int g = grid_of(fn, ws);
-            k_lincomb<NI, NO, ND, true><<<g, kThreads, 0, st>>>(a, ws.partial);
+            k_lincomb<NI, NO, ND, true><<<g, kThreads, 0, st>>>(a, red_out(ws));
             SBG_LAUNCH_CHECK();
-            launch_reduce_finish(ws, g, a.ndot, st);
             return;
         }
     }
     if (a.dcoef) throw InvalidArgument("launch_lincomb: device coefficients need 6 outputs and dots");
     const void* fn = reinterpret_cast<const void*>(&k_lincomb<NI, NO, ND>);
     const int g = grid_of(fn, ws);
-    k_lincomb<NI, NO, ND><<<g, kThreads, 0, st>>>(a, ws.partial);
+    k_lincomb<NI, NO, ND><<<g, kThreads, 0, st>>>(a, red_out(ws));
     SBG_LAUNCH_CHECK();
-    if (a.ndot > 0) launch_reduce_finish(ws, g, a.ndot, st);
 }
 
 template <int NI, int NO>
@@ -509,19 +537,18 @@ void launch_precond(const PrecArgs& a, const ReduceWs& ws, cudaStream_t st) {
     const void* fn = a.nxc == 0 ? reinterpret_cast<const void*>(&k_precond<0>)
                                 : reinterpret_cast<const void*>(&k_precond<kPrecMaxC>);
     const int g = grid_of(fn, ws);
-    if (a.nxc == 0) k_precond<0><<<g, kThreads, 0, st>>>(a, ws.partial);
-    else k_precond<kPrecMaxC><<<g, kThreads, 0, st>>>(a, ws.partial);
+    if (a.nxc == 0) k_precond<0><<<g, kThreads, 0, st>>>(a, red_out(ws));
+    else k_precond<kPrecMaxC><<<g, kThreads, 0, st>>>(a, red_out(ws));
     SBG_LAUNCH_CHECK();
     const int nd = a.mode == 0 ? a.nxc : (a.y ? 6 : 3);
-    if (nd > 0) launch_reduce_finish(ws, g, nd, st);
+    (void)nd;
 }
 
 void launch_subspace(const SubArgs& a, const ReduceWs& ws, cudaStream_t st) {
     if (a.n & 1) throw InvalidArgument("launch_subspace: odd length");
     const int g = grid_of(reinterpret_cast<const void*>(&k_subspace), ws);
-    k_subspace<<<g, kThreads, 0, st>>>(a, ws.partial);
+    k_subspace<<<g, kThreads, 0, st>>>(a, red_out(ws));
     SBG_LAUNCH_CHECK();
-    launch_reduce_finish(ws, g, a.three ? 9 : 4, st);
 }
 
 void launch_reduce_finish(const ReduceWs& ws, int nblk, int ndot, cudaStream_t st) {
@@ -540,9 +567,8 @@ void launch_gram(const double* const* v, int m, int64_t n, const ReduceWs& ws, c
         a.v[k] = v[k];
     }
     const int g = grid_of(reinterpret_cast<const void*>(&k_gram), ws);
-    k_gram<<<g, kThreads, 0, st>>>(a, ws.partial);
+    k_gram<<<g, kThreads, 0, st>>>(a, red_out(ws));
     SBG_LAUNCH_CHECK();
-    launch_reduce_finish(ws, g, m * (m + 1) / 2, st);
 }
 
 void launch_ritz(const RitzArgs& a, const ReduceWs& ws, cudaStream_t st) {
@@ -553,9 +579,8 @@ void launch_ritz(const RitzArgs& a, const ReduceWs& ws, cudaStream_t st) {
         check_aligned(a.h[i]);
     }
     const int g = grid_of(reinterpret_cast<const void*>(&k_ritz), ws);
-    k_ritz<<<g, kThreads, 0, st>>>(a, ws.partial);
+    k_ritz<<<g, kThreads, 0, st>>>(a, red_out(ws));
     SBG_LAUNCH_CHECK();
-    if (a.last) launch_reduce_finish(ws, g, a.k, st);
 }
 
 void launch_pair_subspace(const PairSubArgs& a, const ReduceWs& ws, cudaStream_t st) {
@@ -565,9 +590,8 @@ void launch_pair_subspace(const PairSubArgs& a, const ReduceWs& ws, cudaStream_t
         check_aligned(a.h[k]);
     }
     const int g = grid_of(reinterpret_cast<const void*>(&k_pair_subspace), ws);
-    k_pair_subspace<<<g, kThreads, 0, st>>>(a, ws.partial);
+    k_pair_subspace<<<g, kThreads, 0, st>>>(a, red_out(ws));
     SBG_LAUNCH_CHECK();
-    launch_reduce_finish(ws, g, a.r * a.r, st);
 }
 
 void launch_argmin_after(const double* D, int64_t nrows, int64_t ncols, int64_t ld, int64_t row_lo, double prev_v,
@@ -582,9 +606,8 @@ void launch_argmin_after(const double* D, int64_t nrows, int64_t ncols, int64_t 
 void launch_kinetic(const double* y, const double* D, double shift, int64_t n, const ReduceWs& ws, cudaStream_t st) {
     if (n & 1) throw InvalidArgument("launch_kinetic: odd length");
     const int g = grid_of(reinterpret_cast<const void*>(&k_kinetic), ws);
-    k_kinetic<<<g, kThreads, 0, st>>>(y, D, shift, n, ws.partial);
+    k_kinetic<<<g, kThreads, 0, st>>>(y, D, shift, n, red_out(ws));
     SBG_LAUNCH_CHECK();
-    launch_reduce_finish(ws, g, 1, st);
 }
 
 void launch_fill(double* p, int64_t n, double v, cudaStream_t st) {
