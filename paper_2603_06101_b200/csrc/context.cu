@@ -4,6 +4,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -246,6 +247,13 @@ Context::Context(int norb_, int nelec_, int ms2_, double e_core_, const double* 
     rws.result = dmalloc<double>(kMaxRed);
     rws.ticket = dmalloc<unsigned int>(1);
     SBG_CUDA(cudaMemset(rws.ticket, 0, sizeof(unsigned int)));
+    if (world == 1 && !(std::getenv("SBG_ZERO_COPY_DOTS") && std::atoi(std::getenv("SBG_ZERO_COPY_DOTS")) == 0)) {
+        zc_ = std::make_unique<ReduceWs::ZeroCopy>();
+        SBG_CUDA(cudaHostAlloc(&zc_->mirror, kMaxRed * sizeof(double), cudaHostAllocMapped));
+        SBG_CUDA(cudaHostAlloc(&zc_->flag, sizeof(unsigned long long), cudaHostAllocMapped));
+        *zc_->flag = 0;
+        rws.zc = zc_.get();
+    }
     SBG_CUDA(cudaMallocHost(&rws.host, kMaxRed * sizeof(double)));
 
     build_tables(h1, eri);
@@ -258,6 +266,10 @@ Context::~Context() {
                     (void*)d_sc_tt_, (void*)d_sc_te_, (void*)rws.partial, (void*)rws.result, (void*)rws.ticket})
         if (p) cudaFree(p);
     if (rws.host) cudaFreeHost(rws.host);
+    if (zc_) {
+        cudaFreeHost(zc_->mirror);
+        cudaFreeHost(zc_->flag);
+    }
     for (auto& pr : red_pass_) {
         cudaFree(pr.first);
         cudaFree(pr.second);
@@ -536,6 +548,7 @@ double Context::spin_squared(const double* x_local) {
             launches += 2;
         } else {
             SBG_CUDA(cudaMemsetAsync(rws.result, 0, 8, st));
+            if (zc_) zc_->fresh = false;
         }
         raised_sq = finish_dots(1)[0];
     }
@@ -546,18 +559,57 @@ void Context::allreduce_inplace_device(double* d, int count) {
     if (world > 1 && count > 0) comm_->all_reduce_sum(d, (size_t)count, st);
 }
 
+// Zero-copy wait: the finishing block of the latest pass with dots writes them into mapped host
+// memory and then sets the flag to that pass's sequence number. Polls with a stream query every few
+// thousand spins, so a stream that drained without setting the flag (cannot happen for the passes
+// that advance the sequence) falls back to the copy path instead of hanging.
+bool Context::poll_zero_copy(unsigned long long seq) {
+    volatile unsigned long long* flag = zc_->flag;
+    for (unsigned spins = 1;; ++spins) {
+        if (*flag >= seq) return true;
+        if ((spins & 4095u) == 0) {
+            const cudaError_t q = cudaStreamQuery(st);
+            if (q == cudaSuccess) return *flag >= seq;
+            if (q != cudaErrorNotReady) SBG_CUDA(q);
+        }
+    }
+}
+
 void Context::post_dots(int ndot) {
+    if (zc_ && zc_->fresh) {  // the flag is the completion signal: nothing to enqueue
+        zc_->fresh = false;
+        post_seq_ = zc_->seq;
+        post_n_ = ndot;
+        return;
+    }
+    post_seq_ = 0;
     allreduce_inplace_device(rws.result, ndot);
     SBG_CUDA(cudaMemcpyAsync(rws.host, rws.result, ndot * 8, cudaMemcpyDeviceToHost, st));
     SBG_CUDA(cudaEventRecord(ev_dots_, st));
 }
 
 const double* Context::wait_dots() {
+    if (post_seq_ && poll_zero_copy(post_seq_)) {
+        std::memcpy(rws.host, (const void*)zc_->mirror, post_n_ * sizeof(double));
+        return rws.host;
+    }
+    if (post_seq_) {  // fallback: the copy path
+        SBG_CUDA(cudaMemcpyAsync(rws.host, rws.result, post_n_ * 8, cudaMemcpyDeviceToHost, st));
+        SBG_CUDA(cudaStreamSynchronize(st));
+        return rws.host;
+    }
     SBG_CUDA(cudaEventSynchronize(ev_dots_));
     return rws.host;
 }
 
 const double* Context::finish_dots(int ndot) {
+    if (zc_ && zc_->fresh) {
+        zc_->fresh = false;
+        if (poll_zero_copy(zc_->seq)) {
+            std::memcpy(rws.host, (const void*)zc_->mirror, ndot * sizeof(double));
+            return rws.host;
+        }
+    }
     allreduce_inplace_device(rws.result, ndot);
     SBG_CUDA(cudaMemcpyAsync(rws.host, rws.result, ndot * 8, cudaMemcpyDeviceToHost, st));
     SBG_CUDA(cudaStreamSynchronize(st));

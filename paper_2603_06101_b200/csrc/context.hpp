@@ -186,6 +186,10 @@ private:
     // alpha-alpha buffers): every build waits for the previous one's completion event
     cudaEvent_t ev_order_ = nullptr;
     cudaEvent_t ev_dots_ = nullptr;  // post_dots -> wait_dots
+    std::unique_ptr<ReduceWs::ZeroCopy> zc_;  // single GPU: dots read from mapped host memory
+    unsigned long long post_seq_ = 0;
+    int post_n_ = 0;
+    bool poll_zero_copy(unsigned long long seq);
     bool order_recorded_ = false;
     void order_begin(cudaStream_t s);
     void order_end(cudaStream_t s);

@@ -141,6 +141,16 @@ struct ReduceWs {
     double* host;     // pinned [kMaxRed]
     int grid;         // capacity of partial in blocks; each pass launches min(grid, resident blocks)
     unsigned int* ticket;  // device counter electing the block that finishes a pass's sums (0 between passes)
+    // single GPU: the finishing block also writes the sums into mapped host memory and then bumps a
+    // sequence flag there, so the host reads a pass's dots by polling host memory instead of a copy
+    // plus a stream synchronisation (Context::finish_dots; small sectors are latency bound)
+    struct ZeroCopy {
+        double* mirror;                 // mapped pinned [kMaxRed] (UVA: valid on host and device)
+        unsigned long long* flag;       // mapped pinned: seq of the last finished pass
+        unsigned long long seq = 0;     // host: seq handed to the latest pass with dots
+        bool fresh = false;             // host: the latest writer of the dot buffer was such a pass
+    };
+    ZeroCopy* zc = nullptr;
 };
 // returns nothing; results land in ws.result (device). Caller copies to host after collectives.
 void launch_lincomb(const LinArgs& a, const ReduceWs& ws, cudaStream_t st);

@@ -147,6 +147,7 @@ public:
             SBG_CUDA(cudaMemcpyAsync(r, v.p + (row - c_.row_lo) * c_.ld + col, 8, cudaMemcpyDeviceToDevice, c_.st));
         else
             SBG_CUDA(cudaMemsetAsync(r, 0, 8, c_.st));
+        if (c_.rws.zc) c_.rws.zc->fresh = false;  // written by a copy, not by a pass
         return c_.finish_dots(1)[0];
     }
     void set_unit(DBuf& v, int64_t gidx) {
@@ -190,6 +191,7 @@ public:
                 all[2 * c_.rank + 1] = (double)bi;
                 // sum-allreduce of a one-hot layout == allgather
                 SBG_CUDA(cudaMemcpyAsync(c_.rws.result, all.data(), all.size() * 8, cudaMemcpyHostToDevice, c_.st));
+                if (c_.rws.zc) c_.rws.zc->fresh = false;
                 const double* h = c_.finish_dots((int)all.size());
                 for (int r = 0; r < c_.world; ++r) {
                     const double v = h[2 * r];

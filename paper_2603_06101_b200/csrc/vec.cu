@@ -27,9 +27,22 @@ struct RedOut {
     double* partial;  // [grid][kMaxRed]
     double* result;   // [kMaxRed]
     unsigned int* ticket;
+    double* mirror;                // mapped host copy of result (nullptr: none)
+    unsigned long long* flag;      // mapped host flag, set to seq once mirror is written
+    unsigned long long seq;
 };
 
-inline RedOut red_out(const ReduceWs& ws) { return RedOut{ws.partial, ws.result, ws.ticket}; }
+// ndot: the dots this launch will finish (0: none — the zero-copy sequence is not advanced)
+inline RedOut red_out(const ReduceWs& ws, int ndot) {
+    RedOut r{ws.partial, ws.result, ws.ticket, nullptr, nullptr, 0};
+    if (ws.zc && ndot > 0) {
+        r.mirror = ws.zc->mirror;
+        r.flag = ws.zc->flag;
+        r.seq = ++ws.zc->seq;
+        ws.zc->fresh = true;
+    }
+    return r;
+}
 
 template <int ND>
 __device__ __forceinline__ void block_reduce_store(double (&acc)[ND], int ndot, const RedOut ro) {
@@ -67,7 +80,17 @@ __device__ __forceinline__ void block_reduce_store(double (&acc)[ND], int ndot, 
         for (int b = lane; b < nblk; b += 32) s += __ldcg(ro.partial + b * kMaxRed + d);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) ro.result[d] = s;
+        if (lane == 0) {
+            ro.result[d] = s;
+            if (ro.mirror) ro.mirror[d] = s;
+        }
+    }
+    if (ro.mirror) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence_system();  // the mirrored sums reach host memory before the flag does
+            *reinterpret_cast<volatile unsigned long long*>(ro.flag) = ro.seq;
+        }
     }
     if (threadIdx.x == 0) *ro.ticket = 0u;  // ready for the next pass on this stream
 }
@@ -489,7 +512,7 @@ void run_lincomb(const LinArgs& a, const ReduceWs& ws, cudaStream_t st) {
         if (a.dcoef) {
             const void* fn = reinterpret_cast<const void*>(&k_lincomb<NI, NO, ND, true>);
             const int g = grid_of(fn, ws);
-            k_lincomb<NI, NO, ND, true><<<g, kThreads, 0, st>>>(a, red_out(ws));
+            k_lincomb<NI, NO, ND, true><<<g, kThreads, 0, st>>>(a, red_out(ws, a.ndot));
             SBG_LAUNCH_CHECK();
             return;
         }
@@ -497,7 +520,7 @@ void run_lincomb(const LinArgs& a, const ReduceWs& ws, cudaStream_t st) {
     if (a.dcoef) throw InvalidArgument("launch_lincomb: device coefficients need 6 outputs and dots");
     const void* fn = reinterpret_cast<const void*>(&k_lincomb<NI, NO, ND>);
     const int g = grid_of(fn, ws);
-    k_lincomb<NI, NO, ND><<<g, kThreads, 0, st>>>(a, red_out(ws));
+    k_lincomb<NI, NO, ND><<<g, kThreads, 0, st>>>(a, red_out(ws, a.ndot));
     SBG_LAUNCH_CHECK();
 }
 
@@ -537,21 +560,21 @@ void launch_precond(const PrecArgs& a, const ReduceWs& ws, cudaStream_t st) {
     const void* fn = a.nxc == 0 ? reinterpret_cast<const void*>(&k_precond<0>)
                                 : reinterpret_cast<const void*>(&k_precond<kPrecMaxC>);
     const int g = grid_of(fn, ws);
-    if (a.nxc == 0) k_precond<0><<<g, kThreads, 0, st>>>(a, red_out(ws));
-    else k_precond<kPrecMaxC><<<g, kThreads, 0, st>>>(a, red_out(ws));
-    SBG_LAUNCH_CHECK();
     const int nd = a.mode == 0 ? a.nxc : (a.y ? 6 : 3);
-    (void)nd;
+    if (a.nxc == 0) k_precond<0><<<g, kThreads, 0, st>>>(a, red_out(ws, nd));
+    else k_precond<kPrecMaxC><<<g, kThreads, 0, st>>>(a, red_out(ws, nd));
+    SBG_LAUNCH_CHECK();
 }
 
 void launch_subspace(const SubArgs& a, const ReduceWs& ws, cudaStream_t st) {
     if (a.n & 1) throw InvalidArgument("launch_subspace: odd length");
     const int g = grid_of(reinterpret_cast<const void*>(&k_subspace), ws);
-    k_subspace<<<g, kThreads, 0, st>>>(a, red_out(ws));
+    k_subspace<<<g, kThreads, 0, st>>>(a, red_out(ws, a.three ? 9 : 4));
     SBG_LAUNCH_CHECK();
 }
 
 void launch_reduce_finish(const ReduceWs& ws, int nblk, int ndot, cudaStream_t st) {
+    if (ws.zc) ws.zc->fresh = false;  // result written without the host mirror
     if (ndot < 1 || ndot > kMaxRed) throw InvalidArgument("reduce: bad dot count");
     k_reduce_finish<<<1, 32 * std::min(ndot, 32), 0, st>>>(ws.partial, nblk, ndot, ws.result);
     SBG_LAUNCH_CHECK();
@@ -567,7 +590,7 @@ void launch_gram(const double* const* v, int m, int64_t n, const ReduceWs& ws, c
         a.v[k] = v[k];
     }
     const int g = grid_of(reinterpret_cast<const void*>(&k_gram), ws);
-    k_gram<<<g, kThreads, 0, st>>>(a, red_out(ws));
+    k_gram<<<g, kThreads, 0, st>>>(a, red_out(ws, m * (m + 1) / 2));
     SBG_LAUNCH_CHECK();
 }
 
@@ -579,7 +602,7 @@ void launch_ritz(const RitzArgs& a, const ReduceWs& ws, cudaStream_t st) {
         check_aligned(a.h[i]);
     }
     const int g = grid_of(reinterpret_cast<const void*>(&k_ritz), ws);
-    k_ritz<<<g, kThreads, 0, st>>>(a, red_out(ws));
+    k_ritz<<<g, kThreads, 0, st>>>(a, red_out(ws, a.last ? a.k : 0));
     SBG_LAUNCH_CHECK();
 }
 
@@ -590,7 +613,7 @@ void launch_pair_subspace(const PairSubArgs& a, const ReduceWs& ws, cudaStream_t
         check_aligned(a.h[k]);
     }
     const int g = grid_of(reinterpret_cast<const void*>(&k_pair_subspace), ws);
-    k_pair_subspace<<<g, kThreads, 0, st>>>(a, red_out(ws));
+    k_pair_subspace<<<g, kThreads, 0, st>>>(a, red_out(ws, a.r * a.r));
     SBG_LAUNCH_CHECK();
 }
 
@@ -606,7 +629,7 @@ void launch_argmin_after(const double* D, int64_t nrows, int64_t ncols, int64_t 
 void launch_kinetic(const double* y, const double* D, double shift, int64_t n, const ReduceWs& ws, cudaStream_t st) {
     if (n & 1) throw InvalidArgument("launch_kinetic: odd length");
     const int g = grid_of(reinterpret_cast<const void*>(&k_kinetic), ws);
-    k_kinetic<<<g, kThreads, 0, st>>>(y, D, shift, n, red_out(ws));
+    k_kinetic<<<g, kThreads, 0, st>>>(y, D, shift, n, red_out(ws, 1));
     SBG_LAUNCH_CHECK();
 }
 
