@@ -137,6 +137,16 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
         "r"(parity)
         : "memory");
 }
+// plain arrival (release at CTA scope): the arriving thread's earlier shared-memory accesses are
+// ordered before the phase completion another thread observes with mbar_wait_parity
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+// arrival that fires once every cp.async this thread has issued so far has landed (the barrier's
+// count already includes it: .noinc) — the loader never blocks on its own copies
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 // generic-proxy accesses to shared memory before this point are ordered before later async-proxy
 // (bulk copy) writes by the same thread — the WAR hand-off when a consumed buffer is refilled
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }

@@ -34,6 +34,10 @@ struct AbPlan {
     int tall; // ws kernel: balanced warp assignment for 5-7 m16 blocks (warps 4-7 span the rest)
     int npass = 1;    // pair-row blocks of 128 rows (npair > 136); 1 = one pass over all rows
     int tma = 0;      // ws red kernel: D rows and reduction lists by bulk copies (UBLKCP) on mbarriers
+    int dc = 0;       // ws red kernel: decoupled (mbarrier) hand-offs with this many D stages (0 = off)
+    int xs = 0;       // ws red kernel: uniform MMA instruction stream (1 = no extra rows, 2 = split extra rows)
+    int gstride = 0;  // staged G tile: row stride in doubles (nt + 8, or nt + 2 with xs) ...
+    int grows = 0;    // ... and rows (npad, + 8 with xs == 2: both partial sums of the extra rows)
     int code_ld = 0;  // rows per beta string of the scatter-code table (npad, or npass * 128)
     int64_t NA, NB, ld;
     size_t smem;

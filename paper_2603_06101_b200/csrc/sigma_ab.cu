@@ -65,6 +65,11 @@ struct AbParams {
     int nvec;
     const double* xv[kMaxSigmaVec];
     double* yv[kMaxSigmaVec];
+    // decoupled hand-offs (tma path): number of D stages (2 or 3), 0 = named-barrier hand-offs.
+    // D(it) is announced on an mbarrier by the loaders' own cp.async completions and the G buffer is
+    // handed back on an mbarrier the MMA warps only look at AFTER their DMMAs, so neither a slow
+    // scatter nor a late gather stops the tensor pipe unless it is a whole tile late
+    int dc;
 };
 
 // Software pipeline per alpha row, one __syncthreads per tile: iteration `it` prefetches D(it+1)
@@ -308,9 +313,21 @@ constexpr int WSU = SBG_WSU;
 constexpr int RED_UNROLL = SBG_RED_UNROLL;  // scatter entries per thread in flight
 constexpr int BAR_DREADY = 1, BAR_FULL = 3, BAR_EMPTY = 5, BAR_SINT = 7, BAR_MINT = 8, BAR_KLIST = 9;
 
-template <int KS, int NT, bool K0E, bool TALL>
+// XS (NT = 32, reduction mode, not TALL): the uniform MMA instruction stream. Every DMMA warp runs
+// the same code with no per-k-step branch or select chain:
+//  * n8 blocks are interleaved over the tile's columns (local block L of the pair P = L >> 1 holds
+//    columns 16 P' + 2 n + (L & 1), n = 0..7), so a lane's B fragments for two blocks are adjacent:
+//    two conflict-free LDS.128 per k-step instead of four LDS.64, and a lane's accumulators cover
+//    four adjacent columns per pair (16-byte stores; G row stride NT + 2 keeps them conflict free);
+//  * XS == 2 (8 m16 blocks + 8 extra rows, the 16-orbital sectors): the extra rows' m8n8k4 DMMAs
+//    are split over ALL eight warps — warp w takes n8 block w & 3 on half of the k range (warps
+//    4-7 walk the k-steps rotated by half, so "the first KH iterations" means the upper half for
+//    them) and stages its partial sums in its own G rows (re + g, re + 8 + g); the reduction list
+//    carries both partials. 136 DMMA.8x8x4 per tile on every warp instead of 144 / 128.
+template <int KS, int NT, bool K0E, bool TALL, int XS>
 __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p) {
-    constexpr int NBT = Tile<NT>::NBT, DSTRIDE = Tile<NT>::DSTRIDE, GSTRIDE = Tile<NT>::GSTRIDE;
+    static_assert(XS == 0 || (NT == 32 && !TALL), "uniform stream: 32-column tiles, no TALL");
+    constexpr int NBT = Tile<NT>::NBT, DSTRIDE = Tile<NT>::DSTRIDE, GSTRIDE = XS ? NT + 2 : Tile<NT>::GSTRIDE;
     extern __shared__ __align__(16) double smem[];
     // D rows: k = 0 is the row Ia itself (all occupation entries, sigma.hpp:33-35), k = 1..K-1 its
     // single excitations. K0E (when (K-1) % 4 == 0): the DMMAs cover k = 1 .. 4*KS and k = 0 is a
@@ -320,11 +337,15 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
     const int KP = K0 + KS * 4;
     const int ntiles = (int)(p.ld / NT);
     const int ntot = ntiles * p.nvec;  // tiles per alpha row over all vectors
-    // mbarriers of the bulk-copy pipeline: [0..1] D stage b landed, [2..3] list stage b landed
+    // mbarriers: [0..2] D stage s landed, [3..4] list stage b landed, [5..6] G buffer b scattered
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
-    double* srow = smem + 4;                 // [ld], absent in red mode
+    uint64_t* const mbD = mbar;
+    uint64_t* const mbL = mbar + 3;
+    uint64_t* const mbE = mbar + 5;
+    const int nds = p.dc ? p.dc : STAGES;    // D stages
+    double* srow = smem + 8;                 // [ld], absent in red mode
     double* Ds = srow + (p.red ? 0 : p.ld);
-    double* sAe = Ds + STAGES * KP * DSTRIDE;
+    double* sAe = Ds + nds * KP * DSTRIDE;
     double* Gs = sAe + KP * 8;
     uint32_t* Lt = reinterpret_cast<uint32_t*>(Gs + STAGES * p.grows * GSTRIDE);
     uint16_t* Le = reinterpret_cast<uint16_t*>(Lt + STAGES * p.maxT);   // red mode: u32 entries
@@ -347,6 +368,42 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
         const int mbh = TALL ? p.mb16 - 4 : 0;
         const bool main_ok = TALL ? w < 4 : w < p.mb16;
         const bool do_extra = p.extra && w < NBT;
+        uint32_t phDm = 0, phEm = 0;  // decoupled hand-offs: phase parity per D stage / G buffer
+        // tile it of a row: wait for D (stage returned), and the hand-back of G buffer b
+        auto wait_d = [&](int it, int& sd) -> const double* {
+            const int b = it & 1;
+            if (p.dbg & 16) return Ds + b * KP * DSTRIDE;  // timing experiment: no hand-offs at all
+            if (p.dc) {
+                mbar_wait_parity(mbD + sd, (phDm >> sd) & 1u);
+                phDm ^= 1u << sd;
+                const double* D = Ds + sd * KP * DSTRIDE;
+                sd = (sd + 1 == p.dc) ? 0 : sd + 1;
+                return D;
+            }
+            bar_sync(BAR_DREADY + b, kWsThreads);
+            if (it >= 2) bar_sync(BAR_EMPTY + b, kWsThreads);
+            return Ds + b * KP * DSTRIDE;
+        };
+        auto wait_g = [&](int it) {  // decoupled: just before the accumulators are staged
+            const int b = it & 1;
+            if (p.dbg & 16) return;
+            if (p.dc && it >= 2) {
+                mbar_wait_parity(mbE + b, (phEm >> b) & 1u);
+                phEm ^= 1u << b;
+            }
+        };
+        auto drain_g = [&](int ntot) {  // row end: the last two tiles have been scattered
+            if (p.dbg & 16) return;
+            for (int it = ntot - 2 < 0 ? 0 : ntot - 2; it < ntot; ++it) {
+                const int b = it & 1;
+                if (p.dc) {
+                    mbar_wait_parity(mbE + b, (phEm >> b) & 1u);
+                    phEm ^= 1u << b;
+                } else {
+                    bar_sync(BAR_EMPTY + b, kWsThreads);
+                }
+            }
+        };
         for (int64_t ia = p.row_lo + blockIdx.x; ia < p.row_hi; ia += gridDim.x) {
             bar_sync(0, kWsThreads);           // row start
             bar_sync(BAR_KLIST, kWsThreads);   // K-list of row ia ready (built by the loader warps)
@@ -383,12 +440,11 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                         ak1[mb] = (K0E && ok) ? aval(rh + 8, 0) : 0.0;
                     }
                     bar_sync(BAR_MINT, kWsHalf);
+                    int sd = 0;
                     for (int it = 0; it < ntot; ++it) {
                         const int b = it & 1;
-                        bar_sync(BAR_DREADY + b, kWsThreads);
-                        if (it >= 2) bar_sync(BAR_EMPTY + b, kWsThreads);
+                        const double* D = wait_d(it, sd);
                         if (!(p.dbg & 2) && nbh < NBT) {
-                            const double* D = Ds + b * KP * DSTRIDE;
                             double* G = Gs + b * p.grows * GSTRIDE;
                             const double* D1 = D + K0 * DSTRIDE + g + nbh * 8;
                             double acc[MH][4];
@@ -401,6 +457,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
 #pragma unroll
                             for (int j = 0; j < KS; ++j) {
                                 const int cur = j & 1;
+                                if (j == KS - 1) wait_g(it);
                                 if (j + 1 < KS) bq[cur ^ 1] = D1[(4 * (j + 1) + t) * DSTRIDE];
 #pragma unroll
                                 for (int mb = 0; mb < MH; ++mb)
@@ -417,13 +474,120 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                                 *reinterpret_cast<double2*>(G + (rh + 8) * GSTRIDE + col) =
                                     make_double2(fma(ak1[mb], cv.x, acc[mb][2]), fma(ak1[mb], cv.y, acc[mb][3]));
                             }
+                        } else {
+                            wait_g(it);
                         }
-                        bar_arrive(BAR_FULL + b, kWsThreads);
+                        if (!(p.dbg & 16)) bar_arrive(BAR_FULL + b, kWsThreads);
                     }
-                    for (int it = ntot - 2 < 0 ? 0 : ntot - 2; it < ntot; ++it)
-                        bar_sync(BAR_EMPTY + (it & 1), kWsThreads);
+                    drain_g(ntot);
                     continue;  // next row
                 }
+            }
+            if constexpr (XS > 0) {
+                constexpr int KH = (KS + 1) / 2;          // iterations carrying an extra-row DMMA
+                const int koff = (XS == 2 && w >= 4) ? KS - KH : 0;  // k-step of iteration 0
+                const int xb = w & 3;                     // extra rows: this warp's n8 block
+                const bool xodd = xb & 1;
+                const int c01 = XS == 2 ? 16 * (xb >> 1) : 0, c23 = 16 - c01;  // columns of local blocks 0,1 / 2,3
+                const int r0 = 16 * w + g, re = 16 * p.mb16;
+                double a0[KS], a1[KS], aer[XS == 2 ? KH : 1];
+#pragma unroll
+                for (int i = 0; i < KS; ++i) {
+                    int kk = i + koff;
+                    if (kk >= KS) kk -= KS;
+                    const int k = K0 + 4 * kk + t;
+                    a0[i] = main_ok ? aval(r0, k) : 0.0;
+                    a1[i] = main_ok ? aval(r0 + 8, k) : 0.0;
+                }
+                if constexpr (XS == 2) {
+#pragma unroll
+                    for (int i = 0; i < KH; ++i) {
+                        const int kk = i + koff;  // odd KS: the middle k-step belongs to warps 0-3
+                        aer[i] = (w >= 4 && kk < KH) ? 0.0 : aval(re + g, K0 + 4 * kk + t);
+                    }
+                } else {
+                    aer[0] = 0.0;
+                }
+                const double a00 = (K0E && main_ok) ? aval(r0, 0) : 0.0, a01 = (K0E && main_ok) ? aval(r0 + 8, 0) : 0.0;
+                const double ae0 = (XS == 2 && K0E && w < 4) ? aval(re + g, 0) : 0.0;
+                const int gx = (re + (w >= 4 ? 8 : 0) + g) * GSTRIDE + c01 + 4 * t + (xodd ? 1 : 0);  // extra partials
+                int sd = 0;
+                for (int it = 0; it < ntot; ++it) {
+                    const int b = it & 1;
+                    const double* D = wait_d(it, sd);
+                    if (!(p.dbg & 2) && (main_ok || XS == 2)) {
+                        double* G = Gs + b * p.grows * GSTRIDE;
+                        const double* pLo = D + (K0 + 4 * koff + t) * DSTRIDE + 2 * g;
+                        const double* pHi = koff ? pLo - 4 * KS * DSTRIDE : pLo;
+                        double acc[4][4];
+                        double acx[2] = {0.0, 0.0};
+#pragma unroll
+                        for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) acc[nb][e] = 0.0;
+                        double2 q[2][2];  // B fragments of local blocks (0,1) and (2,3), one k-step ahead
+                        q[0][0] = *reinterpret_cast<const double2*>(pLo + c01);
+                        q[0][1] = *reinterpret_cast<const double2*>(pLo + c23);
+#pragma unroll
+                        for (int i = 0; i < KS; ++i) {
+                            const int cur = i & 1;
+                            if (i == KS - 1) wait_g(it);  // G buffer b is written from here on
+                            if (i + 1 < KS) {
+                                const double* pn = ((i + 1 < KH) ? pLo : pHi) + (i + 1) * 4 * DSTRIDE;
+                                q[cur ^ 1][0] = *reinterpret_cast<const double2*>(pn + c01);
+                                q[cur ^ 1][1] = *reinterpret_cast<const double2*>(pn + c23);
+                            }
+                            dmma_16x8x4(acc[0], a0[i], a1[i], q[cur][0].x);
+                            dmma_16x8x4(acc[1], a0[i], a1[i], q[cur][0].y);
+                            dmma_16x8x4(acc[2], a0[i], a1[i], q[cur][1].x);
+                            dmma_16x8x4(acc[3], a0[i], a1[i], q[cur][1].y);
+                            if constexpr (XS == 2) {
+                                if (i < KH) dmma_8x8x4(acx, aer[i], xodd ? q[cur][0].y : q[cur][0].x);
+                            }
+                        }
+                        // epilogue: column of acc[L][e] = (L < 2 ? c01 : c23) + 4 t + 2 (e & 1) + (L & 1),
+                        // rows g (e < 2) and g + 8; the k = 0 rank-1 term (K0E) first
+                        const int ca = c01 + 4 * t, cb = c23 + 4 * t;
+                        if constexpr (K0E) {
+                            const double2 va0 = *reinterpret_cast<const double2*>(D + ca), va1 = *reinterpret_cast<const double2*>(D + ca + 2);
+                            const double2 vb0 = *reinterpret_cast<const double2*>(D + cb), vb1 = *reinterpret_cast<const double2*>(D + cb + 2);
+                            acc[0][0] = fma(a00, va0.x, acc[0][0]); acc[1][0] = fma(a00, va0.y, acc[1][0]);
+                            acc[0][1] = fma(a00, va1.x, acc[0][1]); acc[1][1] = fma(a00, va1.y, acc[1][1]);
+                            acc[0][2] = fma(a01, va0.x, acc[0][2]); acc[1][2] = fma(a01, va0.y, acc[1][2]);
+                            acc[0][3] = fma(a01, va1.x, acc[0][3]); acc[1][3] = fma(a01, va1.y, acc[1][3]);
+                            acc[2][0] = fma(a00, vb0.x, acc[2][0]); acc[3][0] = fma(a00, vb0.y, acc[3][0]);
+                            acc[2][1] = fma(a00, vb1.x, acc[2][1]); acc[3][1] = fma(a00, vb1.y, acc[3][1]);
+                            acc[2][2] = fma(a01, vb0.x, acc[2][2]); acc[3][2] = fma(a01, vb0.y, acc[3][2]);
+                            acc[2][3] = fma(a01, vb1.x, acc[2][3]); acc[3][3] = fma(a01, vb1.y, acc[3][3]);
+                            if constexpr (XS == 2) {  // warps 0-3 carry the extra rows' k = 0 term
+                                const double x0 = xodd ? va0.y : va0.x, x1 = xodd ? va1.y : va1.x;
+                                acx[0] = fma(ae0, x0, acx[0]);
+                                acx[1] = fma(ae0, x1, acx[1]);
+                            }
+                        }
+                        if (main_ok) {
+                            double* g0 = G + r0 * GSTRIDE;
+                            double* g1 = g0 + 8 * GSTRIDE;
+                            *reinterpret_cast<double2*>(g0 + ca) = make_double2(acc[0][0], acc[1][0]);
+                            *reinterpret_cast<double2*>(g0 + ca + 2) = make_double2(acc[0][1], acc[1][1]);
+                            *reinterpret_cast<double2*>(g1 + ca) = make_double2(acc[0][2], acc[1][2]);
+                            *reinterpret_cast<double2*>(g1 + ca + 2) = make_double2(acc[0][3], acc[1][3]);
+                            *reinterpret_cast<double2*>(g0 + cb) = make_double2(acc[2][0], acc[3][0]);
+                            *reinterpret_cast<double2*>(g0 + cb + 2) = make_double2(acc[2][1], acc[3][1]);
+                            *reinterpret_cast<double2*>(g1 + cb) = make_double2(acc[2][2], acc[3][2]);
+                            *reinterpret_cast<double2*>(g1 + cb + 2) = make_double2(acc[2][3], acc[3][3]);
+                        }
+                        if constexpr (XS == 2) {
+                            G[gx] = acx[0];
+                            G[gx + 2] = acx[1];
+                        }
+                    } else {
+                        wait_g(it);
+                    }
+                    if (!(p.dbg & 16)) bar_arrive(BAR_FULL + b, kWsThreads);
+                }
+                drain_g(ntot);
+                continue;  // next row
             }
             double a0[KS], a1[KS];
             const int r0 = 16 * w + g, re = 16 * p.mb16;
@@ -442,12 +606,11 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
 #pragma unroll
             for (int j = 0; j < KS; ++j) aer[j] = do_extra ? sAe[(K0 + 4 * j + t) * 8 + g] : 0.0;
             const double ae0 = (K0E && do_extra) ? sAe[g] : 0.0;
+            int sd = 0;
             for (int it = 0; it < ntot; ++it) {
                 const int b = it & 1;
-                bar_sync(BAR_DREADY + b, kWsThreads);
-                if (it >= 2) bar_sync(BAR_EMPTY + b, kWsThreads);
+                const double* D = wait_d(it, sd);
                 if (!(p.dbg & 2) && main_ok) {
-                    const double* D = Ds + b * KP * DSTRIDE;
                     double* G = Gs + b * p.grows * GSTRIDE;
                     double acc[NBT][4];
                     double ace0[2] = {0.0, 0.0}, ace1[2] = {0.0, 0.0};
@@ -470,6 +633,9 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
 #pragma unroll
                     for (int j = 0; j < KS; ++j) {
                         const int cur = j % BFD;
+                        // decoupled: G buffer b is needed from here on (before the last k-step, so the
+                        // staging stores still interleave with the tail of the DMMA chains)
+                        if (j == KS - 1) wait_g(it);
                         if (j + BFD - 1 < KS) {
 #pragma unroll
                             for (int nb = 0; nb < NBT; ++nb)
@@ -488,25 +654,34 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                         }
                     }
                     // epilogue: the k = 0 rank-1 term (K0E; a00 = a01 = ae0 = 0 otherwise), then
-                    // 16-byte stores of the tile
+                    // 16-byte stores of the tile (decoupled: once the scatter has handed buffer b back)
 #pragma unroll
                     for (int nb = 0; nb < NBT; ++nb) {
                         const int col = nb * 8 + 2 * t;
                         const double2 cv = K0E ? *reinterpret_cast<const double2*>(D + col) : make_double2(0.0, 0.0);
-                        *reinterpret_cast<double2*>(G + r0 * GSTRIDE + col) =
-                            make_double2(fma(a00, cv.x, acc[nb][0]), fma(a00, cv.y, acc[nb][1]));
-                        *reinterpret_cast<double2*>(G + (r0 + 8) * GSTRIDE + col) =
-                            make_double2(fma(a01, cv.x, acc[nb][2]), fma(a01, cv.y, acc[nb][3]));
+                        acc[nb][0] = fma(a00, cv.x, acc[nb][0]);
+                        acc[nb][1] = fma(a00, cv.y, acc[nb][1]);
+                        acc[nb][2] = fma(a01, cv.x, acc[nb][2]);
+                        acc[nb][3] = fma(a01, cv.y, acc[nb][3]);
                     }
+                    double2 ge = make_double2(0.0, 0.0);
                     if (do_extra) {
                         const double2 cv = K0E ? *reinterpret_cast<const double2*>(D + w * 8 + 2 * t) : make_double2(0.0, 0.0);
-                        *reinterpret_cast<double2*>(G + (re + g) * GSTRIDE + w * 8 + 2 * t) =
-                            make_double2(fma(ae0, cv.x, ace0[0] + ace1[0]), fma(ae0, cv.y, ace0[1] + ace1[1]));
+                        ge = make_double2(fma(ae0, cv.x, ace0[0] + ace1[0]), fma(ae0, cv.y, ace0[1] + ace1[1]));
                     }
+#pragma unroll
+                    for (int nb = 0; nb < NBT; ++nb) {
+                        const int col = nb * 8 + 2 * t;
+                        *reinterpret_cast<double2*>(G + r0 * GSTRIDE + col) = make_double2(acc[nb][0], acc[nb][1]);
+                        *reinterpret_cast<double2*>(G + (r0 + 8) * GSTRIDE + col) = make_double2(acc[nb][2], acc[nb][3]);
+                    }
+                    if (do_extra) *reinterpret_cast<double2*>(G + (re + g) * GSTRIDE + w * 8 + 2 * t) = ge;
+                } else {
+                    wait_g(it);
                 }
-                bar_arrive(BAR_FULL + b, kWsThreads);
+                if (!(p.dbg & 16)) bar_arrive(BAR_FULL + b, kWsThreads);
             }
-            for (int it = ntot - 2 < 0 ? 0 : ntot - 2; it < ntot; ++it) bar_sync(BAR_EMPTY + (it & 1), kWsThreads);
+            drain_g(ntot);
         }
     } else {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 " SBG_STR(SBG_WS_SREG) ";\n");
@@ -517,12 +692,16 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
         }
         if (p.tma) {
             if (stid == 0) {
-                for (int i = 0; i < 4; ++i) mbar_init(mbar + i, 1);
+                // D stages: one tx-counted arrival (bulk copies) or one deferred arrival per loader
+                // thread (cp.async, decoupled mode); lists: tx-counted; G hand-back: one per loader warp
+                for (int i = 0; i < 3; ++i) mbar_init(mbD + i, (p.dc && p.tma < 2) ? kWsHalf : 1);
+                for (int i = 0; i < 2; ++i) mbar_init(mbL + i, 1);
+                for (int i = 0; i < 2; ++i) mbar_init(mbE + i, kWsHalf / 32);
                 mbar_init_fence();
             }
-            // bulk-copy pipeline (red mode): warp 8 issues every D row (one 256-byte copy per linked
-            // alpha row) and the tile's reduction list (one copy) on the TMA engine; D(it) and
-            // lists(it) complete on mbar[it & 1] / mbar[2 + (it & 1)], whose phase parity every
+            // bulk-copy pipeline (red mode): warp 8 issues the tile's reduction list (one copy) and,
+            // with tma >= 2, every D row (one 256-byte copy per linked alpha row) on the TMA engine;
+            // D(it) and lists(it) complete on mbD[stage] / mbL[it & 1], whose phase parity every
             // loader thread tracks in phD / phL (one completion per tile of that stage)
             uint32_t phD = 0, phL = 0;
             const bool prod = (stid >> 5) == 0;
@@ -556,9 +735,13 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                 }
                 bar_sync(BAR_SINT, kWsHalf);  // sJ visible to the producer warp; previous row's lists read
                 bar_arrive(BAR_KLIST, kWsThreads);
+                if (p.dbg & 16) continue;  // timing experiment: the MMA warps free-run
                 const bool d_bulk = p.tma >= 2;
                 auto gather_d = [&](int stage, int T) {  // tma == 1: D rows by cp.async, all loader threads
-                    if (p.dbg & 4) return;
+                    if (p.dbg & 4) {
+                        if (p.dc) cp_async_mbar_arrive_noinc(mbD + stage);
+                        return;
+                    }
                     const int jt = T % ntiles;
                     const double* xs = p.xv[T / ntiles];
                     double* dst = Ds + stage * KP * DSTRIDE;
@@ -567,30 +750,81 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                         cp_async16(dst + k * DSTRIDE + part * 2, xs + (int64_t)sJ[k] * p.ld + (int64_t)jt * NT + part * 2);
                     }
                     cp_async_commit();
+                    if (p.dc) cp_async_mbar_arrive_noinc(mbD + stage);  // fires when this thread's rows landed
                 };
                 auto issue_d = [&](int stage, int T) {  // producer warp only
                     const int jt = T % ntiles;
                     const double* xs = p.xv[T / ntiles];
                     if (p.dbg & 4) {
-                        if (plane == 0) mbar_arrive_expect_tx(mbar + stage, 0);
+                        if (plane == 0) mbar_arrive_expect_tx(mbD + stage, 0);
                         return;
                     }
                     fence_proxy_async_smem();  // the MMA warps' reads of this stage precede the refill
-                    if (plane == 0) mbar_arrive_expect_tx(mbar + stage, (uint32_t)(KP * NT * 8));
+                    if (plane == 0) mbar_arrive_expect_tx(mbD + stage, (uint32_t)(KP * NT * 8));
                     __syncwarp();
                     double* dst = Ds + stage * KP * DSTRIDE;
                     for (int k = plane; k < KP; k += 32)
-                        bulk_g2s(dst + k * DSTRIDE, xs + (int64_t)sJ[k] * p.ld + (int64_t)jt * NT, NT * 8, mbar + stage);
+                        bulk_g2s(dst + k * DSTRIDE, xs + (int64_t)sJ[k] * p.ld + (int64_t)jt * NT, NT * 8, mbD + stage);
                 };
                 auto issue_l = [&](int stage, int T) {
                     const int jt = T % ntiles;
                     if (plane == 0) {
                         const uint32_t e0 = sTE[jt], bytes = (sTE[jt + 1] - e0) * 4;
                         fence_proxy_async_smem();
-                        mbar_arrive_expect_tx(mbar + 2 + stage, bytes);
-                        if (bytes) bulk_g2s(Le + stage * p.maxE, p.ent32 + e0, bytes, mbar + 2 + stage);
+                        mbar_arrive_expect_tx(mbL + stage, bytes);
+                        if (bytes) bulk_g2s(Le + stage * p.maxE, p.ent32 + e0, bytes, mbL + stage);
                     }
                 };
+                if (p.dc) {
+                    // decoupled hand-offs: the MMA warps take D(it) from mbD and hand G back through
+                    // mbE, so this loop never waits for its own gathers and only meets the MMA warps
+                    // at FULL (G(it) staged, D stage of tile it free)
+                    for (int jt = 0; jt < p.dc && jt < ntot; ++jt) {
+                        if (d_bulk) {
+                            if (prod) issue_d(jt, jt);
+                        } else {
+                            gather_d(jt, jt);
+                        }
+                    }
+                    for (int jt = 0; jt < 2 && jt < ntot; ++jt)
+                        if (prod) issue_l(jt, jt);
+                    int sd = 0;  // D stage of tile it
+                    for (int it = 0; it < ntot; ++it) {
+                        const int b = it & 1, lt = it % ntiles;
+                        double* yrow = p.yv[it / ntiles] + (ia - p.row_lo) * p.ld;
+                        bar_sync(BAR_FULL + b, kWsThreads);   // G(it) staged; D stage sd free
+                        if (it + p.dc < ntot) {
+                            if (!d_bulk) gather_d(sd, it + p.dc);
+                            else if (prod) issue_d(sd, it + p.dc);
+                        }
+                        sd = (sd + 1 == p.dc) ? 0 : sd + 1;
+                        mbar_wait_parity(mbL + b, (phL >> b) & 1u);  // lists(it) landed
+                        phL ^= 1u << b;
+                        if (!(p.dbg & 1)) {
+                            const double* G = Gs + b * p.grows * GSTRIDE;
+                            const uint32_t* l32 = reinterpret_cast<const uint32_t*>(Le + b * p.maxE);
+                            const uint32_t n = sTE[lt + 1] - sTE[lt];
+#pragma unroll RED_UNROLL
+                            for (uint32_t i = stid; i < n; i += kWsHalf) {
+                                const uint32_t en = l32[i];
+                                if (en == 0xFFFFFFFFu) continue;  // 16-byte padding
+                                const long long bits = __double_as_longlong(G[en & 0x7FFFu]) ^ ((long long)(en & 0x8000u) << 48);
+                                red_add_f64(yrow + (en >> 16), __longlong_as_double(bits));
+                            }
+                        }
+                        __syncwarp();
+                        if (plane == 0) mbar_arrive(mbE + b);  // this warp is done with G(it)
+                        bar_sync(BAR_SINT, kWsHalf);           // lists stage b read by every loader
+                        if (it + 2 < ntot && prod) issue_l(b, it + 2);
+                    }
+                    if (p.e_core != 0.0 && p.add_ecore)  // e_core * x, reduced like the tiles
+                        for (int v = 0; v < p.nvec; ++v) {
+                            const double* xr = p.xv[v] + ia * p.ld;
+                            double* yrow = p.yv[v] + (ia - p.row_lo) * p.ld;
+                            for (int64_t c = stid; c < p.NB; c += kWsHalf) red_add_f64(yrow + c, p.e_core * xr[c]);
+                        }
+                    continue;  // next row
+                }
                 for (int jt = 0; jt < 2 && jt < ntot; ++jt) {
                     if (prod) {
                         if (d_bulk) issue_d(jt, jt);
@@ -604,7 +838,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                 }
                 for (int jt = 0; jt < 2 && jt < ntot; ++jt) {
                     if (d_bulk) {
-                        mbar_wait_parity(mbar + jt, (phD >> jt) & 1u);
+                        mbar_wait_parity(mbD + jt, (phD >> jt) & 1u);
                         phD ^= 1u << jt;
                     }
                     bar_arrive(BAR_DREADY + jt, kWsThreads);
@@ -617,7 +851,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                         if (!d_bulk) gather_d(b, it + 2);
                         else if (prod) issue_d(b, it + 2);
                     }
-                    mbar_wait_parity(mbar + 2 + b, (phL >> b) & 1u);  // lists(it) landed
+                    mbar_wait_parity(mbL + b, (phL >> b) & 1u);  // lists(it) landed
                     phL ^= 1u << b;
                     if (!(p.dbg & 1)) {
                         const double* G = Gs + b * p.grows * GSTRIDE;
@@ -637,7 +871,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                     if (it + 2 < ntot) {
                         if (prod) issue_l(b, it + 2);
                         if (d_bulk) {
-                            mbar_wait_parity(mbar + b, (phD >> b) & 1u);   // D(it+2) landed
+                            mbar_wait_parity(mbD + b, (phD >> b) & 1u);   // D(it+2) landed
                             phD ^= 1u << b;
                         }
                         bar_arrive(BAR_DREADY + b, kWsThreads);
@@ -792,9 +1026,9 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
     }
 }
 
-template <int KS, int NT, bool K0E, bool TALL = false>
+template <int KS, int NT, bool K0E, bool TALL = false, int XS = 0>
 void launch_ks(const AbPlan& pl, const AbParams& prm, int grid, cudaStream_t st) {
-    auto kern = pl.ws ? k_sigma_ab_ws<KS, NT, K0E, TALL> : k_sigma_ab<KS, NT>;
+    auto kern = pl.ws ? k_sigma_ab_ws<KS, NT, K0E, TALL, XS> : k_sigma_ab<KS, NT>;
     static int configured[2][64] = {{0}};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -908,7 +1142,7 @@ AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int
             pl.maxE = 2 * 4 * ((nt * (nb_el + nb_el * (norb - nb_el)) + 3) / 4);
         }
         const int64_t ntiles = ld / nt;
-        pl.smem = 32 + (size_t)(pl.red ? 0 : ld) * 8 + (size_t)STAGES * KP * (nt + 4) * 8 + (size_t)KP * 8 * 8 +
+        pl.smem = 64 + (size_t)(pl.red ? 0 : ld) * 8 + (size_t)STAGES * KP * (nt + 4) * 8 + (size_t)KP * 8 * 8 +
                   (size_t)STAGES * pl.npad * (nt + 8) * 8 + (size_t)STAGES * (pl.maxT * 4 + pl.maxE * 2) +
                   (size_t)(ntiles + 1) * 8 + (size_t)KP * 16 + 16;
     };
@@ -936,6 +1170,32 @@ AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int
     // latency), 0 = cp.async for both
     const char* tma_env = getenv("SBG_AB_TMA");
     pl.tma = (pl.ws && pl.red) ? (tma_env ? atoi(tma_env) : 1) : 0;
+    // decoupled hand-offs (mbarrier D announcements, G handed back after the DMMAs) with a third D
+    // stage when it fits; SBG_AB_DC=0 keeps the named-barrier hand-offs, =2 two D stages
+    // uniform MMA instruction stream (see k_sigma_ab_ws): 1 = no extra rows, 2 = extra rows split
+    // over all eight warps (needs all eight m16 blocks in use); SBG_AB_XS=0 keeps the older stream
+    const char* xs_env = getenv("SBG_AB_XS");
+    pl.xs = 0;
+    if (pl.tma && pl.nt == 32 && !pl.tall && !(xs_env && atoi(xs_env) == 0)) {
+        if (!pl.extra) pl.xs = 1;
+        else if (pl.mb16 == 8) pl.xs = 2;
+    }
+    pl.gstride = pl.xs ? pl.nt + 2 : pl.nt + 8;
+    pl.grows = pl.npad + (pl.xs == 2 ? 8 : 0);
+    if (pl.xs) {  // G tiles: grows x gstride instead of npad x (nt + 8); lists: both partials of the extra rows
+        pl.smem -= (size_t)STAGES * pl.npad * (pl.nt + 8) * 8;
+        pl.smem += (size_t)STAGES * pl.grows * pl.gstride * 8;
+        if (pl.xs == 2) {
+            pl.smem += (size_t)STAGES * 2 * (pl.nt * 8) * 2;
+            pl.maxE += 2 * pl.nt * 8;
+        }
+    }
+    const char* dc_env = getenv("SBG_AB_DC");
+    pl.dc = pl.tma ? (dc_env ? atoi(dc_env) : 3) : 0;
+    if (pl.dc != 0 && pl.dc != 2 && pl.dc != 3) pl.dc = 3;
+    const size_t dstage = (size_t)KP * (pl.nt + 4) * 8;
+    if (pl.dc == 3 && pl.smem + dstage > 227 * 1024) pl.dc = 2;
+    if (pl.dc == 3) pl.smem += dstage;
     return pl;
 }
 
@@ -981,7 +1241,7 @@ void build_ab_scatter(const AbPlan& pl, const std::vector<uint16_t>& codes, std:
 // order, padded to 4 entries
 void build_ab_red_list(const AbPlan& pl, const std::vector<uint16_t>& codes, std::vector<uint32_t>& ent,
                        std::vector<uint32_t>& tile_ent, int m0) {
-    const int NT = pl.nt, GSTRIDE = pl.nt + 8;  // Tile<NT>::GSTRIDE
+    const int NT = pl.nt, GSTRIDE = pl.gstride ? pl.gstride : pl.nt + 8;  // the kernel's G row stride
     const int64_t ntiles = pl.ld / NT;
     ent.clear();
     tile_ent.assign(ntiles + 1, 0);
@@ -994,6 +1254,9 @@ void build_ab_red_list(const AbPlan& pl, const std::vector<uint16_t>& codes, std
                 const uint16_t code = codes[(size_t)(jt * NT + c) * pl.code_ld + rs + m0];
                 if (code == 0xFFFF) continue;
                 items.push_back({(uint32_t)(code & 0x7FFF), (uint32_t)((rs * GSTRIDE + c) | (code & 0x8000))});
+                // xs == 2: the extra rows' second partial sum (warps 4-7) sits eight G rows further
+                if (pl.xs == 2 && rs >= 16 * pl.mb16)
+                    items.push_back({(uint32_t)(code & 0x7FFF), (uint32_t)(((rs + 8) * GSTRIDE + c) | (code & 0x8000))});
             }
         // kept in G order (rs-major): a warp's shared-memory reads of G are then near-contiguous;
         // target-sorting them instead (a warp reducing into neighbouring y elements) measured
@@ -1036,6 +1299,7 @@ void launch_sigma_ab_multi(const AbPlan& pl, const AbScatter& sc, const double* 
     prm.tile_ent32 = sc.tile_ent32;
     prm.m0 = pass * 128;
     prm.tma = pl.tma;
+    prm.dc = pl.dc;
     prm.add_ecore = pass == 0;
     if (pass > 0 && !(pl.red && pl.ws)) throw InvalidArgument("sigma_ab: pair-row passes need the reduction kernel");
     if (pl.red && !accumulate) throw InvalidArgument("sigma_ab: reduction mode needs an initialised y");
@@ -1046,7 +1310,7 @@ void launch_sigma_ab_multi(const AbPlan& pl, const AbScatter& sc, const double* 
     prm.extra = pl.extra;
     prm.K = pl.K;
     prm.KP = pl.k0e ? 1 + 4 * pl.KS : 4 * pl.KS;
-    prm.grows = pl.npad;
+    prm.grows = pl.grows ? pl.grows : pl.npad;
     prm.maxT = pl.maxT;
     prm.maxE = pl.maxE;
     prm.NB = pl.NB;
@@ -1065,6 +1329,12 @@ void launch_sigma_ab_multi(const AbPlan& pl, const AbScatter& sc, const double* 
                 if (pl.k0e) launch_ks<n, 32, true, true>(pl, prm, grid, st);                        \
                 else launch_ks<n, 32, false, true>(pl, prm, grid, st);                              \
             }                                                                                       \
+        } else if (pl.nt == 32 && pl.xs == 2) {                                                     \
+            if (pl.k0e) launch_ks<n, 32, true, false, 2>(pl, prm, grid, st);                        \
+            else launch_ks<n, 32, false, false, 2>(pl, prm, grid, st);                              \
+        } else if (pl.nt == 32 && pl.xs == 1) {                                                     \
+            if (pl.k0e) launch_ks<n, 32, true, false, 1>(pl, prm, grid, st);                        \
+            else launch_ks<n, 32, false, false, 1>(pl, prm, grid, st);                              \
         } else if (pl.nt == 32) {                                                                   \
             if (pl.k0e) launch_ks<n, 32, true>(pl, prm, grid, st);                                  \
             else launch_ks<n, 32, false>(pl, prm, grid, st);                                        \
@@ -1073,8 +1343,12 @@ void launch_sigma_ab_multi(const AbPlan& pl, const AbScatter& sc, const double* 
             else launch_ks<n, 16, false>(pl, prm, grid, st);                                        \
         }                                                                                           \
         break;
+#ifdef SBG_KS_ONLY  // developer builds: one k-step count (c4: 16) compiles in seconds
+        SBG_KS(SBG_KS_ONLY)
+#else
         SBG_KS(1) SBG_KS(2) SBG_KS(3) SBG_KS(4) SBG_KS(5) SBG_KS(6) SBG_KS(7) SBG_KS(8) SBG_KS(9) SBG_KS(10)
         SBG_KS(11) SBG_KS(12) SBG_KS(13) SBG_KS(14) SBG_KS(15) SBG_KS(16) SBG_KS(17)
+#endif
 #undef SBG_KS
         default: throw InvalidArgument("sigma_ab: unsupported K");
     }
