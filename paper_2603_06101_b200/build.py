@@ -50,8 +50,18 @@ def nccl_link():
     return ["-lnccl", "-Xlinker", "-rpath,/usr/lib/x86_64-linux-gnu"]
 
 
-def _compile(src, ptxas_verbose):
+def _headers_mtime():
+    hs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp", ".h"))]
+    hs.append(os.path.join(ROOT, "include", "sbg.h"))
+    return max(os.path.getmtime(h) for h in hs)
+
+
+def _compile(src, ptxas_verbose, force=True):
     out = os.path.join(OBJ, src.replace(".cu", ".o"))
+    # incremental: an object newer than its source and every header is kept
+    if (not force and not ptxas_verbose and os.path.exists(out)
+            and os.path.getmtime(out) > max(os.path.getmtime(os.path.join(CSRC, src)), _headers_mtime())):
+        return out, ""
     cmd = [nvcc(), *ARCH, *FLAGS, *EXTRA, *PER_FILE.get(src, []), "-c", os.path.join(CSRC, src), "-o", out]
     if ptxas_verbose:
         cmd += ["-Xptxas", "-v"]
@@ -68,7 +78,7 @@ def build(ptxas_verbose=False, force=False):
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) > newest_src and not ptxas_verbose:
         return LIB
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
-        results = list(ex.map(lambda s: _compile(s, ptxas_verbose), SOURCES))
+        results = list(ex.map(lambda s: _compile(s, ptxas_verbose, force), SOURCES))
     if ptxas_verbose:
         for _, err in results:
             sys.stderr.write(err)

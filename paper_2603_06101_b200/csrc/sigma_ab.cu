@@ -351,9 +351,13 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
     uint16_t* Le = reinterpret_cast<uint16_t*>(Lt + STAGES * p.maxT);   // red mode: u32 entries
     uint32_t* sTT = reinterpret_cast<uint32_t*>(Le + STAGES * p.maxE);
     uint32_t* sTE = sTT + ntiles + 1;
-    int* sJ = reinterpret_cast<int*>(sTE + ntiles + 1);
-    int* sPair = sJ + KP;
-    double* sSign = reinterpret_cast<double*>(sPair + KP);
+    // K-list of an alpha row, double buffered (the loaders build row r+1's while row r runs):
+    // sJ = linked alpha string, sOff = its pair's row of V' (pair * npair), sSign = +-1 (0 for k = 0
+    // and padding), sOcc = the occupation column A(:, 0) of this pass's pair rows
+    int* sJ = reinterpret_cast<int*>(sTE + ntiles + 1);        // [2][KP]
+    int* sOff = sJ + 2 * KP;                                   // [2][KP]
+    double* sSign = reinterpret_cast<double*>(sOff + 2 * KP);  // [2][KP]
+    double* sOcc = sSign + 2 * KP;                             // [2][grows]
 
     const int tid = threadIdx.x;
     const int w = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
@@ -404,23 +408,22 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                 }
             }
         };
-        for (int64_t ia = p.row_lo + blockIdx.x; ia < p.row_hi; ia += gridDim.x) {
-            bar_sync(0, kWsThreads);           // row start
-            bar_sync(BAR_KLIST, kWsThreads);   // K-list of row ia ready (built by the loader warps)
-            const uint64_t sa = string_unrank((uint64_t)ia, p.na_el, norb);
+        int kb = 0;  // K-list buffer of this row
+        for (int64_t ia = p.row_lo + blockIdx.x; ia < p.row_hi; ia += gridDim.x, kb ^= p.tma ? 1 : 0) {
+            bar_sync(0, kWsThreads);           // row start (bulk-copy path: this row's K-list was built during the previous row)
+            if (!p.tma) bar_sync(BAR_KLIST, kWsThreads);   // K-list of row ia ready (built by the loader warps)
+            const int* sOffB = sOff + kb * KP;
+            const double* sSignB = sSign + kb * KP;
+            const double* sOccB = sOcc + kb * p.grows;
+            // A(rs, k) = sign_k V'(pair_k, rs), branch free so that a warp's loads of V' go out together
+            // (one L2 round trip per row instead of one per element)
+            auto aocc = [&](int rs) -> double { return sOccB[rs]; };
             auto aval = [&](int rs, int k) -> double {
-                rs += p.m0;  // pair-row block of this pass
-                if (rs >= npair || k >= p.K) return 0.0;
-                const int pr = sPair[k];
-                if (pr == -1) {
-                    double s = 0.0;
-                    for (uint64_t m = sa; m; m &= m - 1) {
-                        const int q = __ffsll((long long)m) - 1;
-                        s += p.Vp[(size_t)pair_sym(q, q) * npair + rs];
-                    }
-                    return s;
-                }
-                return sSign[k] * p.Vp[(size_t)pr * npair + rs];
+                const int rr = rs + p.m0;  // pair-row block of this pass
+                const double v = p.Vp[(size_t)sOffB[k] + (rr < npair ? rr : 0)];
+                double a = (rr < npair) ? sSignB[k] * v : 0.0;
+                if (!K0E) a = (k == 0) ? sOccB[rs] : a;
+                return a;
             };
             if constexpr (TALL) {
                 if (tall) {
@@ -436,8 +439,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                             ah0[mb][j] = ok ? aval(rh, K0 + 4 * j + t) : 0.0;
                             ah1[mb][j] = ok ? aval(rh + 8, K0 + 4 * j + t) : 0.0;
                         }
-                        ak0[mb] = (K0E && ok) ? aval(rh, 0) : 0.0;
-                        ak1[mb] = (K0E && ok) ? aval(rh + 8, 0) : 0.0;
+                        ak0[mb] = (K0E && ok) ? aocc(rh) : 0.0;
+                        ak1[mb] = (K0E && ok) ? aocc(rh + 8) : 0.0;
                     }
                     bar_sync(BAR_MINT, kWsHalf);
                     int sd = 0;
@@ -496,8 +499,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                     int kk = i + koff;
                     if (kk >= KS) kk -= KS;
                     const int k = K0 + 4 * kk + t;
-                    a0[i] = main_ok ? aval(r0, k) : 0.0;
-                    a1[i] = main_ok ? aval(r0 + 8, k) : 0.0;
+                    a0[i] = aval(main_ok ? r0 : 0, k);  // rows of idle warps (mb16 < 8) are never staged
+                    a1[i] = aval(main_ok ? r0 + 8 : 0, k);
                 }
                 if constexpr (XS == 2) {
 #pragma unroll
@@ -508,8 +511,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                 } else {
                     aer[0] = 0.0;
                 }
-                const double a00 = (K0E && main_ok) ? aval(r0, 0) : 0.0, a01 = (K0E && main_ok) ? aval(r0 + 8, 0) : 0.0;
-                const double ae0 = (XS == 2 && K0E && w < 4) ? aval(re + g, 0) : 0.0;
+                const double a00 = (K0E && main_ok) ? aocc(r0) : 0.0, a01 = (K0E && main_ok) ? aocc(r0 + 8) : 0.0;
+                const double ae0 = (XS == 2 && K0E && w < 4) ? aocc(re + g) : 0.0;
                 const int gx = (re + (w >= 4 ? 8 : 0) + g) * GSTRIDE + c01 + 4 * t + (xodd ? 1 : 0);  // extra partials
                 int sd = 0;
                 for (int it = 0; it < ntot; ++it) {
@@ -597,9 +600,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                 a0[j] = main_ok ? aval(r0, k) : 0.0;
                 a1[j] = main_ok ? aval(r0 + 8, k) : 0.0;
             }
-            const double a00 = (K0E && main_ok) ? aval(r0, 0) : 0.0, a01 = (K0E && main_ok) ? aval(r0 + 8, 0) : 0.0;
+            const double a00 = (K0E && main_ok) ? aocc(r0) : 0.0, a01 = (K0E && main_ok) ? aocc(r0 + 8) : 0.0;
             if (p.extra)
-                for (int i = tid; i < KP * 8; i += kWsHalf) sAe[i] = aval(re + (i & 7), i >> 3);
+                for (int i = tid; i < KP * 8; i += kWsHalf)
+                    sAe[i] = (K0E && (i >> 3) == 0) ? aocc(re + (i & 7)) : aval(re + (i & 7), i >> 3);
             bar_sync(BAR_MINT, kWsHalf);
             // the extra m8 rows' A fragments stay in registers too (warps w < NBT)
             double aer[KS];
@@ -690,6 +694,41 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
             sTT[i] = p.red ? 0u : p.tile_tgt[i];
             sTE[i] = p.red ? p.tile_ent32[i] : p.tile_ent[i];
         }
+        // K-list of alpha row ia into buffer kb: k = 0 the row itself (occupation column, carried by
+        // sOcc), k >= 1 its single excitations (q occupied ascending, p virtual ascending)
+        auto build_klist = [&](int64_t ia, int kb) {
+            const uint64_t sa = string_unrank((uint64_t)ia, p.na_el, norb);
+            for (int k = stid; k < KP; k += kWsHalf) {
+                int J = (int)ia, off = 0;
+                double sg = 0.0;
+                if (k >= 1 && k < p.K) {
+                    const int nv = norb - p.na_el;
+                    const int qi = (k - 1) / nv, pi = (k - 1) % nv;
+                    uint64_t m = sa;
+                    for (int i = 0; i < qi; ++i) m &= m - 1;
+                    const int q = __ffsll((long long)m) - 1;
+                    uint64_t v = ~sa & (((uint64_t)1 << norb) - 1);
+                    for (int i = 0; i < pi; ++i) v &= v - 1;
+                    const int pp = __ffsll((long long)v) - 1;
+                    const uint64_t rem = sa ^ ((uint64_t)1 << q);
+                    J = (int)string_rank(rem | ((uint64_t)1 << pp));
+                    sg = ((pop_below(sa, q) + pop_below(rem, pp)) & 1) ? -1.0 : 1.0;
+                    off = pair_sym(pp, q) * npair;
+                }
+                sJ[kb * KP + k] = J;
+                sOff[kb * KP + k] = off;
+                sSign[kb * KP + k] = sg;
+            }
+            for (int rs = stid; rs < p.grows; rs += kWsHalf) {  // A(rs, 0) = sum over occupied q of V'(qq, rs)
+                double sum = 0.0;
+                if (rs + p.m0 < npair)
+                    for (uint64_t m = sa; m; m &= m - 1) {
+                        const int q = __ffsll((long long)m) - 1;
+                        sum += p.Vp[(size_t)pair_sym(q, q) * npair + rs + p.m0];
+                    }
+                sOcc[kb * p.grows + rs] = sum;
+            }
+        };
         if (p.tma) {
             if (stid == 0) {
                 // D stages: one tx-counted arrival (bulk copies) or one deferred arrival per loader
@@ -706,36 +745,17 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
             uint32_t phD = 0, phL = 0;
             const bool prod = (stid >> 5) == 0;
             const int plane = stid & 31;
-            for (int64_t ia = p.row_lo + blockIdx.x; ia < p.row_hi; ia += gridDim.x) {
-                bar_sync(0, kWsThreads);  // row start: the MMA warps are done with the previous K-list
-                const uint64_t sa = string_unrank((uint64_t)ia, p.na_el, norb);
-                for (int k = stid; k < KP; k += kWsHalf) {  // K-list (as below)
-                    int J = (int)ia, pr = -2;
-                    double sg = 0.0;
-                    if (k == 0) {
-                        pr = -1;
-                        sg = 1.0;
-                    } else if (k < p.K) {
-                        const int nv = norb - p.na_el;
-                        const int qi = (k - 1) / nv, pi = (k - 1) % nv;
-                        uint64_t m = sa;
-                        for (int i = 0; i < qi; ++i) m &= m - 1;
-                        const int q = __ffsll((long long)m) - 1;
-                        uint64_t v = ~sa & (((uint64_t)1 << norb) - 1);
-                        for (int i = 0; i < pi; ++i) v &= v - 1;
-                        const int pp = __ffsll((long long)v) - 1;
-                        const uint64_t rem = sa ^ ((uint64_t)1 << q);
-                        J = (int)string_rank(rem | ((uint64_t)1 << pp));
-                        sg = ((pop_below(sa, q) + pop_below(rem, pp)) & 1) ? -1.0 : 1.0;
-                        pr = pair_sym(pp, q);
-                    }
-                    sJ[k] = J;
-                    sPair[k] = pr;
-                    sSign[k] = sg;
+            // the K-list of a row is built one row ahead (double buffered): the row-start barrier
+            // publishes it, so neither the MMA warps' A fragments nor the first gathers wait for it
+            int kb = 0;
+            if (p.row_lo + blockIdx.x < p.row_hi) build_klist(p.row_lo + blockIdx.x, 0);
+            for (int64_t ia = p.row_lo + blockIdx.x; ia < p.row_hi; ia += gridDim.x, kb ^= 1) {
+                bar_sync(0, kWsThreads);  // row start: K-list kb published; everyone is done with buffer kb ^ 1
+                const int* sJ_row = sJ + kb * KP;
+                if (p.dbg & 16) {  // timing experiment: the MMA warps free-run
+                    if (ia + gridDim.x < p.row_hi) build_klist(ia + gridDim.x, kb ^ 1);
+                    continue;
                 }
-                bar_sync(BAR_SINT, kWsHalf);  // sJ visible to the producer warp; previous row's lists read
-                bar_arrive(BAR_KLIST, kWsThreads);
-                if (p.dbg & 16) continue;  // timing experiment: the MMA warps free-run
                 const bool d_bulk = p.tma >= 2;
                 auto gather_d = [&](int stage, int T) {  // tma == 1: D rows by cp.async, all loader threads
                     if (p.dbg & 4) {
@@ -747,7 +767,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                     double* dst = Ds + stage * KP * DSTRIDE;
                     for (int c = stid; c < KP * (NT / 2); c += kWsHalf) {
                         const int k = c / (NT / 2), part = c % (NT / 2);
-                        cp_async16(dst + k * DSTRIDE + part * 2, xs + (int64_t)sJ[k] * p.ld + (int64_t)jt * NT + part * 2);
+                        cp_async16(dst + k * DSTRIDE + part * 2, xs + (int64_t)sJ_row[k] * p.ld + (int64_t)jt * NT + part * 2);
                     }
                     cp_async_commit();
                     if (p.dc) cp_async_mbar_arrive_noinc(mbD + stage);  // fires when this thread's rows landed
@@ -764,7 +784,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                     __syncwarp();
                     double* dst = Ds + stage * KP * DSTRIDE;
                     for (int k = plane; k < KP; k += 32)
-                        bulk_g2s(dst + k * DSTRIDE, xs + (int64_t)sJ[k] * p.ld + (int64_t)jt * NT, NT * 8, mbD + stage);
+                        bulk_g2s(dst + k * DSTRIDE, xs + (int64_t)sJ_row[k] * p.ld + (int64_t)jt * NT, NT * 8, mbD + stage);
                 };
                 auto issue_l = [&](int stage, int T) {
                     const int jt = T % ntiles;
@@ -788,6 +808,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                     }
                     for (int jt = 0; jt < 2 && jt < ntot; ++jt)
                         if (prod) issue_l(jt, jt);
+                    if (ia + gridDim.x < p.row_hi) build_klist(ia + gridDim.x, kb ^ 1);  // next row's K-list
                     int sd = 0;  // D stage of tile it
                     for (int it = 0; it < ntot; ++it) {
                         const int b = it & 1, lt = it % ntiles;
@@ -832,6 +853,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                     }
                     if (!d_bulk) gather_d(jt, jt);
                 }
+                if (ia + gridDim.x < p.row_hi) build_klist(ia + gridDim.x, kb ^ 1);  // next row's K-list
                 if (!d_bulk) {
                     cp_async_wait<0>();
                     bar_sync(BAR_SINT, kWsHalf);
@@ -888,31 +910,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
         }
         for (int64_t ia = p.row_lo + blockIdx.x; ia < p.row_hi; ia += gridDim.x) {
             bar_sync(0, kWsThreads);  // row start: the MMA warps are done with the previous K-list
-            const uint64_t sa = string_unrank((uint64_t)ia, p.na_el, norb);
-            for (int k = stid; k < KP; k += kWsHalf) {  // K-list (as in k_sigma_ab)
-                int J = (int)ia, pr = -2;
-                double sg = 0.0;
-                if (k == 0) {
-                    pr = -1;
-                    sg = 1.0;
-                } else if (k < p.K) {
-                    const int nv = norb - p.na_el;
-                    const int qi = (k - 1) / nv, pi = (k - 1) % nv;
-                    uint64_t m = sa;
-                    for (int i = 0; i < qi; ++i) m &= m - 1;
-                    const int q = __ffsll((long long)m) - 1;
-                    uint64_t v = ~sa & (((uint64_t)1 << norb) - 1);
-                    for (int i = 0; i < pi; ++i) v &= v - 1;
-                    const int pp = __ffsll((long long)v) - 1;
-                    const uint64_t rem = sa ^ ((uint64_t)1 << q);
-                    J = (int)string_rank(rem | ((uint64_t)1 << pp));
-                    sg = ((pop_below(sa, q) + pop_below(rem, pp)) & 1) ? -1.0 : 1.0;
-                    pr = pair_sym(pp, q);
-                }
-                sJ[k] = J;
-                sPair[k] = pr;
-                sSign[k] = sg;
-            }
+            build_klist(ia, 0);
             if (!p.red)
                 for (int64_t c = stid; c < p.ld; c += kWsHalf) srow[c] = 0.0;
             bar_sync(BAR_SINT, kWsHalf);       // sJ visible to every loader
@@ -1144,7 +1142,7 @@ AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int
         const int64_t ntiles = ld / nt;
         pl.smem = 64 + (size_t)(pl.red ? 0 : ld) * 8 + (size_t)STAGES * KP * (nt + 4) * 8 + (size_t)KP * 8 * 8 +
                   (size_t)STAGES * pl.npad * (nt + 8) * 8 + (size_t)STAGES * (pl.maxT * 4 + pl.maxE * 2) +
-                  (size_t)(ntiles + 1) * 8 + (size_t)KP * 16 + 16;
+                  (size_t)(ntiles + 1) * 8 + (size_t)KP * 32 + (size_t)(pl.npad + 8) * 16 + 16;
     };
     const char* nt_env = getenv("SBG_AB_NT");
     const int nt_force = nt_env ? atoi(nt_env) : 0;
@@ -1258,10 +1256,10 @@ void build_ab_red_list(const AbPlan& pl, const std::vector<uint16_t>& codes, std
                 if (pl.xs == 2 && rs >= 16 * pl.mb16)
                     items.push_back({(uint32_t)(code & 0x7FFF), (uint32_t)(((rs + 8) * GSTRIDE + c) | (code & 0x8000))});
             }
+        tile_ent[jt] = (uint32_t)ent.size();
         // kept in G order (rs-major): a warp's shared-memory reads of G are then near-contiguous;
         // target-sorting them instead (a warp reducing into neighbouring y elements) measured
         // slightly slower — the row's targets are sparse within a tile either way
-        tile_ent[jt] = (uint32_t)ent.size();
         for (auto& it : items) ent.push_back((it.first << 16) | it.second);
         while (ent.size() % 4) ent.push_back(0xFFFFFFFFu);
         if ((int64_t)(ent.size() - tile_ent[jt]) * 2 > pl.maxE) throw InvalidArgument("sigma_ab: red list overflow");
