@@ -23,6 +23,7 @@
 // warp-specialized kernel with SBG_AB_WS=1).
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 #include "common.cuh"
 #include "kernels.cuh"
@@ -55,7 +56,7 @@ struct AbParams {
     int accumulate;
     int dbg;  // profiling experiments only: 1 = skip scatter, 2 = skip MMA, 4 = skip gathers (ws kernel)
     int red;  // k_sigma_ab_ws: 1 = scatter by red.global.add into y (no sigma row in shared memory)
-    const uint32_t* ent32;      // red mode, per tile: target << 16 | negative << 15 | G offset
+    const uint32_t* ent32;      // red mode, per tile: [npos][target << 16 | G byte offset ...] (build_ab_red_list)
     const uint32_t* tile_ent32; // [ntiles+1] offsets into ent32 (multiples of 4)
     int m0;                     // first pair row of this pass (pair-row blocks when npair > 136)
     int add_ecore;              // this pass adds e_core * x
@@ -296,6 +297,14 @@ __device__ __forceinline__ void bar_arrive(int id, int n) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 constexpr int kWsThreads = 512, kWsHalf = 256;
+// The SBG_AB_DEBUG timing experiments (skip the scatter / the DMMAs / the gathers / every hand-off)
+// are compiled into k_sigma_ab_ws only with -DSBG_AB_DEBUG_SWITCHES (tools/ab_variant.sh): every
+// instruction in the DMMA warps' tile loop costs tensor-pipe time.
+#ifdef SBG_AB_DEBUG_SWITCHES
+#define SBG_DBG(bit) (p.dbg & (bit))
+#else
+#define SBG_DBG(bit) (false)
+#endif
 // register split between the MMA and the loader/scatter warpgroups (sum 256: 256 threads each)
 #ifndef SBG_WS_MREG
 #define SBG_WS_MREG 200
@@ -376,7 +385,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
         // tile it of a row: wait for D (stage returned), and the hand-back of G buffer b
         auto wait_d = [&](int it, int& sd) -> const double* {
             const int b = it & 1;
-            if (p.dbg & 16) return Ds + b * KP * DSTRIDE;  // timing experiment: no hand-offs at all
+            if SBG_DBG(16) return Ds + b * KP * DSTRIDE;  // timing experiment: no hand-offs at all
             if (p.dc) {
                 mbar_wait_parity(mbD + sd, (phDm >> sd) & 1u);
                 phDm ^= 1u << sd;
@@ -390,14 +399,14 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
         };
         auto wait_g = [&](int it) {  // decoupled: just before the accumulators are staged
             const int b = it & 1;
-            if (p.dbg & 16) return;
+            if SBG_DBG(16) return;
             if (p.dc && it >= 2) {
                 mbar_wait_parity(mbE + b, (phEm >> b) & 1u);
                 phEm ^= 1u << b;
             }
         };
         auto drain_g = [&](int ntot) {  // row end: the last two tiles have been scattered
-            if (p.dbg & 16) return;
+            if SBG_DBG(16) return;
             for (int it = ntot - 2 < 0 ? 0 : ntot - 2; it < ntot; ++it) {
                 const int b = it & 1;
                 if (p.dc) {
@@ -447,7 +456,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                     for (int it = 0; it < ntot; ++it) {
                         const int b = it & 1;
                         const double* D = wait_d(it, sd);
-                        if (!(p.dbg & 2) && nbh < NBT) {
+                        if (!SBG_DBG(2) && nbh < NBT) {
                             double* G = Gs + b * p.grows * GSTRIDE;
                             const double* D1 = D + K0 * DSTRIDE + g + nbh * 8;
                             double acc[MH][4];
@@ -480,7 +489,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                         } else {
                             wait_g(it);
                         }
-                        if (!(p.dbg & 16)) bar_arrive(BAR_FULL + b, kWsThreads);
+                        if (!SBG_DBG(16)) bar_arrive(BAR_FULL + b, kWsThreads);
                     }
                     drain_g(ntot);
                     continue;  // next row
@@ -513,82 +522,97 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                 }
                 const double a00 = (K0E && main_ok) ? aocc(r0) : 0.0, a01 = (K0E && main_ok) ? aocc(r0 + 8) : 0.0;
                 const double ae0 = (XS == 2 && K0E && w < 4) ? aocc(re + g) : 0.0;
-                const int gx = (re + (w >= 4 ? 8 : 0) + g) * GSTRIDE + c01 + 4 * t + (xodd ? 1 : 0);  // extra partials
-                int sd = 0;
-                for (int it = 0; it < ntot; ++it) {
-                    const int b = it & 1;
-                    const double* D = wait_d(it, sd);
-                    if (!(p.dbg & 2) && (main_ok || XS == 2)) {
-                        double* G = Gs + b * p.grows * GSTRIDE;
-                        const double* pLo = D + (K0 + 4 * koff + t) * DSTRIDE + 2 * g;
-                        const double* pHi = koff ? pLo - 4 * KS * DSTRIDE : pLo;
-                        double acc[4][4];
-                        double acx[2] = {0.0, 0.0};
+                // lane-dependent byte offsets, fixed for the kernel: pinned in registers (the opaque asm
+                // stops the compiler from rebuilding them from the thread index in every tile)
+                int oB01 = ((K0 + 4 * koff + t) * DSTRIDE + 2 * g + c01) * 8;  // B fragments, blocks 0,1, iterations < KH
+                int oB23 = oB01 + (c23 - c01) * 8;                             // ... blocks 2,3
+                int oHi = koff ? -4 * KS * DSTRIDE * 8 : 0;                    // ... iterations >= KH (rotated k order)
+                int oG01 = (r0 * GSTRIDE + 4 * t + c01) * 8;                   // staged accumulators, row g of the block
+                int oG23 = oG01 + (c23 - c01) * 8;
+                int oX = ((re + (w >= 4 ? 8 : 0) + g) * GSTRIDE + c01 + 4 * t + (xodd ? 1 : 0)) * 8;  // extra partials
+                int oC01 = (c01 + 4 * t) * 8, oC23 = (c23 + 4 * t) * 8;        // the row's own tile (k = 0 term)
+                asm volatile("" : "+r"(oB01), "+r"(oB23), "+r"(oHi), "+r"(oG01), "+r"(oG23), "+r"(oX), "+r"(oC01), "+r"(oC23));
+                // the tile loop, compiled once per parity of the extra block (a sub-partition's two DMMA
+                // warps share it): picking the odd or even block's B fragment costs no select
+                auto tile_loop = [&](auto xodd_c) {
+                    constexpr bool XODD = decltype(xodd_c)::value;
+                    int sd = 0;
+                    for (int it = 0; it < ntot; ++it) {
+                        const int b = it & 1;
+                        const char* D = reinterpret_cast<const char*>(wait_d(it, sd));
+                        if (!SBG_DBG(2) && (main_ok || XS == 2)) {
+                            char* G = reinterpret_cast<char*>(Gs + b * p.grows * GSTRIDE);
+                            const char* pLo01 = D + oB01;
+                            const char* pLo23 = D + oB23;
+                            const char* pHi01 = pLo01 + oHi;
+                            const char* pHi23 = pLo23 + oHi;
+                            double acc[4][4];
+                            double acx[2] = {0.0, 0.0};
 #pragma unroll
-                        for (int nb = 0; nb < 4; ++nb)
+                            for (int nb = 0; nb < 4; ++nb)
 #pragma unroll
-                            for (int e = 0; e < 4; ++e) acc[nb][e] = 0.0;
-                        double2 q[2][2];  // B fragments of local blocks (0,1) and (2,3), one k-step ahead
-                        q[0][0] = *reinterpret_cast<const double2*>(pLo + c01);
-                        q[0][1] = *reinterpret_cast<const double2*>(pLo + c23);
+                                for (int e = 0; e < 4; ++e) acc[nb][e] = 0.0;
+                            double2 q[2][2];  // B fragments of local blocks (0,1) and (2,3), one k-step ahead
+                            q[0][0] = *reinterpret_cast<const double2*>(pLo01);
+                            q[0][1] = *reinterpret_cast<const double2*>(pLo23);
 #pragma unroll
-                        for (int i = 0; i < KS; ++i) {
-                            const int cur = i & 1;
-                            if (i == KS - 1) wait_g(it);  // G buffer b is written from here on
-                            if (i + 1 < KS) {
-                                const double* pn = ((i + 1 < KH) ? pLo : pHi) + (i + 1) * 4 * DSTRIDE;
-                                q[cur ^ 1][0] = *reinterpret_cast<const double2*>(pn + c01);
-                                q[cur ^ 1][1] = *reinterpret_cast<const double2*>(pn + c23);
+                            for (int i = 0; i < KS; ++i) {
+                                const int cur = i & 1;
+                                if (i == KS - 1) wait_g(it);  // G buffer b is written from here on
+                                if (i + 1 < KS) {
+                                    constexpr int STEP = 4 * DSTRIDE * 8;
+                                    q[cur ^ 1][0] = *reinterpret_cast<const double2*>(((i + 1 < KH) ? pLo01 : pHi01) + (i + 1) * STEP);
+                                    q[cur ^ 1][1] = *reinterpret_cast<const double2*>(((i + 1 < KH) ? pLo23 : pHi23) + (i + 1) * STEP);
+                                }
+                                dmma_16x8x4(acc[0], a0[i], a1[i], q[cur][0].x);
+                                dmma_16x8x4(acc[1], a0[i], a1[i], q[cur][0].y);
+                                dmma_16x8x4(acc[2], a0[i], a1[i], q[cur][1].x);
+                                dmma_16x8x4(acc[3], a0[i], a1[i], q[cur][1].y);
+                                if constexpr (XS == 2) {
+                                    if (i < KH) dmma_8x8x4(acx, aer[i], XODD ? q[cur][0].y : q[cur][0].x);
+                                }
                             }
-                            dmma_16x8x4(acc[0], a0[i], a1[i], q[cur][0].x);
-                            dmma_16x8x4(acc[1], a0[i], a1[i], q[cur][0].y);
-                            dmma_16x8x4(acc[2], a0[i], a1[i], q[cur][1].x);
-                            dmma_16x8x4(acc[3], a0[i], a1[i], q[cur][1].y);
+                            // epilogue: column of acc[L][e] = (L < 2 ? c01 : c23) + 4 t + 2 (e & 1) + (L & 1),
+                            // rows g (e < 2) and g + 8; the k = 0 rank-1 term (K0E) first
+                            if constexpr (K0E) {
+                                const double2 va0 = *reinterpret_cast<const double2*>(D + oC01), va1 = *reinterpret_cast<const double2*>(D + oC01 + 16);
+                                const double2 vb0 = *reinterpret_cast<const double2*>(D + oC23), vb1 = *reinterpret_cast<const double2*>(D + oC23 + 16);
+                                acc[0][0] = fma(a00, va0.x, acc[0][0]); acc[1][0] = fma(a00, va0.y, acc[1][0]);
+                                acc[0][1] = fma(a00, va1.x, acc[0][1]); acc[1][1] = fma(a00, va1.y, acc[1][1]);
+                                acc[0][2] = fma(a01, va0.x, acc[0][2]); acc[1][2] = fma(a01, va0.y, acc[1][2]);
+                                acc[0][3] = fma(a01, va1.x, acc[0][3]); acc[1][3] = fma(a01, va1.y, acc[1][3]);
+                                acc[2][0] = fma(a00, vb0.x, acc[2][0]); acc[3][0] = fma(a00, vb0.y, acc[3][0]);
+                                acc[2][1] = fma(a00, vb1.x, acc[2][1]); acc[3][1] = fma(a00, vb1.y, acc[3][1]);
+                                acc[2][2] = fma(a01, vb0.x, acc[2][2]); acc[3][2] = fma(a01, vb0.y, acc[3][2]);
+                                acc[2][3] = fma(a01, vb1.x, acc[2][3]); acc[3][3] = fma(a01, vb1.y, acc[3][3]);
+                                if constexpr (XS == 2) {  // warps 0-3 carry the extra rows' k = 0 term
+                                    acx[0] = fma(ae0, XODD ? va0.y : va0.x, acx[0]);
+                                    acx[1] = fma(ae0, XODD ? va1.y : va1.x, acx[1]);
+                                }
+                            }
+                            if (main_ok) {
+                                constexpr int ROW8 = 8 * GSTRIDE * 8;
+                                *reinterpret_cast<double2*>(G + oG01) = make_double2(acc[0][0], acc[1][0]);
+                                *reinterpret_cast<double2*>(G + oG01 + 16) = make_double2(acc[0][1], acc[1][1]);
+                                *reinterpret_cast<double2*>(G + oG01 + ROW8) = make_double2(acc[0][2], acc[1][2]);
+                                *reinterpret_cast<double2*>(G + oG01 + ROW8 + 16) = make_double2(acc[0][3], acc[1][3]);
+                                *reinterpret_cast<double2*>(G + oG23) = make_double2(acc[2][0], acc[3][0]);
+                                *reinterpret_cast<double2*>(G + oG23 + 16) = make_double2(acc[2][1], acc[3][1]);
+                                *reinterpret_cast<double2*>(G + oG23 + ROW8) = make_double2(acc[2][2], acc[3][2]);
+                                *reinterpret_cast<double2*>(G + oG23 + ROW8 + 16) = make_double2(acc[2][3], acc[3][3]);
+                            }
                             if constexpr (XS == 2) {
-                                if (i < KH) dmma_8x8x4(acx, aer[i], xodd ? q[cur][0].y : q[cur][0].x);
+                                *reinterpret_cast<double*>(G + oX) = acx[0];
+                                *reinterpret_cast<double*>(G + oX + 16) = acx[1];
                             }
+                        } else {
+                            wait_g(it);
                         }
-                        // epilogue: column of acc[L][e] = (L < 2 ? c01 : c23) + 4 t + 2 (e & 1) + (L & 1),
-                        // rows g (e < 2) and g + 8; the k = 0 rank-1 term (K0E) first
-                        const int ca = c01 + 4 * t, cb = c23 + 4 * t;
-                        if constexpr (K0E) {
-                            const double2 va0 = *reinterpret_cast<const double2*>(D + ca), va1 = *reinterpret_cast<const double2*>(D + ca + 2);
-                            const double2 vb0 = *reinterpret_cast<const double2*>(D + cb), vb1 = *reinterpret_cast<const double2*>(D + cb + 2);
-                            acc[0][0] = fma(a00, va0.x, acc[0][0]); acc[1][0] = fma(a00, va0.y, acc[1][0]);
-                            acc[0][1] = fma(a00, va1.x, acc[0][1]); acc[1][1] = fma(a00, va1.y, acc[1][1]);
-                            acc[0][2] = fma(a01, va0.x, acc[0][2]); acc[1][2] = fma(a01, va0.y, acc[1][2]);
-                            acc[0][3] = fma(a01, va1.x, acc[0][3]); acc[1][3] = fma(a01, va1.y, acc[1][3]);
-                            acc[2][0] = fma(a00, vb0.x, acc[2][0]); acc[3][0] = fma(a00, vb0.y, acc[3][0]);
-                            acc[2][1] = fma(a00, vb1.x, acc[2][1]); acc[3][1] = fma(a00, vb1.y, acc[3][1]);
-                            acc[2][2] = fma(a01, vb0.x, acc[2][2]); acc[3][2] = fma(a01, vb0.y, acc[3][2]);
-                            acc[2][3] = fma(a01, vb1.x, acc[2][3]); acc[3][3] = fma(a01, vb1.y, acc[3][3]);
-                            if constexpr (XS == 2) {  // warps 0-3 carry the extra rows' k = 0 term
-                                const double x0 = xodd ? va0.y : va0.x, x1 = xodd ? va1.y : va1.x;
-                                acx[0] = fma(ae0, x0, acx[0]);
-                                acx[1] = fma(ae0, x1, acx[1]);
-                            }
-                        }
-                        if (main_ok) {
-                            double* g0 = G + r0 * GSTRIDE;
-                            double* g1 = g0 + 8 * GSTRIDE;
-                            *reinterpret_cast<double2*>(g0 + ca) = make_double2(acc[0][0], acc[1][0]);
-                            *reinterpret_cast<double2*>(g0 + ca + 2) = make_double2(acc[0][1], acc[1][1]);
-                            *reinterpret_cast<double2*>(g1 + ca) = make_double2(acc[0][2], acc[1][2]);
-                            *reinterpret_cast<double2*>(g1 + ca + 2) = make_double2(acc[0][3], acc[1][3]);
-                            *reinterpret_cast<double2*>(g0 + cb) = make_double2(acc[2][0], acc[3][0]);
-                            *reinterpret_cast<double2*>(g0 + cb + 2) = make_double2(acc[2][1], acc[3][1]);
-                            *reinterpret_cast<double2*>(g1 + cb) = make_double2(acc[2][2], acc[3][2]);
-                            *reinterpret_cast<double2*>(g1 + cb + 2) = make_double2(acc[2][3], acc[3][3]);
-                        }
-                        if constexpr (XS == 2) {
-                            G[gx] = acx[0];
-                            G[gx + 2] = acx[1];
-                        }
-                    } else {
-                        wait_g(it);
+                        if (!SBG_DBG(16)) bar_arrive(BAR_FULL + b, kWsThreads);
                     }
-                    if (!(p.dbg & 16)) bar_arrive(BAR_FULL + b, kWsThreads);
-                }
+                };
+                if (XS == 2 && xodd) tile_loop(std::true_type{});
+                else tile_loop(std::false_type{});
                 drain_g(ntot);
                 continue;  // next row
             }
@@ -614,7 +638,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
             for (int it = 0; it < ntot; ++it) {
                 const int b = it & 1;
                 const double* D = wait_d(it, sd);
-                if (!(p.dbg & 2) && main_ok) {
+                if (!SBG_DBG(2) && main_ok) {
                     double* G = Gs + b * p.grows * GSTRIDE;
                     double acc[NBT][4];
                     double ace0[2] = {0.0, 0.0}, ace1[2] = {0.0, 0.0};
@@ -683,7 +707,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                 } else {
                     wait_g(it);
                 }
-                if (!(p.dbg & 16)) bar_arrive(BAR_FULL + b, kWsThreads);
+                if (!SBG_DBG(16)) bar_arrive(BAR_FULL + b, kWsThreads);
             }
             drain_g(ntot);
         }
@@ -729,22 +753,55 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                 sOcc[kb * p.grows + rs] = sum;
             }
         };
+        // One reduction per list entry. Tile blob (build_ab_red_list): [npos][entries], the first npos
+        // entries add +G, the rest add -G (the sign is loop invariant: no per-entry sign arithmetic);
+        // entry = target column << 16 | byte offset into the G tile; the 16-byte padding at the end
+        // points at a G padding column that holds 0.0, so it needs no test either.
+        auto scatter_tile = [&](const double* G, const uint32_t* blob, uint32_t nwords, double* yrow) {
+            if (nwords == 0) return;
+            const uint32_t npos = blob[0], n = nwords - 1;
+            const uint32_t* l32 = blob + 1;
+            const char* Gb = reinterpret_cast<const char*>(G);
+#pragma unroll RED_UNROLL
+            for (uint32_t i = stid; i < npos; i += kWsHalf) {
+                const uint32_t en = l32[i];
+                red_add_f64(yrow + (en >> 16), *reinterpret_cast<const double*>(Gb + (en & 0xFFFFu)));
+            }
+#pragma unroll RED_UNROLL
+            for (uint32_t i = npos + stid; i < n; i += kWsHalf) {
+                const uint32_t en = l32[i];
+                const double v = *reinterpret_cast<const double*>(Gb + (en & 0xFFFFu));
+                red_add_f64(yrow + (en >> 16), __hiloint2double(__double2hiint(v) ^ 0x80000000, __double2loint(v)));
+            }
+        };
+        if (p.red)  // the G padding columns the lists' padding entries read (never written by the MMA warps)
+            for (int i = stid; i < STAGES * p.grows; i += kWsHalf) Gs[i * GSTRIDE + NT] = 0.0;
         if (p.tma) {
             if (stid == 0) {
-                // D stages: one tx-counted arrival (bulk copies) or one deferred arrival per loader
-                // thread (cp.async, decoupled mode); lists: tx-counted; G hand-back: one per loader warp
-                for (int i = 0; i < 3; ++i) mbar_init(mbD + i, (p.dc && p.tma < 2) ? kWsHalf : 1);
+                // D stages: one deferred arrival per loader thread (its cp.async completions); lists:
+                // tx-counted bulk copy; G hand-back: one arrival per loader warp
+                for (int i = 0; i < 3; ++i) mbar_init(mbD + i, kWsHalf);
                 for (int i = 0; i < 2; ++i) mbar_init(mbL + i, 1);
                 for (int i = 0; i < 2; ++i) mbar_init(mbE + i, kWsHalf / 32);
                 mbar_init_fence();
             }
-            // bulk-copy pipeline (red mode): warp 8 issues the tile's reduction list (one copy) and,
-            // with tma >= 2, every D row (one 256-byte copy per linked alpha row) on the TMA engine;
-            // D(it) and lists(it) complete on mbD[stage] / mbL[it & 1], whose phase parity every
-            // loader thread tracks in phD / phL (one completion per tile of that stage)
-            uint32_t phD = 0, phL = 0;
+            // Decoupled pipeline (reduction mode): all loader threads gather the D rows with cp.async
+            // and announce them on mbD through their own completions; warp 8 brings the tile's
+            // reduction list with one bulk copy (TMA engine) onto mbL; the DMMA warps hand G back
+            // through mbE. This loop only meets the DMMA warps at FULL (G(it) staged, D stage free).
+            uint32_t phL = 0;
             const bool prod = (stid >> 5) == 0;
             const int plane = stid & 31;
+            // this thread's 16-byte chunks of a D tile (row k, column pair `part`): shared offsets are
+            // fixed, global offsets (16-byte units, from the K-list) change per row — a tile's gathers
+            // cost one add and one cp.async per chunk
+            constexpr int NCH = 5;  // >= ceil(KP * (NT / 2) / 256), KP <= 69
+            uint32_t soff[NCH], goff[NCH];
+#pragma unroll
+            for (int i = 0; i < NCH; ++i) {
+                const int c = stid + i * kWsHalf;
+                soff[i] = c < KP * (NT / 2) ? (uint32_t)((c / (NT / 2)) * DSTRIDE + (c % (NT / 2)) * 2) : 0xFFFFFFFFu;
+            }
             // the K-list of a row is built one row ahead (double buffered): the row-start barrier
             // publishes it, so neither the MMA warps' A fragments nor the first gathers wait for it
             int kb = 0;
@@ -752,158 +809,71 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
             for (int64_t ia = p.row_lo + blockIdx.x; ia < p.row_hi; ia += gridDim.x, kb ^= 1) {
                 bar_sync(0, kWsThreads);  // row start: K-list kb published; everyone is done with buffer kb ^ 1
                 const int* sJ_row = sJ + kb * KP;
-                if (p.dbg & 16) {  // timing experiment: the MMA warps free-run
+                if SBG_DBG(16) {  // timing experiment: the MMA warps free-run
                     if (ia + gridDim.x < p.row_hi) build_klist(ia + gridDim.x, kb ^ 1);
                     continue;
                 }
-                const bool d_bulk = p.tma >= 2;
-                auto gather_d = [&](int stage, int T) {  // tma == 1: D rows by cp.async, all loader threads
-                    if (p.dbg & 4) {
-                        if (p.dc) cp_async_mbar_arrive_noinc(mbD + stage);
-                        return;
+#pragma unroll
+                for (int i = 0; i < NCH; ++i) {
+                    const int c = stid + i * kWsHalf;
+                    if (soff[i] != 0xFFFFFFFFu)
+                        goff[i] = (uint32_t)(((int64_t)sJ_row[c / (NT / 2)] * p.ld) >> 1) + (uint32_t)(c % (NT / 2));
+                }
+                // tiles are gathered / listed in sequence order: running (tile, vector) counters
+                int g_t = 0, g_v = 0, l_t = 0;
+                auto gather_next = [&](int stage) {
+                    if (!SBG_DBG(4)) {
+                        const double* xs = p.xv[g_v] + (int64_t)g_t * NT;
+                        double* dst = Ds + stage * KP * DSTRIDE;
+#pragma unroll
+                        for (int i = 0; i < NCH; ++i)
+                            if (soff[i] != 0xFFFFFFFFu) cp_async16(dst + soff[i], xs + ((int64_t)goff[i] << 1));
+                        if (++g_t == ntiles) {
+                            g_t = 0;
+                            ++g_v;
+                        }
                     }
-                    const int jt = T % ntiles;
-                    const double* xs = p.xv[T / ntiles];
-                    double* dst = Ds + stage * KP * DSTRIDE;
-                    for (int c = stid; c < KP * (NT / 2); c += kWsHalf) {
-                        const int k = c / (NT / 2), part = c % (NT / 2);
-                        cp_async16(dst + k * DSTRIDE + part * 2, xs + (int64_t)sJ_row[k] * p.ld + (int64_t)jt * NT + part * 2);
-                    }
-                    cp_async_commit();
-                    if (p.dc) cp_async_mbar_arrive_noinc(mbD + stage);  // fires when this thread's rows landed
+                    cp_async_mbar_arrive_noinc(mbD + stage);  // fires when this thread's chunks have landed
                 };
-                auto issue_d = [&](int stage, int T) {  // producer warp only
-                    const int jt = T % ntiles;
-                    const double* xs = p.xv[T / ntiles];
-                    if (p.dbg & 4) {
-                        if (plane == 0) mbar_arrive_expect_tx(mbD + stage, 0);
-                        return;
-                    }
-                    fence_proxy_async_smem();  // the MMA warps' reads of this stage precede the refill
-                    if (plane == 0) mbar_arrive_expect_tx(mbD + stage, (uint32_t)(KP * NT * 8));
-                    __syncwarp();
-                    double* dst = Ds + stage * KP * DSTRIDE;
-                    for (int k = plane; k < KP; k += 32)
-                        bulk_g2s(dst + k * DSTRIDE, xs + (int64_t)sJ_row[k] * p.ld + (int64_t)jt * NT, NT * 8, mbD + stage);
-                };
-                auto issue_l = [&](int stage, int T) {
-                    const int jt = T % ntiles;
+                auto list_next = [&](int stage) {  // producer warp
                     if (plane == 0) {
-                        const uint32_t e0 = sTE[jt], bytes = (sTE[jt + 1] - e0) * 4;
+                        const uint32_t e0 = sTE[l_t], bytes = (sTE[l_t + 1] - e0) * 4;
                         fence_proxy_async_smem();
                         mbar_arrive_expect_tx(mbL + stage, bytes);
                         if (bytes) bulk_g2s(Le + stage * p.maxE, p.ent32 + e0, bytes, mbL + stage);
                     }
+                    if (++l_t == ntiles) l_t = 0;
                 };
-                if (p.dc) {
-                    // decoupled hand-offs: the MMA warps take D(it) from mbD and hand G back through
-                    // mbE, so this loop never waits for its own gathers and only meets the MMA warps
-                    // at FULL (G(it) staged, D stage of tile it free)
-                    for (int jt = 0; jt < p.dc && jt < ntot; ++jt) {
-                        if (d_bulk) {
-                            if (prod) issue_d(jt, jt);
-                        } else {
-                            gather_d(jt, jt);
-                        }
-                    }
-                    for (int jt = 0; jt < 2 && jt < ntot; ++jt)
-                        if (prod) issue_l(jt, jt);
-                    if (ia + gridDim.x < p.row_hi) build_klist(ia + gridDim.x, kb ^ 1);  // next row's K-list
-                    int sd = 0;  // D stage of tile it
-                    for (int it = 0; it < ntot; ++it) {
-                        const int b = it & 1, lt = it % ntiles;
-                        double* yrow = p.yv[it / ntiles] + (ia - p.row_lo) * p.ld;
-                        bar_sync(BAR_FULL + b, kWsThreads);   // G(it) staged; D stage sd free
-                        if (it + p.dc < ntot) {
-                            if (!d_bulk) gather_d(sd, it + p.dc);
-                            else if (prod) issue_d(sd, it + p.dc);
-                        }
-                        sd = (sd + 1 == p.dc) ? 0 : sd + 1;
-                        mbar_wait_parity(mbL + b, (phL >> b) & 1u);  // lists(it) landed
-                        phL ^= 1u << b;
-                        if (!(p.dbg & 1)) {
-                            const double* G = Gs + b * p.grows * GSTRIDE;
-                            const uint32_t* l32 = reinterpret_cast<const uint32_t*>(Le + b * p.maxE);
-                            const uint32_t n = sTE[lt + 1] - sTE[lt];
-#pragma unroll RED_UNROLL
-                            for (uint32_t i = stid; i < n; i += kWsHalf) {
-                                const uint32_t en = l32[i];
-                                if (en == 0xFFFFFFFFu) continue;  // 16-byte padding
-                                const long long bits = __double_as_longlong(G[en & 0x7FFFu]) ^ ((long long)(en & 0x8000u) << 48);
-                                red_add_f64(yrow + (en >> 16), __longlong_as_double(bits));
-                            }
-                        }
-                        __syncwarp();
-                        if (plane == 0) mbar_arrive(mbE + b);  // this warp is done with G(it)
-                        bar_sync(BAR_SINT, kWsHalf);           // lists stage b read by every loader
-                        if (it + 2 < ntot && prod) issue_l(b, it + 2);
-                    }
-                    if (p.e_core != 0.0 && p.add_ecore)  // e_core * x, reduced like the tiles
-                        for (int v = 0; v < p.nvec; ++v) {
-                            const double* xr = p.xv[v] + ia * p.ld;
-                            double* yrow = p.yv[v] + (ia - p.row_lo) * p.ld;
-                            for (int64_t c = stid; c < p.NB; c += kWsHalf) red_add_f64(yrow + c, p.e_core * xr[c]);
-                        }
-                    continue;  // next row
-                }
-                for (int jt = 0; jt < 2 && jt < ntot; ++jt) {
-                    if (prod) {
-                        if (d_bulk) issue_d(jt, jt);
-                        issue_l(jt, jt);
-                    }
-                    if (!d_bulk) gather_d(jt, jt);
-                }
+                for (int jt = 0; jt < p.dc && jt < ntot; ++jt) gather_next(jt);
+                for (int jt = 0; jt < 2 && jt < ntot; ++jt)
+                    if (prod) list_next(jt);
                 if (ia + gridDim.x < p.row_hi) build_klist(ia + gridDim.x, kb ^ 1);  // next row's K-list
-                if (!d_bulk) {
-                    cp_async_wait<0>();
-                    bar_sync(BAR_SINT, kWsHalf);
-                }
-                for (int jt = 0; jt < 2 && jt < ntot; ++jt) {
-                    if (d_bulk) {
-                        mbar_wait_parity(mbD + jt, (phD >> jt) & 1u);
-                        phD ^= 1u << jt;
-                    }
-                    bar_arrive(BAR_DREADY + jt, kWsThreads);
-                }
+                int sd = 0, s_t = 0, s_v = 0;  // D stage, tile and vector of the tile being scattered
+                double* yrow = p.yv[0] + (ia - p.row_lo) * p.ld;
                 for (int it = 0; it < ntot; ++it) {
-                    const int b = it & 1, lt = it % ntiles;
-                    double* yrow = p.yv[it / ntiles] + (ia - p.row_lo) * p.ld;
-                    bar_sync(BAR_FULL + b, kWsThreads);   // G(it) staged; D stage b free
-                    if (it + 2 < ntot) {
-                        if (!d_bulk) gather_d(b, it + 2);
-                        else if (prod) issue_d(b, it + 2);
-                    }
+                    const int b = it & 1;
+                    bar_sync(BAR_FULL + b, kWsThreads);   // G(it) staged; D stage sd free
+                    if (it + p.dc < ntot) gather_next(sd);
+                    sd = (sd + 1 == p.dc) ? 0 : sd + 1;
                     mbar_wait_parity(mbL + b, (phL >> b) & 1u);  // lists(it) landed
                     phL ^= 1u << b;
-                    if (!(p.dbg & 1)) {
-                        const double* G = Gs + b * p.grows * GSTRIDE;
-                        const uint32_t* l32 = reinterpret_cast<const uint32_t*>(Le + b * p.maxE);
-                        const uint32_t n = sTE[lt + 1] - sTE[lt];
-#pragma unroll RED_UNROLL
-                        for (uint32_t i = stid; i < n; i += kWsHalf) {
-                            const uint32_t en = l32[i];
-                            if (en == 0xFFFFFFFFu) continue;  // 16-byte padding
-                            const long long bits = __double_as_longlong(G[en & 0x7FFFu]) ^ ((long long)(en & 0x8000u) << 48);
-                            red_add_f64(yrow + (en >> 16), __longlong_as_double(bits));
-                        }
+                    if (!SBG_DBG(1))
+                        scatter_tile(Gs + b * p.grows * GSTRIDE, reinterpret_cast<const uint32_t*>(Le + b * p.maxE),
+                                     sTE[s_t + 1] - sTE[s_t], yrow);
+                    if (++s_t == ntiles) {
+                        s_t = 0;
+                        if (++s_v < p.nvec) yrow = p.yv[s_v] + (ia - p.row_lo) * p.ld;
                     }
-                    bar_arrive(BAR_EMPTY + b, kWsThreads);
-                    if (!d_bulk) cp_async_wait<0>();      // this thread's rows of D(it+2)
-                    bar_sync(BAR_SINT, kWsHalf);          // lists stage b read by all; (cp.async) D(it+2) landed
-                    if (it + 2 < ntot) {
-                        if (prod) issue_l(b, it + 2);
-                        if (d_bulk) {
-                            mbar_wait_parity(mbD + b, (phD >> b) & 1u);   // D(it+2) landed
-                            phD ^= 1u << b;
-                        }
-                        bar_arrive(BAR_DREADY + b, kWsThreads);
-                    }
+                    __syncwarp();
+                    if (plane == 0) mbar_arrive(mbE + b);  // this warp is done with G(it)
+                    bar_sync(BAR_SINT, kWsHalf);           // lists stage b read by every loader
+                    if (it + 2 < ntot && prod) list_next(b);
                 }
                 if (p.e_core != 0.0 && p.add_ecore)  // e_core * x, reduced like the tiles
                     for (int v = 0; v < p.nvec; ++v) {
                         const double* xr = p.xv[v] + ia * p.ld;
-                        double* yrow = p.yv[v] + (ia - p.row_lo) * p.ld;
-                        for (int64_t c = stid; c < p.NB; c += kWsHalf) red_add_f64(yrow + c, p.e_core * xr[c]);
+                        double* yr = p.yv[v] + (ia - p.row_lo) * p.ld;
+                        for (int64_t c = stid; c < p.NB; c += kWsHalf) red_add_f64(yr + c, p.e_core * xr[c]);
                     }
             }
             return;
@@ -916,7 +886,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
             bar_sync(BAR_SINT, kWsHalf);       // sJ visible to every loader
             bar_arrive(BAR_KLIST, kWsThreads);
             auto load_d = [&](int stage, int jt) {
-                if (p.dbg & 4) return;  // experiment: no gathers
+                if SBG_DBG(4) return;  // experiment: no gathers
                 double* dst = Ds + stage * KP * DSTRIDE;
                 for (int c = stid; c < KP * (NT / 2); c += kWsHalf) {
                     const int k = c / (NT / 2), part = c % (NT / 2);
@@ -952,18 +922,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                 bar_sync(BAR_FULL + b, kWsThreads);   // G(it) staged; D stage b free
                 if (it + 2 < ntiles) load_d(b, it + 2);
                 cp_async_commit();
-                if (p.red && !(p.dbg & 1)) {  // one reduction into y per (rs, column) entry
-                    const double* G = Gs + b * p.grows * GSTRIDE;
-                    const uint32_t* l32 = reinterpret_cast<const uint32_t*>(Le + b * p.maxE);
-                    const uint32_t n = sTE[it + 1] - sTE[it];
-#pragma unroll RED_UNROLL
-                    for (uint32_t i = stid; i < n; i += kWsHalf) {
-                        const uint32_t en = l32[i];
-                        if (en == 0xFFFFFFFFu) continue;  // 16-byte padding
-                        const long long bits = __double_as_longlong(G[en & 0x7FFFu]) ^ ((long long)(en & 0x8000u) << 48);
-                        red_add_f64(yrow + (en >> 16), __longlong_as_double(bits));
-                    }
-                } else if (!(p.dbg & 1)) {
+                if (p.red && !SBG_DBG(1)) {  // one reduction into y per (rs, column) entry
+                    scatter_tile(Gs + b * p.grows * GSTRIDE, reinterpret_cast<const uint32_t*>(Le + b * p.maxE),
+                                 sTE[it + 1] - sTE[it], yrow);
+                } else if (!SBG_DBG(1)) {
                     const double* G = Gs + b * p.grows * GSTRIDE;
                     const uint32_t* lt = Lt + b * p.maxT;
                     const uint16_t* le = Le + b * p.maxE;
@@ -1083,8 +1045,9 @@ void launch_sigma_ab_direct(const double* x_full, double* y_local, const double*
     SBG_LAUNCH_CHECK();
 }
 
-AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int64_t ld, int nsm) {
-    (void)nsm;
+namespace {
+// k0e_allowed: the occupation column k = 0 may leave the DGEMM (rank-1 epilogue term, K0E)
+AbPlan plan_sigma_ab_impl(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int64_t ld, bool k0e_allowed) {
     AbPlan pl{};
     pl.norb = norb;
     pl.na_el = na_el;
@@ -1113,7 +1076,7 @@ AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int
     pl.ws = (ws_env ? (atoi(ws_env) != 0) : 0) || pl.red;
     // k_sigma_ab_ws with K0E (the K - 1 links fill whole k-steps): KS = (K - 1) / 4 DMMA k-steps,
     // k = 0 an epilogue rank-1 term, D tiles of 1 + 4 KS rows; otherwise KS = ceil(K / 4), 4 KS rows
-    pl.k0e = pl.ws && pl.K > 1 && (pl.K - 1) % 4 == 0;
+    pl.k0e = pl.ws && pl.K > 1 && (pl.K - 1) % 4 == 0 && k0e_allowed;
     if (pl.k0e) pl.KS = (pl.K - 1) / 4;
     const int KP = pl.k0e ? 1 + 4 * pl.KS : 4 * pl.KS;
     auto configure = [&](int nt) {
@@ -1137,7 +1100,7 @@ AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int
         pl.maxE = 8 * ((nt * (nb_el + nb_el * (norb - nb_el)) + 7) / 8);
         if (pl.red) {  // one u32 per entry (maxE counts u16 slots), no target lists, no sigma row
             pl.maxT = 0;
-            pl.maxE = 2 * 4 * ((nt * (nb_el + nb_el * (norb - nb_el)) + 3) / 4);
+            pl.maxE = 2 * 4 * ((nt * (nb_el + nb_el * (norb - nb_el)) + 1 + 3) / 4);  // + the npos header
         }
         const int64_t ntiles = ld / nt;
         pl.smem = 64 + (size_t)(pl.red ? 0 : ld) * 8 + (size_t)STAGES * KP * (nt + 4) * 8 + (size_t)KP * 8 * 8 +
@@ -1167,7 +1130,10 @@ AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int
     // per linked row: measured slower at c4, 107.7 vs 100.7 ms — the 2-stage ring does not hide its
     // latency), 0 = cp.async for both
     const char* tma_env = getenv("SBG_AB_TMA");
-    pl.tma = (pl.ws && pl.red) ? (tma_env ? atoi(tma_env) : 1) : 0;
+    const char* dc_env0 = getenv("SBG_AB_DC");
+    pl.tma = (pl.ws && pl.red) ? ((tma_env ? atoi(tma_env) != 0 : 1) && !(dc_env0 && atoi(dc_env0) == 0)) : 0;
+    // 16-byte-unit row offsets of the hoisted gathers are 32-bit: vectors up to 64 GB
+    if ((double)NA * (double)ld >= 8.0e9) pl.tma = 0;
     // decoupled hand-offs (mbarrier D announcements, G handed back after the DMMAs) with a third D
     // stage when it fits; SBG_AB_DC=0 keeps the named-barrier hand-offs, =2 two D stages
     // uniform MMA instruction stream (see k_sigma_ab_ws): 1 = no extra rows, 2 = extra rows split
@@ -1190,10 +1156,30 @@ AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int
     }
     const char* dc_env = getenv("SBG_AB_DC");
     pl.dc = pl.tma ? (dc_env ? atoi(dc_env) : 3) : 0;
-    if (pl.dc != 0 && pl.dc != 2 && pl.dc != 3) pl.dc = 3;
+    if (pl.tma && pl.dc != 2 && pl.dc != 3) pl.dc = 3;
     const size_t dstage = (size_t)KP * (pl.nt + 4) * 8;
     if (pl.dc == 3 && pl.smem + dstage > 227 * 1024) pl.dc = 2;
     if (pl.dc == 3) pl.smem += dstage;
+    return pl;
+}
+}  // namespace
+
+AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int64_t ld, int nsm) {
+    (void)nsm;
+    // K0E (k = 0 as an epilogue rank-1 term, one k-step fewer when K - 1 is a multiple of 4) pays in
+    // the TALL kernel (c2: 0.301 vs 0.335 ms) but not in the uniform stream, whose DMMA warps then
+    // push 16 DFMAs per tile through the FP64 pipe they share with the other warp's DMMAs (c4: 93.9
+    // ms with it, 92.2 ms with a 17th k-step instead). SBG_AB_K0E=0/1 forces it off / on.
+    const char* env = getenv("SBG_AB_K0E");
+    const int force = env ? (atoi(env) != 0 ? 1 : 0) : -1;
+    AbPlan pl = plan_sigma_ab_impl(norb, na_el, nb_el, NA, NB, ld, force != 0);
+    if (force < 0 && pl.k0e && pl.xs) {
+        try {
+            const AbPlan alt = plan_sigma_ab_impl(norb, na_el, nb_el, NA, NB, ld, false);
+            if (alt.xs) pl = alt;
+        } catch (const InvalidArgument&) {  // the extra k-step does not fit: keep the epilogue form
+        }
+    }
     return pl;
 }
 
@@ -1257,11 +1243,24 @@ void build_ab_red_list(const AbPlan& pl, const std::vector<uint16_t>& codes, std
                     items.push_back({(uint32_t)(code & 0x7FFF), (uint32_t)(((rs + 8) * GSTRIDE + c) | (code & 0x8000))});
             }
         tile_ent[jt] = (uint32_t)ent.size();
-        // kept in G order (rs-major): a warp's shared-memory reads of G are then near-contiguous;
-        // target-sorting them instead (a warp reducing into neighbouring y elements) measured
-        // slightly slower — the row's targets are sparse within a tile either way
-        for (auto& it : items) ent.push_back((it.first << 16) | it.second);
-        while (ent.size() % 4) ent.push_back(0xFFFFFFFFu);
+        // Tile blob: [npos][positive entries][negative entries][padding to 16 bytes]; entry = target
+        // column << 16 | byte offset into the staged G tile. Each sign group is kept in G order
+        // (rs-major): a warp's shared-memory reads of G are then near-contiguous; target-sorting them
+        // instead (a warp reducing into neighbouring y elements) measured slightly slower, and one
+        // reduction per distinct target (a thread summing a target's entries first) much slower
+        // (146 vs 98 ms at c4: divergent dependent chains). Padding entries read the G padding
+        // column (0.0) and add it to column 0.
+        uint32_t npos = 0;
+        for (auto& it : items) npos += (it.second & 0x8000u) ? 0u : 1u;
+        ent.push_back(npos);
+        for (int neg = 0; neg < 2; ++neg)
+            for (auto& it : items) {
+                if (((it.second & 0x8000u) != 0) != (neg != 0)) continue;
+                const uint32_t byte_off = (it.second & 0x7FFFu) * 8u;
+                if (byte_off > 0xFFFFu) throw InvalidArgument("sigma_ab: staged tile too large for 16-bit list offsets");
+                ent.push_back((it.first << 16) | byte_off);
+            }
+        while (ent.size() % 4) ent.push_back((uint32_t)(NT * 8));
         if ((int64_t)(ent.size() - tile_ent[jt]) * 2 > pl.maxE) throw InvalidArgument("sigma_ab: red list overflow");
     }
     tile_ent[ntiles] = (uint32_t)ent.size();
