@@ -73,6 +73,7 @@ struct SsPlan {
     int64_t NK;
     size_t smem;
     int bulk = 1;  // staged tiles reduced into y by TMA bulk reductions (UBLKRED)
+    int xrows = 0; // rows per staged X tile
 };
 SsPlan plan_sigma_ss(int norb, int nel);
 // generic fallback outside plan_sigma_ss's limits: the one-spin two-body operator as CSR

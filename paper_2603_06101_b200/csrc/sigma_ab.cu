@@ -453,24 +453,27 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                     }
                     bar_sync(BAR_MINT, kWsHalf);
                     int sd = 0;
+                    // lane-dependent offsets pinned in registers (not rebuilt from the thread index per tile)
+                    int oB = (K0 + t) * DSTRIDE + g + nbh * 8, oGt = (16 * 4 + g) * GSTRIDE + nbh * 8 + 2 * t;
+                    asm volatile("" : "+r"(oB), "+r"(oGt));
                     for (int it = 0; it < ntot; ++it) {
                         const int b = it & 1;
                         const double* D = wait_d(it, sd);
                         if (!SBG_DBG(2) && nbh < NBT) {
                             double* G = Gs + b * p.grows * GSTRIDE;
-                            const double* D1 = D + K0 * DSTRIDE + g + nbh * 8;
+                            const double* D1 = D + oB;  // row K0 + t, this warp's n8 block
                             double acc[MH][4];
 #pragma unroll
                             for (int mb = 0; mb < MH; ++mb)
 #pragma unroll
                                 for (int e = 0; e < 4; ++e) acc[mb][e] = 0.0;
                             double bq[2];
-                            bq[0] = D1[t * DSTRIDE];
+                            bq[0] = D1[0];
 #pragma unroll
                             for (int j = 0; j < KS; ++j) {
                                 const int cur = j & 1;
                                 if (j == KS - 1) wait_g(it);
-                                if (j + 1 < KS) bq[cur ^ 1] = D1[(4 * (j + 1) + t) * DSTRIDE];
+                                if (j + 1 < KS) bq[cur ^ 1] = D1[4 * (j + 1) * DSTRIDE];
 #pragma unroll
                                 for (int mb = 0; mb < MH; ++mb)
                                     if (mb < mbh) dmma_16x8x4(acc[mb], ah0[mb][j], ah1[mb][j], bq[cur]);
@@ -480,10 +483,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
 #pragma unroll
                             for (int mb = 0; mb < MH; ++mb) {
                                 if (mb >= mbh) break;
-                                const int rh = 16 * (4 + mb) + g;
-                                *reinterpret_cast<double2*>(G + rh * GSTRIDE + col) =
+                                double* gr = G + oGt + 16 * mb * GSTRIDE;
+                                *reinterpret_cast<double2*>(gr) =
                                     make_double2(fma(ak0[mb], cv.x, acc[mb][0]), fma(ak0[mb], cv.y, acc[mb][1]));
-                                *reinterpret_cast<double2*>(G + (rh + 8) * GSTRIDE + col) =
+                                *reinterpret_cast<double2*>(gr + 8 * GSTRIDE) =
                                     make_double2(fma(ak1[mb], cv.x, acc[mb][2]), fma(ak1[mb], cv.y, acc[mb][3]));
                             }
                         } else {
@@ -635,6 +638,9 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
             for (int j = 0; j < KS; ++j) aer[j] = do_extra ? sAe[(K0 + 4 * j + t) * 8 + g] : 0.0;
             const double ae0 = (K0E && do_extra) ? sAe[g] : 0.0;
             int sd = 0;
+            // lane-dependent offsets pinned in registers (not rebuilt from the thread index per tile)
+            int oBm = (K0 + t) * DSTRIDE + g, oGm = r0 * GSTRIDE + 2 * t;
+            asm volatile("" : "+r"(oBm), "+r"(oGm));
             for (int it = 0; it < ntot; ++it) {
                 const int b = it & 1;
                 const double* D = wait_d(it, sd);
@@ -646,7 +652,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                     for (int nb = 0; nb < NBT; ++nb)
 #pragma unroll
                         for (int e = 0; e < 4; ++e) acc[nb][e] = 0.0;
-                    const double* D1 = D + K0 * DSTRIDE;  // rows of the DMMA k range
+                    const double* D1 = D + oBm;  // row K0 + t, column g: B fragments of the DMMA k range
 #ifndef SBG_BF_DEPTH
 #define SBG_BF_DEPTH 2
 #endif
@@ -656,7 +662,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                     for (int jj = 0; jj < BFD - 1; ++jj)
                         if (jj < KS) {
 #pragma unroll
-                            for (int nb = 0; nb < NBT; ++nb) bf[jj][nb] = D1[(4 * jj + t) * DSTRIDE + g + nb * 8];
+                            for (int nb = 0; nb < NBT; ++nb) bf[jj][nb] = D1[4 * jj * DSTRIDE + nb * 8];
                         }
 #pragma unroll
                     for (int j = 0; j < KS; ++j) {
@@ -667,7 +673,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                         if (j + BFD - 1 < KS) {
 #pragma unroll
                             for (int nb = 0; nb < NBT; ++nb)
-                                bf[(j + BFD - 1) % BFD][nb] = D1[(4 * (j + BFD - 1) + t) * DSTRIDE + g + nb * 8];
+                                bf[(j + BFD - 1) % BFD][nb] = D1[4 * (j + BFD - 1) * DSTRIDE + nb * 8];
                         }
 #pragma unroll
                         for (int nb = 0; nb < NBT; ++nb) dmma_16x8x4(acc[nb], a0[j], a1[j], bf[cur][nb]);
@@ -699,9 +705,9 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                     }
 #pragma unroll
                     for (int nb = 0; nb < NBT; ++nb) {
-                        const int col = nb * 8 + 2 * t;
-                        *reinterpret_cast<double2*>(G + r0 * GSTRIDE + col) = make_double2(acc[nb][0], acc[nb][1]);
-                        *reinterpret_cast<double2*>(G + (r0 + 8) * GSTRIDE + col) = make_double2(acc[nb][2], acc[nb][3]);
+                        double* gr = G + oGm + nb * 8;
+                        *reinterpret_cast<double2*>(gr) = make_double2(acc[nb][0], acc[nb][1]);
+                        *reinterpret_cast<double2*>(gr + 8 * GSTRIDE) = make_double2(acc[nb][2], acc[nb][3]);
                     }
                     if (do_extra) *reinterpret_cast<double2*>(G + (re + g) * GSTRIDE + w * 8 + 2 * t) = ge;
                 } else {

@@ -30,7 +30,11 @@ constexpr int YSTRIDE = NTS + 8;  // == 8 mod 16 doubles: conflict-free 16-byte 
 #ifndef SBG_SS_MINB
 #define SBG_SS_MINB 4
 #endif
-constexpr int kMaxTilesPerCta = SBG_SS_TPC;  // column tiles per CTA: amortizes the per-K setup (pair list, A)
+constexpr int kMaxTilesPerCta = SBG_SS_TPC;
+#ifndef SBG_SS_STAGES
+#define SBG_SS_STAGES 2
+#endif
+constexpr int SS_STAGES = SBG_SS_STAGES;  // X tiles in flight (3: P-row stages, the k padding rows alias the next buffer)  // column tiles per CTA: amortizes the per-K setup (pair list, A)
 
 struct SsParams {
     const double* x;
@@ -48,6 +52,7 @@ struct SsParams {
     int nvec;
     const double* xv[kMaxSigmaVec];
     double* yv[kMaxSigmaVec];
+    int xrows;  // rows per X stage (KPP, or P with three stages)
 };
 
 template <int KSS>
@@ -60,7 +65,8 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
     extern __shared__ __align__(16) double smem[];
     double* Xs = smem;                        // [2][KPP][XSTRIDE]
     const int ysrows = max(KPP, 16 * (int)(blockDim.x >> 5));
-    double* Ys = Xs + 2 * KPP * XSTRIDE;      // [ysrows][YSTRIDE]
+    const int xstage = p.xrows * XSTRIDE;     // doubles per X stage
+    double* Ys = Xs + SS_STAGES * xstage;     // [ysrows][YSTRIDE]
     int* sJ = reinterpret_cast<int*>(Ys + ysrows * YSTRIDE);
     int* sPi = sJ + KPP;
     double* sPhi = reinterpret_cast<double*>(sPi + KPP);
@@ -128,14 +134,18 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
     auto load = [&](int tt) {  // tile tt of the sequence: column tile tt % ntt of vector tt / ntt
         const int64_t c0 = c_begin + (int64_t)(tt % ntt) * NTS;
         const double* xs = p.xv[tt / ntt];
-        double* dst = Xs + (tt & 1) * KPP * XSTRIDE;
-        for (int c = tid; c < KPP * (NTS / 2); c += nthr) {
+        double* dst = Xs + (tt % SS_STAGES) * xstage;
+        for (int c = tid; c < p.xrows * (NTS / 2); c += nthr) {
             const int k = c / (NTS / 2), part = c % (NTS / 2);
             // the last tile may overhang the padded row: those columns are never reduced
             if (c0 + part * 2 < p.ldx)
                 cp_async16(dst + k * XSTRIDE + part * 2, xs + (int64_t)sJ[k] * p.ldx + c0 + part * 2);
         }
     };
+    if (SS_STAGES > 2) {  // aliased padding rows must hold finite numbers from the start
+        for (int i = tid; i < SS_STAGES * xstage + ysrows * YSTRIDE; i += nthr) Xs[i] = 0.0;
+        __syncthreads();
+    }
     if (ntt > 0) load(0);
     cp_async_commit();
     if (p.bulk) {
@@ -147,14 +157,18 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
         // overwrites it.
         const int64_t full_end = p.col_pad > p.col_hi ? p.col_pad : p.col_hi;
         const int nseq = ntt * p.nvec;
+        if (SS_STAGES > 2) {
+            if (1 < nseq) load(1);
+            cp_async_commit();
+        }
         for (int tt = 0; tt < nseq; ++tt) {
             const int64_t c0 = c_begin + (int64_t)(tt % ntt) * NTS;
             double* const yv = p.yv[tt / ntt];
-            cp_async_wait<0>();
-            __syncthreads();  // X(tt) visible; every warp is done with X(tt-1), whose buffer load(tt+1) refills
-            if (tt + 1 < nseq) load(tt + 1);
+            cp_async_wait<SS_STAGES - 2>();
+            __syncthreads();  // X(tt) visible; every warp is done with X(tt-1), whose buffer the next load refills
+            if (tt + SS_STAGES - 1 < nseq) load(tt + SS_STAGES - 1);
             cp_async_commit();
-            const double* X = Xs + (tt & 1) * KPP * XSTRIDE;
+            const double* X = Xs + (tt % SS_STAGES) * xstage;
             double acc[NTS / 8][4];
 #pragma unroll
             for (int nb = 0; nb < NTS / 8; ++nb)
@@ -210,7 +224,7 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
         cp_async_commit();
         cp_async_wait<1>();
         __syncthreads();  // X(tt) visible; the reductions of tile tt-1 finished reading Ys
-        const double* X = Xs + (tt & 1) * KPP * XSTRIDE;
+        const double* X = Xs + (tt % SS_STAGES) * xstage;
         double acc[NTS / 8][4];
 #pragma unroll
         for (int nb = 0; nb < NTS / 8; ++nb)
@@ -411,7 +425,8 @@ SsPlan plan_sigma_ss(int norb, int nel) {
     pl.warps = (pl.P + 15) / 16;
     const int KPP = pl.KSS * 4;
     const int rows = std::max(KPP, 16 * pl.warps);
-    pl.smem = (size_t)(2 * KPP * XSTRIDE + rows * YSTRIDE) * 8 + (size_t)KPP * 8 * 5 + 16;
+    pl.xrows = SS_STAGES > 2 ? pl.P : KPP;
+    pl.smem = (size_t)(SS_STAGES * pl.xrows * XSTRIDE + rows * YSTRIDE) * 8 + (size_t)KPP * 8 * 5 + 16;
     // staged tiles reach y through TMA bulk reductions (cp.reduce.async.bulk .add.f64, one 256-byte
     // row segment per instruction); SBG_SS_BULK=0 keeps the per-lane red.global.add form
     const char* bulk_env = getenv("SBG_SS_BULK");
@@ -449,6 +464,7 @@ void launch_sigma_ss_multi(const SsPlan& pl, const double* const* xv, double* co
     if (nvec < 1 || nvec > kMaxSigmaVec || (nvec > 1 && !bulk))
         throw InvalidArgument("sigma_ss: several vectors per launch need the bulk-reduction kernel");
     SsParams prm{x, y, Va, pl.norb, pl.nel, pl.P, pl.npa, ldx, col_lo, col_hi, tpc, ldy, ycol0, bulk, col_pad, nvec};
+    prm.xrows = pl.xrows;
     for (int v = 0; v < nvec; ++v) {
         prm.xv[v] = xv[v];
         prm.yv[v] = yvs[v];
