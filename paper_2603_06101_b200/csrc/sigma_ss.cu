@@ -131,22 +131,32 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
     const int64_t c_begin = (p.col_lo / NTS + (int64_t)blockIdx.y * p.tpc) * NTS;
     const int64_t c_end = ((p.col_hi + NTS - 1) / NTS) * NTS;
     const int ntt = (int)std::min<int64_t>(p.tpc, (c_end - c_begin) / NTS);
-    auto load = [&](int tt) {  // tile tt of the sequence: column tile tt % ntt of vector tt / ntt
-        const int64_t c0 = c_begin + (int64_t)(tt % ntt) * NTS;
-        const double* xs = p.xv[tt / ntt];
-        double* dst = Xs + (tt % SS_STAGES) * xstage;
-        for (int c = tid; c < p.xrows * (NTS / 2); c += nthr) {
-            const int k = c / (NTS / 2), part = c % (NTS / 2);
-            // the last tile may overhang the padded row: those columns are never reduced
-            if (c0 + part * 2 < p.ldx)
-                cp_async16(dst + k * XSTRIDE + part * 2, xs + (int64_t)sJ[k] * p.ldx + c0 + part * 2);
+    int ld_k = tid / (NTS / 2), ld_part2 = (tid % (NTS / 2)) * 2, ld_soff = ld_k * XSTRIDE + ld_part2;
+    asm volatile("" : "+r"(ld_k), "+r"(ld_part2), "+r"(ld_soff));  // fixed per thread: not rebuilt per tile
+    auto load = [&](int tcol, int vec, int stage) {  // column tile tcol of vector vec into X stage `stage`
+        const int64_t c0 = c_begin + (int64_t)tcol * NTS;
+        const double* xs = p.xv[vec] + c0;
+        double* dst = Xs + stage * xstage;
+        // a tile may overhang the padded row only when ldx is not a multiple of NTS: those columns
+        // are never reduced
+        const bool inside = c0 + NTS <= p.ldx;
+        // chunk i of this thread: row ld_k + i * KSTEP, column pair ld_part2 (the block has a whole
+        // number of 16-thread rows, so the column pair is the same for every chunk): one row-offset
+        // load, one address add and one cp.async per chunk, unrolled
+        constexpr int NTHR = 32 * ((KSS + 3) / 4), KSTEP = NTHR / (NTS / 2), NCH = (KPP + KSTEP - 1) / KSTEP;
+        if (inside || c0 + ld_part2 < p.ldx) {
+#pragma unroll
+            for (int i = 0; i < NCH; ++i) {
+                const int k = ld_k + i * KSTEP;
+                if (k < p.xrows) cp_async16(dst + ld_soff + i * KSTEP * XSTRIDE, xs + sRow[k] + ld_part2);
+            }
         }
     };
     if (SS_STAGES > 2) {  // aliased padding rows must hold finite numbers from the start
         for (int i = tid; i < SS_STAGES * xstage + ysrows * YSTRIDE; i += nthr) Xs[i] = 0.0;
         __syncthreads();
     }
-    if (ntt > 0) load(0);
+    if (ntt > 0) load(0, 0, 0);
     cp_async_commit();
     if (p.bulk) {
         // One block barrier per tile. Each warp stages ITS OWN 16 rows of the tile in Ys and reduces
@@ -157,18 +167,34 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
         // overwrites it.
         const int64_t full_end = p.col_pad > p.col_hi ? p.col_pad : p.col_hi;
         const int nseq = ntt * p.nvec;
+        // tile tt of the sequence is column tile tt % ntt of vector tt / ntt: running counters for the
+        // tile being loaded (ld_*) and the tile being computed (cu_*) instead of divisions per tile
+        int ld_t = 1 % ntt, ld_v = 1 / ntt, ld_s = 1 % SS_STAGES, cu_t = 0, cu_v = 0, cu_s = 0;
+        auto load_next = [&]() {
+            load(ld_t, ld_v, ld_s);
+            if (++ld_t == ntt) {
+                ld_t = 0;
+                ++ld_v;
+            }
+            if (++ld_s == SS_STAGES) ld_s = 0;
+        };
         if (SS_STAGES > 2) {
-            if (1 < nseq) load(1);
+            if (1 < nseq) load_next();
             cp_async_commit();
         }
         for (int tt = 0; tt < nseq; ++tt) {
-            const int64_t c0 = c_begin + (int64_t)(tt % ntt) * NTS;
-            double* const yv = p.yv[tt / ntt];
+            const int64_t c0 = c_begin + (int64_t)cu_t * NTS;
+            double* const yv = p.yv[cu_v];
+            const double* X = Xs + cu_s * xstage;
+            if (++cu_t == ntt) {
+                cu_t = 0;
+                ++cu_v;
+            }
+            if (++cu_s == SS_STAGES) cu_s = 0;
             cp_async_wait<SS_STAGES - 2>();
             __syncthreads();  // X(tt) visible; every warp is done with X(tt-1), whose buffer the next load refills
-            if (tt + SS_STAGES - 1 < nseq) load(tt + SS_STAGES - 1);
+            if (tt + SS_STAGES - 1 < nseq) load_next();
             cp_async_commit();
-            const double* X = Xs + (tt % SS_STAGES) * xstage;
             double acc[NTS / 8][4];
 #pragma unroll
             for (int nb = 0; nb < NTS / 8; ++nb)
@@ -220,7 +246,7 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
     }
     for (int tt = 0; tt < ntt; ++tt) {
         const int64_t c0 = c_begin + (int64_t)tt * NTS;
-        if (tt + 1 < ntt) load(tt + 1);
+        if (tt + 1 < ntt) load(tt + 1, 0, (tt + 1) % SS_STAGES);
         cp_async_commit();
         cp_async_wait<1>();
         __syncthreads();  // X(tt) visible; the reductions of tile tt-1 finished reading Ys
