@@ -484,10 +484,14 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                             for (int mb = 0; mb < MH; ++mb) {
                                 if (mb >= mbh) break;
                                 double* gr = G + oGt + 16 * mb * GSTRIDE;
-                                *reinterpret_cast<double2*>(gr) =
-                                    make_double2(fma(ak0[mb], cv.x, acc[mb][0]), fma(ak0[mb], cv.y, acc[mb][1]));
-                                *reinterpret_cast<double2*>(gr + 8 * GSTRIDE) =
-                                    make_double2(fma(ak1[mb], cv.x, acc[mb][2]), fma(ak1[mb], cv.y, acc[mb][3]));
+                                if constexpr (K0E) {  // (without it no FP64 add may reach the pipe the DMMAs use)
+                                    acc[mb][0] = fma(ak0[mb], cv.x, acc[mb][0]);
+                                    acc[mb][1] = fma(ak0[mb], cv.y, acc[mb][1]);
+                                    acc[mb][2] = fma(ak1[mb], cv.x, acc[mb][2]);
+                                    acc[mb][3] = fma(ak1[mb], cv.y, acc[mb][3]);
+                                }
+                                *reinterpret_cast<double2*>(gr) = make_double2(acc[mb][0], acc[mb][1]);
+                                *reinterpret_cast<double2*>(gr + 8 * GSTRIDE) = make_double2(acc[mb][2], acc[mb][3]);
                             }
                         } else {
                             wait_g(it);
@@ -497,6 +501,79 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                     drain_g(ntot);
                     continue;  // next row
                 }
+                // warps 0-3 of the TALL kernel: m16 block w with every n8 block, the blocks interleaved
+                // over the tile's columns as in the uniform stream (two LDS.128 per k-step, no per-k-step
+                // branch)
+                static_assert(NT == 32, "TALL: 32-column tiles");
+                const int r0 = 16 * w + g;
+                double a0[KS], a1[KS];
+#pragma unroll
+                for (int j = 0; j < KS; ++j) {
+                    a0[j] = aval(r0, K0 + 4 * j + t);
+                    a1[j] = aval(r0 + 8, K0 + 4 * j + t);
+                }
+                const double a00 = K0E ? aocc(r0) : 0.0, a01 = K0E ? aocc(r0 + 8) : 0.0;
+                bar_sync(BAR_MINT, kWsHalf);
+                int oB = (K0 + t) * DSTRIDE + 2 * g, oG = r0 * GSTRIDE + 4 * t;
+                asm volatile("" : "+r"(oB), "+r"(oG));
+                int sd = 0;
+                for (int it = 0; it < ntot; ++it) {
+                    const int b = it & 1;
+                    const double* D = wait_d(it, sd);
+                    if (!SBG_DBG(2)) {
+                        double* G = Gs + b * p.grows * GSTRIDE;
+                        const double* pB = D + oB;
+                        double acc[4][4];
+#pragma unroll
+                        for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) acc[nb][e] = 0.0;
+                        double2 q[2][2];
+                        q[0][0] = *reinterpret_cast<const double2*>(pB);
+                        q[0][1] = *reinterpret_cast<const double2*>(pB + 16);
+#pragma unroll
+                        for (int j = 0; j < KS; ++j) {
+                            const int cur = j & 1;
+                            if (j == KS - 1) wait_g(it);
+                            if (j + 1 < KS) {
+                                q[cur ^ 1][0] = *reinterpret_cast<const double2*>(pB + 4 * (j + 1) * DSTRIDE);
+                                q[cur ^ 1][1] = *reinterpret_cast<const double2*>(pB + 4 * (j + 1) * DSTRIDE + 16);
+                            }
+                            dmma_16x8x4(acc[0], a0[j], a1[j], q[cur][0].x);
+                            dmma_16x8x4(acc[1], a0[j], a1[j], q[cur][0].y);
+                            dmma_16x8x4(acc[2], a0[j], a1[j], q[cur][1].x);
+                            dmma_16x8x4(acc[3], a0[j], a1[j], q[cur][1].y);
+                        }
+                        // column of acc[L][e] = 16 (L >> 1) + 4 t + 2 (e & 1) + (L & 1), rows g (e < 2), g + 8
+                        if constexpr (K0E) {
+                            const double2 va0 = *reinterpret_cast<const double2*>(D + 4 * t), va1 = *reinterpret_cast<const double2*>(D + 4 * t + 2);
+                            const double2 vb0 = *reinterpret_cast<const double2*>(D + 16 + 4 * t), vb1 = *reinterpret_cast<const double2*>(D + 18 + 4 * t);
+                            acc[0][0] = fma(a00, va0.x, acc[0][0]); acc[1][0] = fma(a00, va0.y, acc[1][0]);
+                            acc[0][1] = fma(a00, va1.x, acc[0][1]); acc[1][1] = fma(a00, va1.y, acc[1][1]);
+                            acc[0][2] = fma(a01, va0.x, acc[0][2]); acc[1][2] = fma(a01, va0.y, acc[1][2]);
+                            acc[0][3] = fma(a01, va1.x, acc[0][3]); acc[1][3] = fma(a01, va1.y, acc[1][3]);
+                            acc[2][0] = fma(a00, vb0.x, acc[2][0]); acc[3][0] = fma(a00, vb0.y, acc[3][0]);
+                            acc[2][1] = fma(a00, vb1.x, acc[2][1]); acc[3][1] = fma(a00, vb1.y, acc[3][1]);
+                            acc[2][2] = fma(a01, vb0.x, acc[2][2]); acc[3][2] = fma(a01, vb0.y, acc[3][2]);
+                            acc[2][3] = fma(a01, vb1.x, acc[2][3]); acc[3][3] = fma(a01, vb1.y, acc[3][3]);
+                        }
+                        double* g0 = G + oG;
+                        double* g1 = g0 + 8 * GSTRIDE;
+                        *reinterpret_cast<double2*>(g0) = make_double2(acc[0][0], acc[1][0]);
+                        *reinterpret_cast<double2*>(g0 + 2) = make_double2(acc[0][1], acc[1][1]);
+                        *reinterpret_cast<double2*>(g1) = make_double2(acc[0][2], acc[1][2]);
+                        *reinterpret_cast<double2*>(g1 + 2) = make_double2(acc[0][3], acc[1][3]);
+                        *reinterpret_cast<double2*>(g0 + 16) = make_double2(acc[2][0], acc[3][0]);
+                        *reinterpret_cast<double2*>(g0 + 18) = make_double2(acc[2][1], acc[3][1]);
+                        *reinterpret_cast<double2*>(g1 + 16) = make_double2(acc[2][2], acc[3][2]);
+                        *reinterpret_cast<double2*>(g1 + 18) = make_double2(acc[2][3], acc[3][3]);
+                    } else {
+                        wait_g(it);
+                    }
+                    if (!SBG_DBG(16)) bar_arrive(BAR_FULL + b, kWsThreads);
+                }
+                drain_g(ntot);
+                continue;  // next row
             }
             if constexpr (XS > 0) {
                 constexpr int KH = (KS + 1) / 2;          // iterations carrying an extra-row DMMA
@@ -689,19 +766,23 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                     }
                     // epilogue: the k = 0 rank-1 term (K0E; a00 = a01 = ae0 = 0 otherwise), then
                     // 16-byte stores of the tile (decoupled: once the scatter has handed buffer b back)
+                    if constexpr (K0E) {
 #pragma unroll
-                    for (int nb = 0; nb < NBT; ++nb) {
-                        const int col = nb * 8 + 2 * t;
-                        const double2 cv = K0E ? *reinterpret_cast<const double2*>(D + col) : make_double2(0.0, 0.0);
-                        acc[nb][0] = fma(a00, cv.x, acc[nb][0]);
-                        acc[nb][1] = fma(a00, cv.y, acc[nb][1]);
-                        acc[nb][2] = fma(a01, cv.x, acc[nb][2]);
-                        acc[nb][3] = fma(a01, cv.y, acc[nb][3]);
+                        for (int nb = 0; nb < NBT; ++nb) {
+                            const double2 cv = *reinterpret_cast<const double2*>(D + nb * 8 + 2 * t);
+                            acc[nb][0] = fma(a00, cv.x, acc[nb][0]);
+                            acc[nb][1] = fma(a00, cv.y, acc[nb][1]);
+                            acc[nb][2] = fma(a01, cv.x, acc[nb][2]);
+                            acc[nb][3] = fma(a01, cv.y, acc[nb][3]);
+                        }
                     }
                     double2 ge = make_double2(0.0, 0.0);
                     if (do_extra) {
-                        const double2 cv = K0E ? *reinterpret_cast<const double2*>(D + w * 8 + 2 * t) : make_double2(0.0, 0.0);
-                        ge = make_double2(fma(ae0, cv.x, ace0[0] + ace1[0]), fma(ae0, cv.y, ace0[1] + ace1[1]));
+                        ge = make_double2(ace0[0] + ace1[0], ace0[1] + ace1[1]);
+                        if constexpr (K0E) {
+                            const double2 cv = *reinterpret_cast<const double2*>(D + w * 8 + 2 * t);
+                            ge = make_double2(fma(ae0, cv.x, ge.x), fma(ae0, cv.y, ge.y));
+                        }
                     }
 #pragma unroll
                     for (int nb = 0; nb < NBT; ++nb) {
