@@ -1256,16 +1256,25 @@ AbPlan plan_sigma_ab(int norb, int na_el, int nb_el, int64_t NA, int64_t NB, int
     // K0E (k = 0 as an epilogue rank-1 term, one k-step fewer when K - 1 is a multiple of 4) pays in
     // the TALL kernel (c2: 0.301 vs 0.335 ms) but not in the uniform stream, whose DMMA warps then
     // push 16 DFMAs per tile through the FP64 pipe they share with the other warp's DMMAs (c4: 93.9
-    // ms with it, 92.2 ms with a 17th k-step instead). SBG_AB_K0E=0/1 forces it off / on.
+    // ms with it, 92.2 ms with a 17th k-step instead). SBG_AB_K0E=0 turns it off everywhere.
     const char* env = getenv("SBG_AB_K0E");
-    const int force = env ? (atoi(env) != 0 ? 1 : 0) : -1;
-    AbPlan pl = plan_sigma_ab_impl(norb, na_el, nb_el, NA, NB, ld, force != 0);
-    if (force < 0 && pl.k0e && pl.xs) {
-        try {
-            const AbPlan alt = plan_sigma_ab_impl(norb, na_el, nb_el, NA, NB, ld, false);
-            if (alt.xs) pl = alt;
-        } catch (const InvalidArgument&) {  // the extra k-step does not fit: keep the epilogue form
+    const bool allow = !(env && atoi(env) == 0);
+    AbPlan pl = plan_sigma_ab_impl(norb, na_el, nb_el, NA, NB, ld, allow);
+    if (pl.k0e && pl.xs) {  // the uniform stream is only built without the epilogue form
+        const AbPlan alt = plan_sigma_ab_impl(norb, na_el, nb_el, NA, NB, ld, false);
+        if (alt.xs) return alt;
+        // the extra k-step changed the plan (it no longer takes the uniform stream): fall back to the
+        // older stream with the epilogue form
+        pl.xs = 0;
+        const int gold = pl.gstride, rold = pl.grows;
+        pl.gstride = pl.nt + 8;
+        pl.grows = pl.npad;
+        pl.smem += (size_t)STAGES * ((size_t)pl.grows * pl.gstride - (size_t)rold * gold) * 8;
+        if (pl.smem > 227 * 1024 && pl.dc == 3) {
+            pl.dc = 2;
+            pl.smem -= (size_t)(pl.k0e ? 1 + 4 * pl.KS : 4 * pl.KS) * (pl.nt + 4) * 8;
         }
+        if (pl.smem > 227 * 1024) throw InvalidArgument("sigma_ab: beta row does not fit in shared memory");
     }
     return pl;
 }
@@ -1413,12 +1422,13 @@ void launch_sigma_ab_multi(const AbPlan& pl, const AbScatter& sc, const double* 
                 if (pl.k0e) launch_ks<n, 32, true, true>(pl, prm, grid, st);                        \
                 else launch_ks<n, 32, false, true>(pl, prm, grid, st);                              \
             }                                                                                       \
-        } else if (pl.nt == 32 && pl.xs == 2) {                                                     \
-            if (pl.k0e) launch_ks<n, 32, true, false, 2>(pl, prm, grid, st);                        \
-            else launch_ks<n, 32, false, false, 2>(pl, prm, grid, st);                              \
+        } else if (pl.nt == 32 && pl.xs == 2) { /* the uniform stream keeps k = 0 in the DGEMM */  \
+            /* 8 m16 blocks + 8 extra rows = 16 orbitals: K = 1 + n (16 - n), these k-step counts */  \
+            if constexpr (n == 4 || n == 8 || n == 10 || n == 13 || n == 14 || n == 16 || n == 17)    \
+                launch_ks<n, 32, false, false, 2>(pl, prm, grid, st);                               \
+            else throw InvalidArgument("sigma_ab: no split-extra-rows kernel for this K");          \
         } else if (pl.nt == 32 && pl.xs == 1) {                                                     \
-            if (pl.k0e) launch_ks<n, 32, true, false, 1>(pl, prm, grid, st);                        \
-            else launch_ks<n, 32, false, false, 1>(pl, prm, grid, st);                              \
+            launch_ks<n, 32, false, false, 1>(pl, prm, grid, st);                                   \
         } else if (pl.nt == 32) {                                                                   \
             if (pl.k0e) launch_ks<n, 32, true>(pl, prm, grid, st);                                  \
             else launch_ks<n, 32, false>(pl, prm, grid, st);                                        \
