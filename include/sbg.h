@@ -100,6 +100,13 @@ typedef void (*sbg_trace_fn)(const sbg_trace_record* rec, void* user);
 const char* sbg_last_error(void);
 const char* sbg_version(void);
 uint64_t sbg_binomial(int n, int k);                                  /* determinants.hpp:17-31 */
+/* Diagnostics (host logic only, no GPU needed): the launch plan of the opposite-spin kernel for a
+ * sector. out[0..15] = k-steps, tile columns, m16 blocks, extra-row block, rank-1 epilogue (K0E),
+ * TALL, uniform stream (0/1/2), D stages of the mbarrier hand-offs (0 = named barriers), bulk-copied
+ * lists, pair-row passes, dynamic shared memory in bytes, staged G rows, G row stride, list buffer
+ * (u16 slots), threads, reduction mode. SBG_EINVAL when the sector is outside the tensor-core
+ * kernel's limits (the operator then uses the link-table kernel). */
+int sbg_ab_plan_info(int norb, int n_alpha, int n_beta, int64_t* out16);
 int sbg_determinant_count(int norb, int n_alpha, int n_beta, uint64_t* out); /* determinants.hpp:33-37 */
 sbg_config sbg_config_default(void);                                  /* config.hpp:11-22 */
 int sbg_config_validate(const sbg_config* cfg);                       /* config.hpp:26-43 */

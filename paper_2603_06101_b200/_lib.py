@@ -62,6 +62,7 @@ def lib() -> C.CDLL:
         "sbg_last_error": (C.c_char_p, []),
         "sbg_version": (C.c_char_p, []),
         "sbg_binomial": (C.c_uint64, [C.c_int, C.c_int]),
+        "sbg_ab_plan_info": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int64)]),
         "sbg_determinant_count": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_uint64)]),
         "sbg_config_default": (Config, []),
         "sbg_config_validate": (C.c_int, [C.POINTER(Config)]),
@@ -116,7 +117,7 @@ def lib() -> C.CDLL:
 
 
 # every symbol declared in include/sbg.h (checked by tests/test_abi.py against the header)
-EXPORTED = ["sbg_last_error", "sbg_version", "sbg_binomial", "sbg_determinant_count", "sbg_config_default",
+EXPORTED = ["sbg_last_error", "sbg_version", "sbg_binomial", "sbg_ab_plan_info", "sbg_determinant_count", "sbg_config_default",
             "sbg_config_validate", "sbg_synthetic_integrals", "sbg_shard_range", "sbg_device_count", "sbg_create",
             "sbg_create_dist", "sbg_nccl_unique_id", "sbg_destroy", "sbg_dim", "sbg_sector", "sbg_local_rows",
             "sbg_diagonal", "sbg_table_sizes", "sbg_string_tables", "sbg_sigma", "sbg_sigma_device",

@@ -145,6 +145,21 @@ int sbg_determinant_count(int norb, int n_alpha, int n_beta, uint64_t* out) {
     });
 }
 
+int sbg_ab_plan_info(int norb, int n_alpha, int n_beta, int64_t* out) {
+    return guarded([&] {
+        if (norb < 1 || norb > sbg::kMaxOrb || n_alpha < 0 || n_beta < 0 || n_alpha > norb || n_beta > norb)
+            throw std::invalid_argument("ab_plan_info: sector out of range");
+        if (n_alpha == 0 || n_beta == 0) throw std::invalid_argument("ab_plan_info: no opposite-spin term");
+        const int64_t NA = (int64_t)binomial_u64(norb, n_alpha), NB = (int64_t)binomial_u64(norb, n_beta);
+        const int64_t ld = sbg::round_up(NB, 32);
+        const sbg::AbPlan pl = sbg::plan_sigma_ab(norb, n_alpha, n_beta, NA, NB, ld, 148);
+        const int64_t v[16] = {pl.KS, pl.nt, pl.mb16, pl.extra, pl.k0e, pl.tall, pl.xs, pl.dc, pl.tma, pl.npass,
+                               (int64_t)pl.smem, pl.grows ? pl.grows : pl.npad, pl.gstride ? pl.gstride : pl.nt + 8,
+                               pl.maxE, pl.threads, pl.red};
+        for (int i = 0; i < 16; ++i) out[i] = v[i];
+    });
+}
+
 sbg_config sbg_config_default(void) {
     sbg::SolverConfig s;
     sbg_config c{};

@@ -1228,8 +1228,12 @@ AbPlan plan_sigma_ab_impl(int norb, int na_el, int nb_el, int64_t NA, int64_t NB
     const char* xs_env = getenv("SBG_AB_XS");
     pl.xs = 0;
     if (pl.tma && pl.nt == 32 && !pl.tall && !(xs_env && atoi(xs_env) == 0)) {
+        // split extra rows: 8 m16 blocks + 8 rows = 16 orbitals; built for the k-step counts of
+        // K = 1 + n (16 - n), 1 <= n <= 15 (a full alpha shell, K = 1, keeps the older stream)
+        const int ks = (pl.K + 3) / 4;  // the uniform stream keeps k = 0 in the DGEMM (plan_sigma_ab)
+        const bool ks2 = ks == 4 || ks == 8 || ks == 10 || ks == 13 || ks == 14 || ks == 16 || ks == 17;
         if (!pl.extra) pl.xs = 1;
-        else if (pl.mb16 == 8) pl.xs = 2;
+        else if (pl.mb16 == 8 && ks2) pl.xs = 2;
     }
     pl.gstride = pl.xs ? pl.nt + 2 : pl.nt + 8;
     pl.grows = pl.npad + (pl.xs == 2 ? 8 : 0);

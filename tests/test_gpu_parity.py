@@ -674,6 +674,23 @@ def test_sigma_large_orbital_fallbacks(dev, rest, monkeypatch, spec, direct):
     op.close()
 
 
+@pytest.mark.parametrize("spec", [(16, 18, 14), (16, 30, 0), (16, 28, 2), (16, 3, 1), (16, 17, 15)])
+def test_sigma_sixteen_orbital_edge_sectors(dev, rest, spec):
+    """16 orbitals (136 pair rows: the kernel with split extra rows) at the ends of the electron range:
+    a full alpha shell (K = 1 linked row, the older instruction stream), nearly full shells (K = 16, 29)
+    and nearly empty ones; sigma matches the restatement of contract_sigma."""
+    norb, nelec, ms2 = spec
+    h1, eri = rest.synthetic(norb, 70 + nelec, 0.06)
+    q = Problem(norb, nelec, ms2, 0.2, h1, eri, f"{norb}o{nelec}e{ms2}")
+    op = P.FciOperator(to_product(q), max_determinants=2 ** 62)
+    X = np.stack([seeded(op.dim(), s) for s in (8, 9)])
+    Y = op.apply(X)
+    for x, y in zip(X, Y):
+        ref = rest.sigma(q, x, exact=True)
+        assert np.abs(y - ref).max() <= SIGMA_RTOL * np.abs(ref).max()
+    op.close()
+
+
 def test_sbci1_large_orbital_sector_vs_dense(dev, rest):
     """(17o,2e): both terms on the generic kernels; SBCI1 energies against the dense spectrum."""
     h1, eri = rest.synthetic(17, 61, 0.06)
