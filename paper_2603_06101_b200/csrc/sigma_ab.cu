@@ -615,7 +615,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                 // the tile loop, compiled once per parity of the extra block (a sub-partition's two DMMA
                 // warps share it): picking the odd or even block's B fragment costs no select
                 auto tile_loop = [&](auto xodd_c) {
-                    constexpr bool XODD = decltype(xodd_c)::value;
+                    [[maybe_unused]] constexpr bool XODD = decltype(xodd_c)::value;
                     int sd = 0;
                     for (int it = 0; it < ntot; ++it) {
                         const int b = it & 1;
@@ -627,7 +627,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
                             const char* pHi01 = pLo01 + oHi;
                             const char* pHi23 = pLo23 + oHi;
                             double acc[4][4];
-                            double acx[2] = {0.0, 0.0};
+                            [[maybe_unused]] double acx[2] = {0.0, 0.0};
 #pragma unroll
                             for (int nb = 0; nb < 4; ++nb)
 #pragma unroll
