@@ -34,7 +34,14 @@ constexpr int kMaxTilesPerCta = SBG_SS_TPC;
 #ifndef SBG_SS_STAGES
 #define SBG_SS_STAGES 2
 #endif
-constexpr int SS_STAGES = SBG_SS_STAGES;  // X tiles in flight (3: P-row stages, the k padding rows alias the next buffer)  // column tiles per CTA: amortizes the per-K setup (pair list, A)
+constexpr int SS_STAGES = SBG_SS_STAGES;  // X tiles in flight (3: P-row stages, the k padding rows alias the next buffer)
+// bulk path, two stages: X tiles are announced on mbarriers by the threads' own cp.async completions
+// and handed back per warp, instead of one block barrier per tile (the three warps of a CTA may then
+// run up to a tile apart)
+#ifndef SBG_SS_MBAR
+#define SBG_SS_MBAR 1
+#endif
+constexpr bool SS_MBAR = SBG_SS_MBAR && SS_STAGES == 2;  // column tiles per CTA: amortizes the per-K setup (pair list, A)
 
 struct SsParams {
     const double* x;
@@ -63,7 +70,9 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
     k_sigma_ss(const SsParams p) {
     constexpr int KPP = KSS * 4;
     extern __shared__ __align__(16) double smem[];
-    double* Xs = smem;                        // [2][KPP][XSTRIDE]
+    uint64_t* mbF = reinterpret_cast<uint64_t*>(smem);  // [2] X stage landed, [2] X stage consumed
+    uint64_t* mbE = mbF + 2;
+    double* Xs = smem + 4;                    // [2][KPP][XSTRIDE]
     const int ysrows = max(KPP, 16 * (int)(blockDim.x >> 5));
     const int xstage = p.xrows * XSTRIDE;     // doubles per X stage
     double* Ys = Xs + SS_STAGES * xstage;     // [ysrows][YSTRIDE]
@@ -79,6 +88,13 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
     const uint64_t K = string_unrank(blockIdx.x, p.nel - 2, norb);
     const uint64_t full = ((uint64_t)1 << norb) - 1;
 
+    if (SS_MBAR && tid == 0) {
+        mbar_init(mbF, nthr);
+        mbar_init(mbF + 1, nthr);
+        mbar_init(mbE, nthr >> 5);
+        mbar_init(mbE + 1, nthr >> 5);
+        mbar_init_fence();
+    }
     for (int i = tid; i < KPP; i += nthr) {
         int J = -1, pi = 0;
         double phi = 0.0;
@@ -182,19 +198,35 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
             if (1 < nseq) load_next();
             cp_async_commit();
         }
+        uint32_t phF = 0, phE = 0;  // phase parity per X stage (landed / consumed)
+        if (SS_MBAR) cp_async_mbar_arrive_noinc(mbF);  // tile 0's gathers, issued above
         for (int tt = 0; tt < nseq; ++tt) {
             const int64_t c0 = c_begin + (int64_t)cu_t * NTS;
             double* const yv = p.yv[cu_v];
+            const int s = cu_s;
             const double* X = Xs + cu_s * xstage;
             if (++cu_t == ntt) {
                 cu_t = 0;
                 ++cu_v;
             }
             if (++cu_s == SS_STAGES) cu_s = 0;
-            cp_async_wait<SS_STAGES - 2>();
-            __syncthreads();  // X(tt) visible; every warp is done with X(tt-1), whose buffer the next load refills
-            if (tt + SS_STAGES - 1 < nseq) load_next();
-            cp_async_commit();
+            if (SS_MBAR) {
+                if (tt + 1 < nseq) {
+                    if (tt >= 1) {  // every warp has consumed tile tt-1, whose buffer tile tt+1 refills
+                        mbar_wait_parity(mbE + (s ^ 1), (phE >> (s ^ 1)) & 1u);
+                        phE ^= 1u << (s ^ 1);
+                    }
+                    load_next();
+                    cp_async_mbar_arrive_noinc(mbF + (s ^ 1));  // fires when this thread's chunks have landed
+                }
+                mbar_wait_parity(mbF + s, (phF >> s) & 1u);      // X(tt): every thread's chunks have landed
+                phF ^= 1u << s;
+            } else {
+                cp_async_wait<SS_STAGES - 2>();
+                __syncthreads();  // X(tt) visible; every warp is done with X(tt-1), whose buffer the next load refills
+                if (tt + SS_STAGES - 1 < nseq) load_next();
+                cp_async_commit();
+            }
             double acc[NTS / 8][4];
 #pragma unroll
             for (int nb = 0; nb < NTS / 8; ++nb)
@@ -214,6 +246,10 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
                 }
 #pragma unroll
                 for (int nb = 0; nb < NTS / 8; ++nb) dmma_16x8x4(acc[nb], a0[j], a1[j], bq[cur][nb]);
+            }
+            if (SS_MBAR) {  // this warp is done with X(tt)
+                __syncwarp();
+                if (lane == 0) mbar_arrive(mbE + s);
             }
             if (lane < 16) bulk_wait_read_all();  // this lane's previous row segment has been read
             __syncwarp();
@@ -452,7 +488,7 @@ SsPlan plan_sigma_ss(int norb, int nel) {
     const int KPP = pl.KSS * 4;
     const int rows = std::max(KPP, 16 * pl.warps);
     pl.xrows = SS_STAGES > 2 ? pl.P : KPP;
-    pl.smem = (size_t)(SS_STAGES * pl.xrows * XSTRIDE + rows * YSTRIDE) * 8 + (size_t)KPP * 8 * 5 + 16;
+    pl.smem = 32 + (size_t)(SS_STAGES * pl.xrows * XSTRIDE + rows * YSTRIDE) * 8 + (size_t)KPP * 8 * 5 + 16;
     // staged tiles reach y through TMA bulk reductions (cp.reduce.async.bulk .add.f64, one 256-byte
     // row segment per instruction); SBG_SS_BULK=0 keeps the per-lane red.global.add form
     const char* bulk_env = getenv("SBG_SS_BULK");
