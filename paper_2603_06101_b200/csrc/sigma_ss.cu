@@ -60,6 +60,7 @@ struct SsParams {
     const double* xv[kMaxSigmaVec];
     double* yv[kMaxSigmaVec];
     int xrows;  // rows per X stage (KPP, or P with three stages)
+    int mbar;   // bulk path: mbarrier-announced X tiles (long tile sequences) instead of a block barrier per tile
 };
 
 template <int KSS>
@@ -88,7 +89,8 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
     const uint64_t K = string_unrank(blockIdx.x, p.nel - 2, norb);
     const uint64_t full = ((uint64_t)1 << norb) - 1;
 
-    if (SS_MBAR && tid == 0) {
+    const bool use_mbar = SS_MBAR && p.mbar;
+    if (use_mbar && tid == 0) {
         mbar_init(mbF, nthr);
         mbar_init(mbF + 1, nthr);
         mbar_init(mbE, nthr >> 5);
@@ -199,7 +201,7 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
             cp_async_commit();
         }
         uint32_t phF = 0, phE = 0;  // phase parity per X stage (landed / consumed)
-        if (SS_MBAR) cp_async_mbar_arrive_noinc(mbF);  // tile 0's gathers, issued above
+        if (use_mbar) cp_async_mbar_arrive_noinc(mbF);  // tile 0's gathers, issued above
         for (int tt = 0; tt < nseq; ++tt) {
             const int64_t c0 = c_begin + (int64_t)cu_t * NTS;
             double* const yv = p.yv[cu_v];
@@ -210,7 +212,7 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
                 ++cu_v;
             }
             if (++cu_s == SS_STAGES) cu_s = 0;
-            if (SS_MBAR) {
+            if (use_mbar) {
                 if (tt + 1 < nseq) {
                     if (tt >= 1) {  // every warp has consumed tile tt-1, whose buffer tile tt+1 refills
                         mbar_wait_parity(mbE + (s ^ 1), (phE >> (s ^ 1)) & 1u);
@@ -247,7 +249,7 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
 #pragma unroll
                 for (int nb = 0; nb < NTS / 8; ++nb) dmma_16x8x4(acc[nb], a0[j], a1[j], bq[cur][nb]);
             }
-            if (SS_MBAR) {  // this warp is done with X(tt)
+            if (use_mbar) {  // this warp is done with X(tt)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(mbE + s);
             }
@@ -527,6 +529,10 @@ void launch_sigma_ss_multi(const SsPlan& pl, const double* const* xv, double* co
         throw InvalidArgument("sigma_ss: several vectors per launch need the bulk-reduction kernel");
     SsParams prm{x, y, Va, pl.norb, pl.nel, pl.P, pl.npa, ldx, col_lo, col_hi, tpc, ldy, ycol0, bulk, col_pad, nvec};
     prm.xrows = pl.xrows;
+    // long rows (c4: 128 tiles per CTA) gain from the decoupled warps (32.3 -> 31.4 ms per sigma), short
+    // tile sequences lose (c3: 1.67 -> 1.73 ms, c2: 0.116 -> 0.123 ms); SBG_SS_MBAR=0/1 forces either
+    prm.mbar = ntiles >= 256;
+    if (const char* e = getenv("SBG_SS_MBAR")) prm.mbar = atoi(e) != 0;
     for (int v = 0; v < nvec; ++v) {
         prm.xv[v] = xv[v];
         prm.yv[v] = yvs[v];
