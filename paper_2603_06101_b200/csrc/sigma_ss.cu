@@ -201,6 +201,7 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
             cp_async_commit();
         }
         uint32_t phF = 0, phE = 0;  // phase parity per X stage (landed / consumed)
+        const int oX = t * XSTRIDE + g, oY = i0 * YSTRIDE + 2 * t;  // lane offsets into an X tile / the staging tile
         if (use_mbar) cp_async_mbar_arrive_noinc(mbF);  // tile 0's gathers, issued above
         for (int tt = 0; tt < nseq; ++tt) {
             const int64_t c0 = c_begin + (int64_t)cu_t * NTS;
@@ -238,13 +239,13 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
             // DMMAs of step j issue
             double bq[2][NTS / 8];
 #pragma unroll
-            for (int nb = 0; nb < NTS / 8; ++nb) bq[0][nb] = X[t * XSTRIDE + g + nb * 8];
+            for (int nb = 0; nb < NTS / 8; ++nb) bq[0][nb] = X[oX + nb * 8];
 #pragma unroll
             for (int j = 0; j < KSS; ++j) {
                 const int cur = j & 1;
                 if (j + 1 < KSS) {
 #pragma unroll
-                    for (int nb = 0; nb < NTS / 8; ++nb) bq[cur ^ 1][nb] = X[(4 * (j + 1) + t) * XSTRIDE + g + nb * 8];
+                    for (int nb = 0; nb < NTS / 8; ++nb) bq[cur ^ 1][nb] = X[oX + 4 * (j + 1) * XSTRIDE + nb * 8];
                 }
 #pragma unroll
                 for (int nb = 0; nb < NTS / 8; ++nb) dmma_16x8x4(acc[nb], a0[j], a1[j], bq[cur][nb]);
@@ -257,9 +258,8 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
             __syncwarp();
 #pragma unroll
             for (int nb = 0; nb < NTS / 8; ++nb) {
-                const int col = nb * 8 + 2 * t;
-                *reinterpret_cast<double2*>(Ys + i0 * YSTRIDE + col) = make_double2(acc[nb][0], acc[nb][1]);
-                *reinterpret_cast<double2*>(Ys + (i0 + 8) * YSTRIDE + col) = make_double2(acc[nb][2], acc[nb][3]);
+                *reinterpret_cast<double2*>(Ys + oY + nb * 8) = make_double2(acc[nb][0], acc[nb][1]);
+                *reinterpret_cast<double2*>(Ys + oY + 8 * YSTRIDE + nb * 8) = make_double2(acc[nb][2], acc[nb][3]);
             }
             const bool whole = c0 >= p.col_lo && c0 + NTS <= full_end;
             if (whole) {
