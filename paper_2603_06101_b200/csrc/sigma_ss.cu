@@ -41,7 +41,7 @@ constexpr int SS_STAGES = SBG_SS_STAGES;  // X tiles in flight (3: P-row stages,
 #ifndef SBG_SS_MBAR
 #define SBG_SS_MBAR 1
 #endif
-constexpr bool SS_MBAR = SBG_SS_MBAR && SS_STAGES == 2;  // column tiles per CTA: amortizes the per-K setup (pair list, A)
+constexpr bool SS_MBAR = SBG_SS_MBAR != 0;  // column tiles per CTA: amortizes the per-K setup (pair list, A)
 
 struct SsParams {
     const double* x;
@@ -71,9 +71,9 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
     k_sigma_ss(const SsParams p) {
     constexpr int KPP = KSS * 4;
     extern __shared__ __align__(16) double smem[];
-    uint64_t* mbF = reinterpret_cast<uint64_t*>(smem);  // [2] X stage landed, [2] X stage consumed
-    uint64_t* mbE = mbF + 2;
-    double* Xs = smem + 4;                    // [2][KPP][XSTRIDE]
+    uint64_t* mbF = reinterpret_cast<uint64_t*>(smem);  // [stages] X stage landed, [stages] X stage consumed
+    uint64_t* mbE = mbF + SS_STAGES;
+    double* Xs = smem + 8;                    // [stages][xrows][XSTRIDE]
     const int ysrows = max(KPP, 16 * (int)(blockDim.x >> 5));
     const int xstage = p.xrows * XSTRIDE;     // doubles per X stage
     double* Ys = Xs + SS_STAGES * xstage;     // [ysrows][YSTRIDE]
@@ -91,10 +91,10 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
 
     const bool use_mbar = SS_MBAR && p.mbar;
     if (use_mbar && tid == 0) {
-        mbar_init(mbF, nthr);
-        mbar_init(mbF + 1, nthr);
-        mbar_init(mbE, nthr >> 5);
-        mbar_init(mbE + 1, nthr >> 5);
+        for (int i = 0; i < SS_STAGES; ++i) {
+            mbar_init(mbF + i, nthr);
+            mbar_init(mbE + i, nthr >> 5);
+        }
         mbar_init_fence();
     }
     for (int i = tid; i < KPP; i += nthr) {
@@ -196,13 +196,14 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
             }
             if (++ld_s == SS_STAGES) ld_s = 0;
         };
-        if (SS_STAGES > 2) {
-            if (1 < nseq) load_next();
-            cp_async_commit();
-        }
         uint32_t phF = 0, phE = 0;  // phase parity per X stage (landed / consumed)
         const int oX = t * XSTRIDE + g, oY = i0 * YSTRIDE + 2 * t;  // lane offsets into an X tile / the staging tile
         if (use_mbar) cp_async_mbar_arrive_noinc(mbF);  // tile 0's gathers, issued above
+        if (SS_STAGES > 2) {  // tile 1 as well: the ring runs SS_STAGES - 1 tiles ahead
+            if (1 < nseq) load_next();
+            if (use_mbar) cp_async_mbar_arrive_noinc(mbF + 1);
+            cp_async_commit();
+        }
         for (int tt = 0; tt < nseq; ++tt) {
             const int64_t c0 = c_begin + (int64_t)cu_t * NTS;
             double* const yv = p.yv[cu_v];
@@ -214,13 +215,14 @@ __global__ void __launch_bounds__(KSS > 24 ? 256 : (KSS > 16 ? 192 : 128), KSS >
             }
             if (++cu_s == SS_STAGES) cu_s = 0;
             if (use_mbar) {
-                if (tt + 1 < nseq) {
-                    if (tt >= 1) {  // every warp has consumed tile tt-1, whose buffer tile tt+1 refills
-                        mbar_wait_parity(mbE + (s ^ 1), (phE >> (s ^ 1)) & 1u);
-                        phE ^= 1u << (s ^ 1);
+                if (tt + SS_STAGES - 1 < nseq) {
+                    const int sn = ld_s;  // stage of tile tt + SS_STAGES - 1 = the stage tile tt - 1 used
+                    if (tt >= 1) {  // every warp has consumed tile tt-1
+                        mbar_wait_parity(mbE + sn, (phE >> sn) & 1u);
+                        phE ^= 1u << sn;
                     }
                     load_next();
-                    cp_async_mbar_arrive_noinc(mbF + (s ^ 1));  // fires when this thread's chunks have landed
+                    cp_async_mbar_arrive_noinc(mbF + sn);  // fires when this thread's chunks have landed
                 }
                 mbar_wait_parity(mbF + s, (phF >> s) & 1u);      // X(tt): every thread's chunks have landed
                 phF ^= 1u << s;
@@ -490,7 +492,7 @@ SsPlan plan_sigma_ss(int norb, int nel) {
     const int KPP = pl.KSS * 4;
     const int rows = std::max(KPP, 16 * pl.warps);
     pl.xrows = SS_STAGES > 2 ? pl.P : KPP;
-    pl.smem = 32 + (size_t)(SS_STAGES * pl.xrows * XSTRIDE + rows * YSTRIDE) * 8 + (size_t)KPP * 8 * 5 + 16;
+    pl.smem = 64 + (size_t)(SS_STAGES * pl.xrows * XSTRIDE + rows * YSTRIDE) * 8 + (size_t)KPP * 8 * 5 + 16;
     // staged tiles reach y through TMA bulk reductions (cp.reduce.async.bulk .add.f64, one 256-byte
     // row segment per instruction); SBG_SS_BULK=0 keeps the per-lane red.global.add form
     const char* bulk_env = getenv("SBG_SS_BULK");
