@@ -297,6 +297,12 @@ __device__ __forceinline__ void bar_arrive(int id, int n) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 constexpr int kWsThreads = 512, kWsHalf = 256;
+#ifndef SBG_XS_WAITG
+#define SBG_XS_WAITG 4   // uniform stream: k-steps between the G hand-back wait and the end of the tile
+#endif
+#ifndef SBG_TALL_WAITG
+#define SBG_TALL_WAITG 3   // TALL kernel, warps 0-3 (c3: 4.57 / 4.54 / 4.50 / 4.54 / 4.58 ms for 1 / 2 / 3 / 4 / 6)
+#endif
 // The SBG_AB_DEBUG timing experiments (skip the scatter / the DMMAs / the gathers / every hand-off)
 // are compiled into k_sigma_ab_ws only with -DSBG_AB_DEBUG_SWITCHES (tools/ab_variant.sh): every
 // instruction in the DMMA warps' tile loop costs tensor-pipe time.
@@ -534,7 +540,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
 #pragma unroll
                         for (int j = 0; j < KS; ++j) {
                             const int cur = j & 1;
-                            if (j == KS - 1) wait_g(it);
+                            if (j == (KS > SBG_TALL_WAITG ? KS - SBG_TALL_WAITG : 0)) wait_g(it);
                             if (j + 1 < KS) {
                                 q[cur ^ 1][0] = *reinterpret_cast<const double2*>(pB + 4 * (j + 1) * DSTRIDE);
                                 q[cur ^ 1][1] = *reinterpret_cast<const double2*>(pB + 4 * (j + 1) * DSTRIDE + 16);
@@ -638,19 +644,30 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_sigma_ab_ws(const AbParams p)
 #pragma unroll
                             for (int i = 0; i < KS; ++i) {
                                 const int cur = i & 1;
-                                if (i == KS - 1) wait_g(it);  // G buffer b is written from here on
+                                // G buffer b is needed after the last k-step; the wait sits WG k-steps earlier: its
+                                // position steers the schedule ptxas builds around it (c4, KS = 17: 92.2 / 92.4 /
+                                // 91.2 / 90.4 / 91.3 / 91.0 / 91.5 ms for 1 / 2 / 3 / 4 / 5 / 6 / 8 k-steps)
+                                constexpr int WG = KS > SBG_XS_WAITG ? KS - SBG_XS_WAITG : 0;
+                                if (i == WG) wait_g(it);
                                 if (i + 1 < KS) {
                                     constexpr int STEP = 4 * DSTRIDE * 8;
                                     q[cur ^ 1][0] = *reinterpret_cast<const double2*>(((i + 1 < KH) ? pLo01 : pHi01) + (i + 1) * STEP);
                                     q[cur ^ 1][1] = *reinterpret_cast<const double2*>(((i + 1 < KH) ? pLo23 : pHi23) + (i + 1) * STEP);
                                 }
+#ifdef SBG_XS_EXTRA_FIRST
+                                if constexpr (XS == 2) {
+                                    if (i < KH) dmma_8x8x4(acx, aer[i], XODD ? q[cur][0].y : q[cur][0].x);
+                                }
+#endif
                                 dmma_16x8x4(acc[0], a0[i], a1[i], q[cur][0].x);
                                 dmma_16x8x4(acc[1], a0[i], a1[i], q[cur][0].y);
                                 dmma_16x8x4(acc[2], a0[i], a1[i], q[cur][1].x);
                                 dmma_16x8x4(acc[3], a0[i], a1[i], q[cur][1].y);
+#ifndef SBG_XS_EXTRA_FIRST
                                 if constexpr (XS == 2) {
                                     if (i < KH) dmma_8x8x4(acx, aer[i], XODD ? q[cur][0].y : q[cur][0].x);
                                 }
+#endif
                             }
                             // epilogue: column of acc[L][e] = (L < 2 ? c01 : c23) + 4 t + 2 (e & 1) + (L & 1),
                             // rows g (e < 2) and g + 8; the k = 0 rank-1 term (K0E) first
